@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""bench.py -- FMM matvec throughput on B200 (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+One "step" = one full Helmholtz FMM matvec y = A q (all hot-path rows: permute, S2M, M2M,
+M2L, L2L, L2T, P2P, combine) on BASELINE config 3 ("C4": N = 1e6 points on the unit sphere,
+kappa = 32 pi, depth 7, eps = 1e-8, seed 2) with q resident in HBM.  `e2e` repeats the
+measurement through the public host-pointer API (pinned q in, y out, copies inside the timed
+region).  Multi-GPU (torchrun): strong scaling, max over ranks.
+
+--impl reference: the CPU oracle (oracle/, plain numpy) timed on a bounded sample of the
+same workload and extrapolated to one matvec (the reported baseline; not the target).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# FP64 flops of one P2P pair as implemented: difference 3,
+# r^2 5, rsqrt 6, r and kappa r 2, e^{ix} 26 (Cody-Waite + table + degree-7/6 polynomials),
+# 1/r scaling 2, complex MAC 8.
+P2P_FLOPS_PER_PAIR = 52
+S2M_FLOPS_PER_EVAL = 40      # phase 5 + e^{ix} 26 + complex MAC 8 (+1 scale)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max(float(r[3]) for r in self.rows) if self.rows else None}
+
+
+# ------------------------------------------------------------------------------------------
+def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
+    """Time the CPU oracle (as it stands) on a bounded sample of one matvec and extrapolate.
+
+    Sample: S2M, L2T and P2P on `budget_leaves` far-field leaves, M2M / L2L on 2 children per
+    level, M2L on 2 target boxes per level; each term is scaled by its unit count (points x
+    directions, pairs, children, interaction-list entries).  Returns (seconds per matvec,
+    description, cores)."""
+    from threadpoolctl import threadpool_limits
+    from oracle.plan import make_plan
+    from oracle.fmm import OracleFMM
+    from oracle.tree import interaction_list, neighbours
+    with threadpool_limits(1):
+        plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+        f = OracleFMM(x, cfg.lo, cfg.size, plan)
+        rng = np.random.default_rng(seed)
+        total = 0.0
+        desc = []
+        if plan.L_f is None:
+            t = rng.choice(len(x), size=min(len(x), 200), replace=False)
+            t0 = time.perf_counter()
+            f.p2p(q, t)
+            dt = time.perf_counter() - t0
+            total = dt * len(x) / len(t)
+            return total, f"direct sum for {len(t)} sampled targets, x{len(x) / len(t):.0f}", 1
+        L = plan.L_f
+        lev = f.levels[L]
+        leaves = rng.choice(len(lev.boxes), size=min(budget_leaves, len(lev.boxes)), replace=False)
+        pts = np.concatenate([lev.members[b] for b in leaves])
+        # S2M
+        t0 = time.perf_counter()
+        f.s2m(q, boxes=list(leaves))
+        ts2m = (time.perf_counter() - t0) * len(x) / len(pts)
+        # P2P (pairs-weighted)
+        pairs_s = sum(len(lev.members[b]) * sum(len(lev.members[c]) for c in neighbours(lev, lev.boxes[b]))
+                      for b in leaves)
+        pairs_all = sum(len(lev.members[b]) * sum(len(lev.members[c]) for c in neighbours(lev, lev.boxes[b]))
+                        for b in range(len(lev.boxes)))
+        t0 = time.perf_counter()
+        f.p2p(q, pts)
+        tp2p = (time.perf_counter() - t0) * pairs_all / pairs_s
+        # L2T with a random local field
+        Kf = plan.levels[L].K
+        Lf = {b: rng.standard_normal(Kf) + 1j * rng.standard_normal(Kf) for b in leaves}
+        t0 = time.perf_counter()
+        f.l2t(Lf, pts)
+        tl2t = (time.perf_counter() - t0) * len(x) / len(pts)
+        # M2M / M2L / L2L per level with random fields
+        tmid = 0.0
+        for l in range(2, L + 1):
+            K = plan.levels[l].K
+            levl = f.levels[l]
+            M = {b: rng.standard_normal(K) + 1j * rng.standard_normal(K) for b in range(len(levl.boxes))}
+            tg = list(range(min(2, len(levl.boxes))))
+            nnz_s = sum(len(interaction_list(levl, levl.boxes[a])) for a in tg)
+            nnz = sum(len(interaction_list(levl, levl.boxes[a])) for a in range(len(levl.boxes)))
+            t0 = time.perf_counter()
+            f.m2l(M, l, targets=tg)
+            tmid += (time.perf_counter() - t0) * nnz / max(nnz_s, 1)
+            if l > 2:
+                sub = {b: M[b] for b in list(M)[:2]}
+                t0 = time.perf_counter()
+                f.m2m(sub, l)
+                tmid += (time.perf_counter() - t0) * len(levl.boxes) / 2
+                Kp = plan.levels[l - 1].K
+                Lp = {p: rng.standard_normal(Kp) + 1j * rng.standard_normal(Kp) for p in range(len(f.levels[l - 1].boxes))}
+                t0 = time.perf_counter()
+                f.l2l(Lp, {c: M[c] for c in list(M)[:2]}, l - 1)
+                tmid += (time.perf_counter() - t0) * len(levl.boxes) / 2
+        total = ts2m + tp2p + tl2t + tmid
+        desc = (f"oracle passes on {len(leaves)} of {len(lev.boxes)} far-field leaves ({len(pts)} points: S2M, "
+                f"L2T, P2P), M2L on 2 boxes/level, M2M+L2L on 2 children/level; each term scaled by its unit count")
+        return total, desc, 1
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle, each step a bounded sample, on rank 0 only."""
+    if rank != 0:
+        return
+    from workloads import points_and_charges
+    x, q = points_and_charges(cfg)
+    for _ in range(args.warmup):
+        oracle_sample(cfg, x, q, budget_leaves=1)
+    secs = []
+    desc = ""
+    for k in range(args.steps):
+        s, desc, cores = oracle_sample(cfg, x, q, budget_leaves=1, seed=k)
+        secs.append(s)
+    t = statistics.mean(secs)
+    line = {"metric": "FMM matvecs/s", "value": 1.0 / t, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps,
+                       "seed": cfg.seed, "geometry": cfg.kind},
+            "impl": "reference",
+            "cpu_baseline": {"value": 1.0 / t, "unit": "matvec/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": 1.0 / t, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from workloads import CONFIGS, points_and_charges
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    os.environ["HFMM_PROFILE_STAGES"] = "1"
+    import torch
+    import paper_0911_4114_b200 as hf
+    from paper_0911_4114_b200.build import build
+    if rank == 0:
+        build(verbose=False)
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.barrier()
+    x, q = points_and_charges(cfg)
+    g = hf.HFMM(local_rank)
+    if world > 1:
+        uid = hf.nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, 0)
+        g.set_dist(rank, world, bytes(t.cpu().tolist()))
+    t0 = time.perf_counter()
+    g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+    t_tree = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha)
+    t_pre = time.perf_counter() - t0
+    info = g.info()
+    stream = torch.cuda.current_stream()
+    qd = torch.from_numpy(q).cuda()
+    yd = torch.empty_like(qd)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    local = world > 1
+    for _ in range(args.warmup):
+        g.matvec(qd, out=yd, local=local)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    step_ms, stage = [], {k: [] for k in ("s2m", "m2m", "m2l", "l2l", "l2t", "p2p")}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        flush.zero_()                      # L2 flush between timed iterations (untimed)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        g.matvec(qd, out=yd, local=local)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        st = g.stage_times()
+        for k in stage:
+            stage[k].append(st[k])
+    clocks = sampler.stop()
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = tot.item() / args.steps
+    # end to end through the public host-pointer API (pinned host q, y; copies timed)
+    qh = torch.from_numpy(q).pin_memory()
+    yh = torch.empty_like(qh).pin_memory()
+    e2e_ms = []
+    for _ in range(max(2, args.steps // 2)):
+        flush.zero_()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        g.matvec(qh, out=yh, stream=stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # P2P roofline (dominant kernel): algorithmic FP64 flops / measured duration
+    p2p_ms = statistics.mean(stage["p2p"])
+    pairs = info["p2p_pairs"]
+    peak_tflops = 2 * 64 * 148 * (clocks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
+    achieved = P2P_FLOPS_PER_PAIR * pairs / (p2p_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cfg.name, {}).get("p2p")
+        except Exception:
+            traffic = None
+    L_f = info["L_f"]
+    launches = 3 + (0 if L_f is None else (1 + 2 * (L_f - 2) + (L_f - 1) + 2 * (L_f - 2) + 1))
+    line = {
+        "metric": "FMM matvecs/s", "value": 1e3 / ms, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps,
+                   "seed": cfg.seed, "geometry": cfg.kind, "L_f": L_f, "l2": "flushed (512 MB write) between steps",
+                   "parallelism": f"octree level-2 subtrees x{world}"},
+        "mpoints_per_s": cfg.n * 1e3 / ms / 1e6,
+        "e2e": {"value": 1e3 / te.item(), "unit": "matvec/s", "h2d_bytes_per_step": cfg.n * 16,
+                "d2h_bytes_per_step": cfg.n * 16},
+        "gpu_launches": launches,
+        "roofline": {"kernel": "p2p", "bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tflops, "traffic": traffic,
+                     "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 2 x sm_max_mhz (DESIGN.md)",
+                     "per_unit": f"{P2P_FLOPS_PER_PAIR} FP64 flops per ordered pair", "units_per_launch": pairs},
+        "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
+        "plan": {"levels": [{k: lv[k] for k in ("level", "ell", "n_theta", "n_phi", "F", "active")}
+                            for lv in info["levels"]], "p2p_pairs": pairs, "s2m_evals": info["s2m_evals"]},
+        "setup_s": {"build_tree": t_tree, "precompute": t_pre},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, desc, cores = oracle_sample(cfg, x, q)
+        line["cpu_baseline"] = {"value": 1.0 / s, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.json_out:
+            json.dump(line, open(args.json_out, "w"), indent=1)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

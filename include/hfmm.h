@@ -1,0 +1,190 @@
+/*
+ * hfmm.h -- C ABI of libhfmm, a B200 (sm_100a) implementation of the Fourier-basis
+ * Helmholtz fast multipole matrix-vector product of Cecka & Darve (arXiv 0911.4114).
+ *
+ * Citations "P:n" are line numbers of /root/reference/PAPER.md (the paper's LaTeX source).
+ *
+ * The operation (eqn:HelmholtzMatrixVector):
+ *
+ *     y_i = sum_{j != i} exp(i kappa |x_i - x_j|) / |x_i - x_j| * q_j ,   i = 0..n-1
+ *
+ * (no 1/(4 pi) factor; the self term is excluded), evaluated by the FMM of P:114-138:
+ * S2M at the far-field leaf level, M2M with FFT interpolation,
+ * diagonal M2L with the bandlimited modified transfer function of Alg. 1 (P:123-127,
+ * P:508-530), L2L with FFT anterpolation, L2T + P2P near field
+ * (eqn:FMM_FinalStep).
+ *
+ * Conventions
+ *   - complex numbers are interleaved float64 pairs (re, im), i.e. C99 double _Complex /
+ *     numpy complex128 / torch.complex128 memory layout;
+ *   - positions are row-major n x 3 float64 (x0 y0 z0 x1 y1 z1 ...);
+ *   - every array argument is owned by the caller; the library copies what it keeps;
+ *   - a plan is NOT thread-safe; distinct plans are independent;
+ *   - state machine: create -> build_tree -> precompute -> matvec*; build_tree again
+ *     invalidates the precompute (HFMM_E_STATE if matvec is called too early);
+ *   - return value: 0 success, > 0 warning (result still valid), < 0 error; the message
+ *     of the last non-zero return is available from hfmm_last_error(plan).
+ *
+ * Multi-GPU: call hfmm_set_dist() between create and build_tree; every rank then calls
+ * every function collectively with identical arguments (inputs replicated).  Each rank
+ * computes the far field and near field of the level-2 subtrees it owns (Morton-ordered
+ * partition weighted by work); multipole expansions of every active level are
+ * all-gathered with NCCL over NVLink before M2L; y is all-gathered at the end unless
+ * HFMM_Y_LOCAL is set (then only owned entries of y are written, others are zero).
+ */
+#ifndef HFMM_H
+#define HFMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes -------------------------------------------------------------------- */
+#define HFMM_OK 0
+#define HFMM_W_BREAKDOWN 1    /* some levels inadmissible (L_f < depth)            */
+#define HFMM_W_NO_FARFIELD 2  /* no admissible level: the matvec is the direct sum         */
+#define HFMM_E_ARG (-1)       /* bad argument: n <= 0, depth < 2, kappa <= 0, eps not in
+                                 (0,1), alpha not in (0,1], non-finite input, NULL pointer */
+#define HFMM_E_DOMAIN (-2)    /* a point lies outside the root cube                         */
+#define HFMM_E_COINCIDENT (-3) /* two distinct points coincide (kernel undefined at R = 0) */
+#define HFMM_E_SEARCH (-4)    /* no ell / N_theta / N_phi within the search limits (Algs 2-3)*/
+#define HFMM_E_STATE (-5)     /* call out of order                                          */
+#define HFMM_E_NOMEM (-6)     /* device or host allocation failed                           */
+#define HFMM_E_CUDA (-7)      /* CUDA runtime error (message has the CUDA error string)     */
+#define HFMM_E_NCCL (-8)      /* NCCL error                                                 */
+
+/* ---- precompute flags ---------------------------------------------------------------- */
+#define HFMM_EPS_ABSOLUTE 0x1u     /* use eps itself at every level (default eps/a_l)        */
+#define HFMM_FORCE_ALL_LEVELS 0x2u /* run M2L at every level 2..depth regardless of F_l
+                                      (low-frequency breakdown demonstration)        */
+
+/* ---- matvec memory kinds -------------------------------------------------------------- */
+#define HFMM_HOST 0    /* q and y are host pointers (pinned or pageable)                     */
+#define HFMM_DEVICE 1  /* q and y are device pointers on the plan's device                   */
+#define HFMM_Y_LOCAL 2 /* OR-able with the above: multi-GPU, skip the final y all-gather     */
+
+#define HFMM_MAX_LEVELS 16
+
+typedef struct hfmm_plan hfmm_plan; /* opaque; owns all device memory and the NCCL comm */
+
+typedef struct {
+  int level;        /* l (box size a_l = a_0 / 2^l)                                  */
+  double a;         /* a_l                                                                 */
+  int ell;          /* Gegenbauer truncation                                   */
+  int n_theta;      /* N_theta (Alg. 2), even, 7-smooth                         */
+  int n_phi;        /* N_phi (Alg. 3), multiple of 4, 7-smooth                  */
+  int64_t K;        /* stored quadrature points N_theta * N_phi / 2            */
+  double F;         /* roundoff amplification 8 pi u a_l max|T_l| (NaN if not evaluated)    */
+  int active;       /* 1 if M2L runs at this level                                         */
+  int64_t boxes;    /* occupied boxes at this level                                        */
+  int64_t m2l_pairs;/* interaction-list entries at this level (all ranks)                  */
+} hfmm_level_info;
+
+typedef struct {
+  int64_t n;               /* points                                                       */
+  int depth;               /* configured depth D                                           */
+  int L_f;                 /* far-field leaf level, or -1 if no admissible level             */
+  double kappa, eps, alpha, tau;
+  int nlevels;             /* entries filled in level[] (levels 2..D)                        */
+  hfmm_level_info level[HFMM_MAX_LEVELS];
+  int64_t p2p_pairs;       /* ordered near-field pairs (incl. self pairs skipped)            */
+  int64_t s2m_evals;       /* points x directions at L_f                                    */
+  int rank, nranks;
+  int64_t owned_points;    /* points whose y this rank computes                              */
+} hfmm_info;
+
+/* Create a plan on CUDA device `device` (-1: the current device).  *out receives the plan. */
+int hfmm_create(hfmm_plan **out, int device);
+
+/* Multi-GPU: rank / nranks and the 128-byte ncclUniqueId (broadcast by the caller, e.g. with
+ * torch.distributed).  nranks == 1 (default) disables all collectives. */
+int hfmm_set_dist(hfmm_plan *p, int rank, int nranks, const void *nccl_unique_id_128b);
+
+/* Fill out_128b with a fresh ncclUniqueId (rank 0 calls this and broadcasts the bytes). */
+int hfmm_nccl_unique_id(void *out_128b);
+
+/* Octree over n points.  xyz: HOST pointer, n x 3 row-major float64.  depth >= 2 is the
+ * configured leaf level D (root level 0); root cube [lo, lo + size]^3 must contain every point
+ * (HFMM_E_DOMAIN otherwise).  Box coordinate b = min(floor((x - lo) / a_l), 2^l - 1).
+ * Detects exactly coincident points (HFMM_E_COINCIDENT).  Copies xyz to the device. */
+int hfmm_build_tree(hfmm_plan *p, int64_t n, const double *xyz, int depth,
+                    const double lo[3], double size);
+
+/* Plan for wavenumber kappa > 0 and target accuracy eps in (0,1): per level ell (EBF +
+ * Carayol-Collino), N_theta (Alg. 2), N_phi (Alg. 3), the 316 bandlimited modified
+ * transfer tables (Alg. 1, computed on the GPU), F_l and the far-field leaf level L_f (deepest
+ * level with F_2..F_l <= tau).  alpha in (0,1] scales the design radius |r| = alpha sqrt(3) a_l
+ * (0.8 in the paper's error studies).  tau <= 0 selects min(eps/10, 1e-9).
+ * Returns HFMM_W_BREAKDOWN / HFMM_W_NO_FARFIELD as warnings. */
+int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double alpha, double tau,
+                    unsigned flags);
+
+/* y = A q (eqn:HelmholtzMatrixVector).  q: n complex128 in INPUT order, y: n complex128 in
+ * input order.  mem = HFMM_HOST or HFMM_DEVICE (optionally | HFMM_Y_LOCAL).  stream: a
+ * cudaStream_t on the plan's device, or NULL for the plan's own stream.  For HFMM_HOST the
+ * call returns after y is written; for HFMM_DEVICE it returns after enqueueing (y valid once
+ * `stream` completes). */
+int hfmm_matvec(hfmm_plan *p, const double *q, double *y, int mem, void *stream);
+
+/* Direct O(n^2) sum on the GPU (same P2P kernel over all pairs), same conventions. */
+int hfmm_direct(hfmm_plan *p, const double *q, double *y, int mem, void *stream);
+
+/* Plan summary (valid after precompute). */
+int hfmm_get_info(const hfmm_plan *p, hfmm_info *info);
+
+/* Device timing of the stages of the last matvec in milliseconds (CUDA events on the
+ * launching streams): out[0] S2M, [1] M2M, [2] M2L, [3] L2L, [4] L2T, [5] P2P, [6] total.
+ * Only filled when HFMM_PROFILE_STAGES is set in the environment. */
+int hfmm_stage_times(const hfmm_plan *p, double out[8]);
+
+/* Copy a stage buffer of the last matvec to host memory (testing and validation).
+ * what: 0 M_l, 1 I_l (incoming), 2 L_l (local), 3 T_l (transfer tables [316][K_l]),
+ *       4 y_near (sorted order), 5 y_far (sorted order), 6 permutation (int64, sorted -> input),
+ *       7 box table of level l (int64 [boxes][4]: ix, iy, iz, first point),
+ * level: tree level l.  nbytes: capacity of host_out.  Returns the bytes needed in *needed. */
+int hfmm_debug_copy(const hfmm_plan *p, int what, int level, void *host_out, int64_t nbytes,
+                    int64_t *needed);
+
+/* Message of the last non-zero return of any call on p (or of hfmm_create if p is NULL). */
+const char *hfmm_last_error(const hfmm_plan *p);
+
+/* Free everything owned by the plan, including the NCCL communicator. */
+void hfmm_destroy(hfmm_plan *p);
+
+/* ---- host-only plan helpers (no GPU needed) ---------------------------------------------
+ * The per-level quadrature of P:140-722 for box size a: returns ell, N_theta, N_phi
+ * (rectangular, 7-smooth) and fills ragged[0..N_theta/2] with Alg. 3's per-row N_phi(theta_n)
+ * when ragged != NULL (capacity ragged_cap).  eps is the level's absolute target. */
+int hfmm_level_quadrature(double kappa, double a, double eps_level, double alpha, int *ell,
+                          int *n_theta, int *n_phi, int *ragged, int ragged_cap);
+
+/* ---- operator entry points (microbench, BASELINE config 2; device pointers) -----------------
+ * Batched 5-step Fourier resampling of `nbatch` half-stored fields
+ * [n_theta][n_phi/2] -> [n_theta2][n_phi2/2]: interpolation if the target grid
+ * is larger, anterpolation if smaller.  in/out: device complex128.  work: device scratch of
+ * hfmm_resample_workspace() bytes (NULL: allocated internally per call). */
+int64_t hfmm_resample_workspace(int nbatch, int n_theta, int n_phi, int n_theta2, int n_phi2);
+int hfmm_resample(int nbatch, int n_theta, int n_phi, int n_theta2, int n_phi2, const double *in,
+                  double *out, void *work, void *stream);
+
+/* Fused M2M of 8 children per parent (interpolate, multiply by shift[octant][K_parent],
+ * accumulate): children [nparent*8][K_child] -> parents [nparent][K_parent]. */
+int hfmm_m2m_op(int nparent, int n_theta, int n_phi, int n_theta2, int n_phi2, const double *child,
+                const double *shift, double *parent, void *work, void *stream);
+
+/* Fused L2L: child_out[c] = anterp(conj(shift[c % 8]) * parent[c / 8]) + incoming[c]. */
+int hfmm_l2l_op(int nparent, int n_theta, int n_phi, int n_theta2, int n_phi2,
+                const double *parent, const double *shift, const double *incoming,
+                double *child_out, void *work, void *stream);
+
+/* Diagonal M2L over a CSR interaction list: out[a][k] = sum_e T[oid[e]][k] * M[src[e]][k] for
+ * e in [row[a], row[a+1]).  row: int32 [nbox+1], src: int32, oid: int32 (0..315). */
+int hfmm_m2l_op(int nbox, int64_t K, const int *row, const int *src, const int *oid,
+                const double *T, const double *M, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFMM_H */

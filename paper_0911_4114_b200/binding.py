@@ -1,0 +1,275 @@
+"""Thin ctypes binding of libhfmm (include/hfmm.h): argument marshalling only.
+
+Every step of the matvec runs in libhfmm's CUDA kernels; this module never computes any
+part of the method.  There is no CPU fallback: if libhfmm.so is missing or no GPU is
+present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhfmm.so")
+
+HFMM_OK = 0
+HFMM_W_BREAKDOWN = 1
+HFMM_W_NO_FARFIELD = 2
+HFMM_EPS_ABSOLUTE = 0x1
+HFMM_FORCE_ALL_LEVELS = 0x2
+HFMM_HOST = 0
+HFMM_DEVICE = 1
+HFMM_Y_LOCAL = 2
+MAX_LEVELS = 16
+
+EXPORTED = [
+    "hfmm_create", "hfmm_set_dist", "hfmm_nccl_unique_id", "hfmm_build_tree", "hfmm_precompute", "hfmm_matvec",
+    "hfmm_direct", "hfmm_get_info", "hfmm_stage_times", "hfmm_debug_copy", "hfmm_last_error",
+    "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
+    "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op",
+]
+
+
+class LevelInfo(C.Structure):
+    _fields_ = [("level", C.c_int), ("a", C.c_double), ("ell", C.c_int), ("n_theta", C.c_int),
+                ("n_phi", C.c_int), ("K", C.c_int64), ("F", C.c_double), ("active", C.c_int),
+                ("boxes", C.c_int64), ("m2l_pairs", C.c_int64)]
+
+
+class Info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("depth", C.c_int), ("L_f", C.c_int), ("kappa", C.c_double),
+                ("eps", C.c_double), ("alpha", C.c_double), ("tau", C.c_double), ("nlevels", C.c_int),
+                ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("s2m_evals", C.c_int64),
+                ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64)]
+
+
+class HFMMError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libhfmm error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libhfmm.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                          "(python -m paper_0911_4114_b200.build); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    vp, i64, dbl, ci = C.c_void_p, C.c_int64, C.c_double, C.c_int
+    sig = {
+        "hfmm_create": (ci, [C.POINTER(vp), ci]),
+        "hfmm_set_dist": (ci, [vp, ci, ci, C.c_char_p]),
+        "hfmm_nccl_unique_id": (ci, [vp]),
+        "hfmm_build_tree": (ci, [vp, i64, vp, ci, vp, dbl]),
+        "hfmm_precompute": (ci, [vp, dbl, dbl, dbl, dbl, C.c_uint]),
+        "hfmm_matvec": (ci, [vp, vp, vp, ci, vp]),
+        "hfmm_direct": (ci, [vp, vp, vp, ci, vp]),
+        "hfmm_get_info": (ci, [vp, C.POINTER(Info)]),
+        "hfmm_stage_times": (ci, [vp, vp]),
+        "hfmm_debug_copy": (ci, [vp, ci, ci, vp, i64, C.POINTER(i64)]),
+        "hfmm_last_error": (C.c_char_p, [vp]),
+        "hfmm_destroy": (None, [vp]),
+        "hfmm_level_quadrature": (ci, [dbl, dbl, dbl, dbl, C.POINTER(ci), C.POINTER(ci), C.POINTER(ci), vp, ci]),
+        "hfmm_resample_workspace": (i64, [ci, ci, ci, ci, ci]),
+        "hfmm_resample": (ci, [ci, ci, ci, ci, ci, vp, vp, vp, vp]),
+        "hfmm_m2m_op": (ci, [ci, ci, ci, ci, ci, vp, vp, vp, vp, vp]),
+        "hfmm_l2l_op": (ci, [ci, ci, ci, ci, ci, vp, vp, vp, vp, vp, vp]),
+        "hfmm_m2l_op": (ci, [ci, i64, vp, vp, vp, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it; the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    rc = load().hfmm_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_nccl_unique_id")
+    return buf.raw
+
+
+def level_quadrature(kappa: float, a: float, eps_level: float, alpha: float = 0.8):
+    """Host-only per-level quadrature (ell, N_theta, N_phi, ragged rows) -- no GPU needed."""
+    lib = load()
+    ell, nth, nph = C.c_int(), C.c_int(), C.c_int()
+    cap = 4096
+    rag = (C.c_int * cap)()
+    rc = lib.hfmm_level_quadrature(kappa, a, eps_level, alpha, C.byref(ell), C.byref(nth), C.byref(nph),
+                                   C.cast(rag, C.c_void_p), cap)
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_level_quadrature failed")
+    return ell.value, nth.value, nph.value, list(rag[: nth.value // 2 + 1])
+
+
+def _ptr(a) -> int:
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+class HFMM:
+    """One FMM plan on one GPU (see include/hfmm.h for the contract)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        h = C.c_void_p()
+        rc = self.lib.hfmm_create(C.byref(h), device)
+        if rc != 0:
+            raise HFMMError(rc, self.lib.hfmm_last_error(None).decode())
+        self.h = h
+        self.n = 0
+        self.last_rc = 0
+
+    def _check(self, rc):
+        self.last_rc = rc
+        if rc < 0:
+            raise HFMMError(rc, self.lib.hfmm_last_error(self.h).decode())
+        return rc
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.hfmm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_dist(self, rank: int, nranks: int, uid: Optional[bytes]):
+        return self._check(self.lib.hfmm_set_dist(self.h, rank, nranks, uid))
+
+    def build_tree(self, xyz: np.ndarray, depth: int, lo, size: float):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        self.n = xyz.shape[0]
+        return self._check(self.lib.hfmm_build_tree(self.h, self.n, xyz.ctypes.data, depth, lo.ctypes.data, size))
+
+    def precompute(self, kappa: float, eps: float, alpha: float = 0.8, tau: float = 0.0, flags: int = 0):
+        return self._check(self.lib.hfmm_precompute(self.h, kappa, eps, alpha, tau, flags))
+
+    def _apply(self, fn, q, out=None, stream=None, local=False):
+        mem_local = HFMM_Y_LOCAL if local else 0
+        if hasattr(q, "is_cuda") and q.is_cuda:
+            import torch
+            if out is None:
+                out = torch.empty_like(q)
+            s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+            self._check(fn(self.h, q.data_ptr(), out.data_ptr(), HFMM_DEVICE | mem_local, C.c_void_p(s)))
+            return out
+        if hasattr(q, "data_ptr"):  # CPU torch tensor (pinned or pageable): host path
+            import torch
+            if out is None:
+                out = torch.empty_like(q)
+            s = None if stream is None else C.c_void_p(stream)
+            self._check(fn(self.h, q.data_ptr(), out.data_ptr(), HFMM_HOST | mem_local, s))
+            return out
+        q = np.ascontiguousarray(q, dtype=np.complex128)
+        if out is None:
+            out = np.empty_like(q)
+        self._check(fn(self.h, q.ctypes.data, out.ctypes.data, HFMM_HOST | mem_local, None))
+        return out
+
+    def matvec(self, q, out=None, stream=None, local=False):
+        """y = A q (eqn:HelmholtzMatrixVector); numpy/CPU tensors use the host path."""
+        return self._apply(self.lib.hfmm_matvec, q, out, stream, local)
+
+    def direct(self, q, out=None, stream=None):
+        return self._apply(self.lib.hfmm_direct, q, out, stream)
+
+    def info(self) -> dict:
+        inf = Info()
+        self._check(self.lib.hfmm_get_info(self.h, C.byref(inf)))
+        levels = []
+        for i in range(inf.nlevels):
+            lv = inf.level[i]
+            levels.append(dict(level=lv.level, a=lv.a, ell=lv.ell, n_theta=lv.n_theta, n_phi=lv.n_phi, K=lv.K,
+                               F=lv.F, active=bool(lv.active), boxes=lv.boxes, m2l_pairs=lv.m2l_pairs))
+        return dict(n=inf.n, depth=inf.depth, L_f=(None if inf.L_f < 0 else inf.L_f), kappa=inf.kappa,
+                    eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
+                    s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points)
+
+    def stage_times(self):
+        out = (C.c_double * 8)()
+        self._check(self.lib.hfmm_stage_times(self.h, C.cast(out, C.c_void_p)))
+        keys = ["s2m", "m2m", "m2l", "l2l", "l2t", "p2p", "total"]
+        return {k: out[i] for i, k in enumerate(keys)}
+
+    def debug(self, what: int, level: int = 0) -> np.ndarray:
+        need = C.c_int64()
+        self._check(self.lib.hfmm_debug_copy(self.h, what, level, None, 0, C.byref(need)))
+        if what in (6, 7):
+            buf = np.empty(need.value // 8, dtype=np.int64)
+        else:
+            buf = np.empty(need.value // 16, dtype=np.complex128)
+        if need.value:
+            self._check(self.lib.hfmm_debug_copy(self.h, what, level, buf.ctypes.data, need.value, C.byref(need)))
+        if what == 7:
+            buf = buf.reshape(-1, 4)
+        return buf
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(stream)
+
+
+def resample(inp, nth, nph, nth2, nph2, out, work=None, stream=None):
+    """Batched 5-step resample of device fields [B][nth][nph/2] -> [B][nth2][nph2/2] (torch tensors)."""
+    lib = load()
+    rc = lib.hfmm_resample(inp.shape[0], nth, nph, nth2, nph2, inp.data_ptr(), out.data_ptr(),
+                           None if work is None else work.data_ptr(), _stream(stream))
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_resample")
+    return out
+
+
+def resample_workspace(nbatch, nth, nph, nth2, nph2) -> int:
+    return load().hfmm_resample_workspace(nbatch, nth, nph, nth2, nph2)
+
+
+def m2m_op(child, shift, parent, nth, nph, nth2, nph2, work=None, stream=None):
+    lib = load()
+    rc = lib.hfmm_m2m_op(parent.shape[0], nth, nph, nth2, nph2, child.data_ptr(), shift.data_ptr(),
+                         parent.data_ptr(), None if work is None else work.data_ptr(), _stream(stream))
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_m2m_op")
+    return parent
+
+
+def l2l_op(parent, shift, incoming, child_out, nth, nph, nth2, nph2, work=None, stream=None):
+    lib = load()
+    rc = lib.hfmm_l2l_op(parent.shape[0], nth, nph, nth2, nph2, parent.data_ptr(), shift.data_ptr(),
+                         None if incoming is None else incoming.data_ptr(), child_out.data_ptr(),
+                         None if work is None else work.data_ptr(), _stream(stream))
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_l2l_op")
+    return child_out
+
+
+def m2l_op(row, src, oid, T, M, out, stream=None):
+    lib = load()
+    nbox = row.shape[0] - 1
+    K = M.shape[-1] if M.dim() == 2 else M.shape[1] * M.shape[2]
+    rc = lib.hfmm_m2l_op(nbox, K, row.data_ptr(), src.data_ptr(), oid.data_ptr(), T.data_ptr(), M.data_ptr(),
+                         out.data_ptr(), _stream(stream))
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_m2l_op")
+    return out

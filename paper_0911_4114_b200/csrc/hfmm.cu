@@ -1,0 +1,979 @@
+// libhfmm C ABI and matvec orchestration (product code, sm_100a).  See include/hfmm.h.
+// Pass order of one matvec:
+//   permute q -> S2M (L_f) -> M2M (L_f..3) -> [all-gather M_l, multi-GPU] -> M2L (2..L_f)
+//   -> L2L (2..L_f-1) -> L2T (L_f) ; P2P (L_f) on a second stream ; combine + unpermute.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "hfmm_impl.h"
+#include "../../include/hfmm.h"
+
+using namespace hfmm;
+
+namespace {
+
+const double kPi = 3.14159265358979323846;
+const double kURound = 1.1102230246251565e-16;  // 2^-53
+
+struct LevelDev {
+  int l = 0;
+  double a = 0;
+  int ell = 0, nth = 0, nph = 0;
+  int64_t K = 0;
+  double F = NAN;
+  bool active = false;
+  int64_t nbox = 0;
+  int64_t own0 = 0, own1 = 0;  // owned box range (Morton order)
+  std::vector<int64_t> rlo, rhi; // every rank's owned range (for the all-gather)
+  double *cx = nullptr, *cy = nullptr, *cz = nullptr;
+  double *ks = nullptr;          // kappa s [3][K]
+  double2 *T = nullptr;          // [316][K]
+  double2 *M = nullptr, *I = nullptr, *L = nullptr;  // [nbox][K]
+  int32_t *il_row = nullptr, *il_src = nullptr, *il_oid = nullptr;
+  int64_t il_nnz = 0;
+  int32_t *parent = nullptr;     // into level l-1
+  int8_t *oct = nullptr;         // octant of the box inside its parent
+  int32_t *cbeg = nullptr;       // children range into level l+1
+  double2 *shift = nullptr;      // [8][K] e^{i kappa s.(c_child - c_parent)} on this grid
+};
+
+template <class T>
+T *dalloc(size_t count) {
+  if (!count) return nullptr;
+  void *p = nullptr;
+  if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) return nullptr;
+  return (T *)p;
+}
+
+template <class T>
+T *dupload(const std::vector<T> &h) {
+  if (h.empty()) return nullptr;
+  T *d = dalloc<T>(h.size());
+  if (d) cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return d;
+}
+
+TwiddleSet &global_twiddles(int device) {
+  static std::map<int, std::unique_ptr<TwiddleSet>> sets;
+  auto it = sets.find(device);
+  if (it != sets.end()) return *it->second;
+  std::vector<int> lens;
+  for (int N = 2; N < 1024; ++N)
+    if (seven_smooth(N)) lens.push_back(N);
+  auto ts = std::make_unique<TwiddleSet>();
+  ts->build(lens);
+  TwiddleSet &ref = *ts;
+  sets[device] = std::move(ts);
+  return ref;
+}
+
+}  // namespace
+
+struct hfmm_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr, stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::string err;
+  bool have_tree = false, have_plan = false;
+  Tree tree;
+  // dist
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  // points (sorted)
+  double *px = nullptr, *py = nullptr, *pz = nullptr;
+  int64_t *perm = nullptr;
+  double2 *q_in = nullptr, *q_sorted = nullptr, *y_out = nullptr, *y_near = nullptr, *y_far = nullptr;
+  // plan
+  double kappa = 0, eps = 0, alpha = 0, tau = 0;
+  unsigned flags = 0;
+  int L_f = -1;
+  std::vector<LevelDev> lv;  // index = level
+  int near_level = 0;        // level of the near-field boxes (L_f or 0)
+  int64_t own_pt0 = 0, own_pt1 = 0;
+  int64_t *first_near = nullptr;  // point ranges of near-level boxes
+  int32_t *nb_row = nullptr, *nb_box = nullptr;
+  int32_t *tile_leaf = nullptr;
+  int64_t *tile_begin = nullptr;
+  int64_t ntiles = 0;
+  // all-pairs (direct) tiles
+  int32_t *dir_tile_leaf = nullptr, *dir_nb_row = nullptr, *dir_nb_box = nullptr;
+  int64_t *dir_tile_begin = nullptr, *dir_first = nullptr;
+  int64_t dir_ntiles = 0;
+  double2 *tmp = nullptr;
+  size_t tmp_elems = 0;
+  hfmm_info info{};
+  double stage_ms[8] = {0};
+  bool profile = false;
+  cudaEvent_t sev[10] = {nullptr};
+};
+
+static thread_local std::string g_create_err;
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      p->err = std::string(#call) + ": " + cudaGetErrorString(e_);                    \
+      return HFMM_E_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+#define CKN(call)                                                                    \
+  do {                                                                               \
+    ncclResult_t r_ = (call);                                                        \
+    if (r_ != ncclSuccess) {                                                         \
+      p->err = std::string(#call) + ": " + ncclGetErrorString(r_);                    \
+      return HFMM_E_NCCL;                                                            \
+    }                                                                                \
+  } while (0)
+
+static void free_levels(hfmm_plan *p) {
+  for (auto &L : p->lv) {
+    for (void *ptr : {(void *)L.cx, (void *)L.cy, (void *)L.cz, (void *)L.ks, (void *)L.T, (void *)L.M,
+                      (void *)L.I, (void *)L.L, (void *)L.il_row, (void *)L.il_src, (void *)L.il_oid,
+                      (void *)L.parent, (void *)L.oct, (void *)L.cbeg, (void *)L.shift})
+      if (ptr) cudaFree(ptr);
+  }
+  p->lv.clear();
+  for (void *ptr : {(void *)p->first_near, (void *)p->nb_row, (void *)p->nb_box, (void *)p->tile_leaf,
+                    (void *)p->tile_begin, (void *)p->tmp, (void *)p->y_far})
+    if (ptr) cudaFree(ptr);
+  p->first_near = nullptr, p->nb_row = p->nb_box = p->tile_leaf = nullptr;
+  p->tile_begin = nullptr, p->tmp = nullptr, p->y_far = nullptr;
+  p->tmp_elems = 0;
+  p->ntiles = 0;
+  p->have_plan = false;
+}
+
+static void free_points(hfmm_plan *p) {
+  for (void *ptr : {(void *)p->px, (void *)p->py, (void *)p->pz, (void *)p->perm, (void *)p->q_in,
+                    (void *)p->q_sorted, (void *)p->y_out, (void *)p->y_near, (void *)p->dir_tile_leaf,
+                    (void *)p->dir_nb_row, (void *)p->dir_nb_box, (void *)p->dir_tile_begin,
+                    (void *)p->dir_first})
+    if (ptr) cudaFree(ptr);
+  p->px = p->py = p->pz = nullptr;
+  p->perm = nullptr;
+  p->q_in = p->q_sorted = p->y_out = p->y_near = nullptr;
+  p->dir_tile_leaf = p->dir_nb_row = p->dir_nb_box = nullptr;
+  p->dir_tile_begin = p->dir_first = nullptr;
+  p->have_tree = false;
+}
+
+extern "C" int hfmm_create(hfmm_plan **out, int device) {
+  if (!out) return HFMM_E_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    g_create_err = "hfmm_create: no CUDA device (libhfmm has no CPU fallback)";
+    return HFMM_E_CUDA;
+  }
+  if (device < 0) cudaGetDevice(&device);
+  if (device >= ndev) {
+    g_create_err = "hfmm_create: bad device index";
+    return HFMM_E_ARG;
+  }
+  auto *p = new hfmm_plan();
+  p->device = device;
+  cudaSetDevice(device);
+  CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  for (auto &e : p->sev) CK(cudaEventCreate(&e));
+  const char *prof = std::getenv("HFMM_PROFILE_STAGES");
+  p->profile = prof && prof[0] && prof[0] != '0';
+  global_twiddles(device);
+  *out = p;
+  return HFMM_OK;
+}
+
+extern "C" int hfmm_set_dist(hfmm_plan *p, int rank, int nranks, const void *id) {
+  if (!p) return HFMM_E_ARG;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !id)) {
+    p->err = "hfmm_set_dist: bad rank/nranks/id";
+    return HFMM_E_ARG;
+  }
+  if (p->have_tree) {
+    p->err = "hfmm_set_dist: must be called before build_tree";
+    return HFMM_E_STATE;
+  }
+  cudaSetDevice(p->device);
+  if (p->comm) {
+    ncclCommDestroy(p->comm);
+    p->comm = nullptr;
+  }
+  p->rank = rank;
+  p->nranks = nranks;
+  if (nranks > 1) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    CKN(ncclCommInitRank(&p->comm, nranks, uid, rank));
+  }
+  return HFMM_OK;
+}
+
+extern "C" int hfmm_nccl_unique_id(void *out) {
+  if (!out) return HFMM_E_ARG;
+  ncclUniqueId uid;
+  if (ncclGetUniqueId(&uid) != ncclSuccess) return HFMM_E_NCCL;
+  std::memcpy(out, &uid, sizeof(uid));
+  return HFMM_OK;
+}
+
+extern "C" int hfmm_build_tree(hfmm_plan *p, int64_t n, const double *xyz, int depth, const double lo[3],
+                               double size) {
+  if (!p) return HFMM_E_ARG;
+  if (!xyz || !lo) {
+    p->err = "hfmm_build_tree: NULL pointer";
+    return HFMM_E_ARG;
+  }
+  cudaSetDevice(p->device);
+  free_levels(p);
+  free_points(p);
+  int rc = build_tree(xyz, n, depth, lo, size, p->tree, p->err);
+  if (rc) return rc;
+  const Tree &t = p->tree;
+  p->px = dupload(t.xs), p->py = dupload(t.ys), p->pz = dupload(t.zs);
+  p->perm = dupload(t.perm);
+  p->q_in = dalloc<double2>(n), p->q_sorted = dalloc<double2>(n);
+  p->y_out = dalloc<double2>(n), p->y_near = dalloc<double2>(n);
+  if (!p->px || !p->py || !p->pz || !p->perm || !p->q_in || !p->q_sorted || !p->y_out || !p->y_near) {
+    p->err = "hfmm_build_tree: device allocation failed";
+    return HFMM_E_NOMEM;
+  }
+  // all-pairs tiles for hfmm_direct: one box (the root) containing every point
+  {
+    std::vector<int32_t> tl;
+    std::vector<int64_t> tb;
+    for (int64_t s = 0; s < n; s += 128) tl.push_back(0), tb.push_back(s);
+    p->dir_tile_leaf = dupload(tl);
+    p->dir_tile_begin = dupload(tb);
+    p->dir_ntiles = (int64_t)tl.size();
+    p->dir_nb_row = dupload(std::vector<int32_t>{0, 1});
+    p->dir_nb_box = dupload(std::vector<int32_t>{0});
+    p->dir_first = dupload(std::vector<int64_t>{0, n});
+  }
+  p->have_tree = true;
+  return HFMM_OK;
+}
+
+// ---- precompute helpers ---------------------------------------------------------------------
+static int level_tables(hfmm_plan *p, LevelDev &L, double2 **T_out, double *F_out) {
+  // Alg. 1 for the 316 offsets on the GPU; c_n per distinct |r0| from the host.
+  std::vector<double2> coef;
+  std::vector<int32_t> coef_of(316);
+  std::vector<double> r0hat(316 * 3);
+  std::map<int, int> by_norm2;
+  for (int id = 0; id < 316; ++id) {
+    int o[3];
+    offset_vec(id, o);
+    int n2 = o[0] * o[0] + o[1] * o[1] + o[2] * o[2];
+    auto it = by_norm2.find(n2);
+    if (it == by_norm2.end()) {
+      std::vector<cplx> c;
+      transfer_series(L.ell, p->kappa, std::sqrt((double)n2) * L.a, c);
+      int idx = (int)by_norm2.size();
+      by_norm2[n2] = idx;
+      for (auto &v : c) coef.push_back(make_double2(v.real(), v.imag()));
+      coef_of[id] = idx;
+    } else {
+      coef_of[id] = it->second;
+    }
+    double nr = std::sqrt((double)n2);
+    for (int d = 0; d < 3; ++d) r0hat[3 * id + d] = o[d] / nr;
+  }
+  for (auto &v : coef)
+    if (!std::isfinite(v.x) || !std::isfinite(v.y)) {
+      // h_n overflow: deep in the low-frequency breakdown; table unusable
+      *T_out = nullptr;
+      *F_out = INFINITY;
+      return HFMM_OK;
+    }
+  double2 *dcoef = dupload(coef);
+  int32_t *dcof = dupload(coef_of);
+  double *dr0 = dupload(r0hat);
+  double2 *T = dalloc<double2>((size_t)316 * L.K);
+  if (!dcoef || !dcof || !dr0 || !T) {
+    p->err = "precompute: allocation failed (transfer tables)";
+    return HFMM_E_NOMEM;
+  }
+  if (L.nph >= 2 * L.ell + 2) {
+    launch_alg1_tables(dcoef, dcof, dr0, L.ell, L.nth, L.nph, L.nph / 2, T, p->stream);
+  } else {
+    const int nphf = 2 * L.ell + 2;
+    double2 *full = dalloc<double2>((size_t)316 * L.nth * nphf);
+    if (!full) {
+      p->err = "precompute: allocation failed (phi-fine tables)";
+      return HFMM_E_NOMEM;
+    }
+    launch_alg1_tables(dcoef, dcof, dr0, L.ell, L.nth, nphf, nphf, full, p->stream);
+    launch_phi_anterp(full, L.nth, nphf, L.nph, T, p->stream);
+    CK(cudaStreamSynchronize(p->stream));
+    cudaFree(full);
+  }
+  double *dmax = dalloc<double>(1);
+  launch_absmax(T, (int64_t)316 * L.K, dmax, p->stream);
+  double mx = 0;
+  CK(cudaMemcpyAsync(&mx, dmax, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  CK(cudaGetLastError());
+  cudaFree(dmax);
+  cudaFree(dcoef);
+  cudaFree(dcof);
+  cudaFree(dr0);
+  *T_out = T;
+  *F_out = 8.0 * kPi * kURound * L.a * mx;
+  return HFMM_OK;
+}
+
+static void grid_dirs(int nth, int nph, double kappa, std::vector<double> &ks) {
+  const int64_t h = nph / 2, K = (int64_t)nth * h;
+  ks.assign(3 * K, 0.0);
+  for (int n = 0; n < nth; ++n) {
+    long double th = 2.0L * 3.141592653589793238462643383279502884L * n / nth;
+    double st = (double)sinl(th), ct = (double)cosl(th);
+    for (int m = 0; m < h; ++m) {
+      long double ph = 2.0L * 3.141592653589793238462643383279502884L * m / nph;
+      double cp = (double)cosl(ph), sp = (double)sinl(ph);
+      int64_t k = (int64_t)n * h + m;
+      ks[k] = kappa * (cp * st);
+      ks[K + k] = kappa * (sp * st);
+      ks[2 * K + k] = kappa * ct;
+    }
+  }
+}
+
+static void partition(hfmm_plan *p) {
+  // Ownership by contiguous Morton ranges of level-2 subtrees (or of points if no far field),
+  // balanced by an estimate of FP64 work: P2P pairs + S2M/L2T evaluations.  Every rank
+  // computes every rank's ranges (needed for the variable-size all-gather).
+  const Tree &t = p->tree;
+  const int R = p->nranks, r = p->rank;
+  if (p->L_f < 0) {
+    const int64_t n = t.n;
+    auto cutp = [&](int k) -> int64_t {
+      if (k >= R) return n;
+      int64_t c = (n * k / R) / 128 * 128;   // tile-aligned (P2P tiles are 128 targets)
+      return std::min(c, n);
+    };
+    p->own_pt0 = cutp(r);
+    p->own_pt1 = cutp(r + 1);
+    return;
+  }
+  const LevelBoxes &B2 = t.levels[2];
+  const LevelBoxes &BL = t.levels[p->L_f];
+  const int64_t KL = p->lv[p->L_f].K;
+  std::vector<double> w(B2.nbox(), 0.0);
+  for (int64_t b = 0; b < BL.nbox(); ++b) {
+    int64_t nb = BL.first[b + 1] - BL.first[b];
+    int64_t src = 0;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          int32_t k = BL.find(BL.ix[b] + dx, BL.iy[b] + dy, BL.iz[b] + dz);
+          if (k >= 0) src += BL.first[k + 1] - BL.first[k];
+        }
+    int32_t a = (int32_t)b;
+    for (int l = p->L_f; l > 2; --l) a = t.levels[l].parent[a];
+    w[a] += (double)nb * (double)src + 2.0 * (double)nb * (double)KL;
+  }
+  double tot = std::accumulate(w.begin(), w.end(), 0.0);
+  std::vector<int64_t> cut(R + 1, B2.nbox());
+  cut[0] = 0;
+  double acc = 0;
+  int k = 1;
+  for (int64_t b = 0; b < B2.nbox() && k < R; ++b) {
+    acc += w[b];
+    while (k < R && acc >= tot * k / R) cut[k++] = b + 1;
+  }
+  for (; k < R; ++k) cut[k] = B2.nbox();
+  for (int l = 2; l <= p->L_f; ++l) {
+    LevelDev &L = p->lv[l];
+    L.rlo.assign(R, 0), L.rhi.assign(R, 0);
+    for (int q = 0; q < R; ++q) {
+      if (l == 2) {
+        L.rlo[q] = cut[q], L.rhi[q] = cut[q + 1];
+      } else {
+        const LevelBoxes &P = t.levels[l - 1];
+        const LevelDev &U = p->lv[l - 1];
+        L.rlo[q] = P.child_begin[U.rlo[q]];
+        L.rhi[q] = P.child_begin[U.rhi[q]];
+      }
+    }
+    L.own0 = L.rlo[r], L.own1 = L.rhi[r];
+  }
+  const LevelDev &Lf = p->lv[p->L_f];
+  p->own_pt0 = BL.first[Lf.own0];
+  p->own_pt1 = BL.first[Lf.own1];
+}
+
+extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double alpha, double tau,
+                               unsigned flags) {
+  if (!p) return HFMM_E_ARG;
+  if (!p->have_tree) {
+    p->err = "hfmm_precompute: build_tree first";
+    return HFMM_E_STATE;
+  }
+  if (!(kappa > 0) || !std::isfinite(kappa) || !(eps > 0) || !(eps < 1) || !(alpha > 0) || alpha > 1) {
+    p->err = "hfmm_precompute: need kappa > 0, 0 < eps < 1, 0 < alpha <= 1";
+    return HFMM_E_ARG;
+  }
+  cudaSetDevice(p->device);
+  free_levels(p);
+  p->kappa = kappa, p->eps = eps, p->alpha = alpha, p->flags = flags;
+  p->tau = (tau > 0) ? tau : std::min(eps / 10.0, 1e-9);
+  const Tree &t = p->tree;
+  const int D = t.depth;
+  p->lv.assign(D + 1, LevelDev());
+  // per-level quadrature (host)
+  for (int l = 2; l <= D; ++l) {
+    LevelDev &L = p->lv[l];
+    L.l = l;
+    L.a = t.size / (double)(1 << l);
+    const double eps_l = (flags & HFMM_EPS_ABSOLUTE) ? eps : eps / L.a;
+    const double r = alpha * std::sqrt(3.0) * L.a, r0 = 2.0 * L.a;
+    int rc = select_ell(kappa, r, r0, eps_l, &L.ell);
+    if (!rc) rc = select_ntheta(L.ell, kappa, r, r0, eps_l, &L.nth);
+    if (!rc) rc = select_nphi(L.ell, kappa, r, r0, eps_l, L.nth, &L.nph, nullptr);
+    if (rc) {
+      p->err = "hfmm_precompute: quadrature search failed at level " + std::to_string(l);
+      return rc;
+    }
+    L.K = (int64_t)L.nth * L.nph / 2;
+    L.nbox = t.levels[l].nbox();
+  }
+  // admissibility F_l <= tau, shallowest first (R-9)
+  p->L_f = -1;
+  const bool force = flags & HFMM_FORCE_ALL_LEVELS;
+  for (int l = 2; l <= D; ++l) {
+    LevelDev &L = p->lv[l];
+    double2 *T = nullptr;
+    int rc = level_tables(p, L, &T, &L.F);
+    if (rc) return rc;
+    L.active = force || (L.F <= p->tau);
+    if (!L.active) {
+      if (T) cudaFree(T);
+      break;
+    }
+    L.T = T;
+    p->L_f = l;
+  }
+  // monotone grids along the active chain (R-5)
+  for (int l = p->L_f - 1; l >= 2; --l) {
+    LevelDev &U = p->lv[l], &Dn = p->lv[l + 1];
+    int nth = std::max(U.nth, Dn.nth), nph = std::max(U.nph, Dn.nph);
+    if (nth != U.nth || nph != U.nph) {
+      U.nth = nth, U.nph = nph, U.K = (int64_t)nth * nph / 2;
+      cudaFree(U.T);
+      int rc = level_tables(p, U, &U.T, &U.F);
+      if (rc) return rc;
+    }
+  }
+  partition(p);
+  // device data of the active levels
+  size_t tmp_need = 0;
+  for (int l = 2; l <= p->L_f; ++l) {
+    LevelDev &L = p->lv[l];
+    const LevelBoxes &B = t.levels[l];
+    std::vector<double> cx(B.nbox()), cy(B.nbox()), cz(B.nbox());
+    for (int64_t b = 0; b < B.nbox(); ++b) {
+      cx[b] = t.lo[0] + (B.ix[b] + 0.5) * L.a;
+      cy[b] = t.lo[1] + (B.iy[b] + 0.5) * L.a;
+      cz[b] = t.lo[2] + (B.iz[b] + 0.5) * L.a;
+    }
+    L.cx = dupload(cx), L.cy = dupload(cy), L.cz = dupload(cz);
+    std::vector<double> ks;
+    grid_dirs(L.nth, L.nph, kappa, ks);
+    L.ks = dupload(ks);
+    L.M = dalloc<double2>((size_t)L.nbox * L.K);
+    L.I = dalloc<double2>((size_t)L.nbox * L.K);
+    L.L = dalloc<double2>((size_t)L.nbox * L.K);
+    if (!L.M || !L.I || !L.L || !L.ks) {
+      p->err = "hfmm_precompute: allocation failed (level buffers)";
+      return HFMM_E_NOMEM;
+    }
+    // interaction lists for every box of the level
+    std::vector<int32_t> row(1, 0), src, oid;
+    for (int64_t b = 0; b < B.nbox(); ++b) {
+      const int px = B.ix[b] >> 1, py = B.iy[b] >> 1, pz = B.iz[b] >> 1;
+      for (int dx = -3; dx <= 3; ++dx)
+        for (int dy = -3; dy <= 3; ++dy)
+          for (int dz = -3; dz <= 3; ++dz) {
+            if (std::max(std::abs(dx), std::max(std::abs(dy), std::abs(dz))) < 2) continue;
+            int x = B.ix[b] + dx, y = B.iy[b] + dy, z = B.iz[b] + dz;
+            if (std::abs((x >> 1) - px) > 1 || std::abs((y >> 1) - py) > 1 || std::abs((z >> 1) - pz) > 1)
+              continue;
+            int32_t k = B.find(x, y, z);
+            if (k < 0) continue;
+            src.push_back(k);
+            oid.push_back(offset_id(dx, dy, dz));
+          }
+      row.push_back((int32_t)src.size());
+    }
+    L.il_nnz = (int64_t)src.size();
+    L.il_row = dupload(row), L.il_src = dupload(src), L.il_oid = dupload(oid);
+    // tree links
+    std::vector<int32_t> par(B.parent.begin(), B.parent.end());
+    std::vector<int8_t> oc(B.nbox());
+    for (int64_t b = 0; b < B.nbox(); ++b) oc[b] = (int8_t)(((B.ix[b] & 1) << 2) | ((B.iy[b] & 1) << 1) | (B.iz[b] & 1));
+    L.parent = dupload(par);
+    L.oct = dupload(oc);
+    if (l < p->L_f) {
+      std::vector<int32_t> cb(B.child_begin.begin(), B.child_begin.end());
+      L.cbeg = dupload(cb);
+      // translation tables on this grid for children at level l+1
+      const double h = 0.5 * p->lv[l + 1].a;
+      std::vector<double2> sh((size_t)8 * L.K);
+      for (int o = 0; o < 8; ++o) {
+        const double d0 = ((o >> 2) & 1) ? h : -h, d1 = ((o >> 1) & 1) ? h : -h, d2 = (o & 1) ? h : -h;
+        for (int64_t k = 0; k < L.K; ++k) {
+          double ph = ks[k] * d0 + ks[L.K + k] * d1 + ks[2 * L.K + k] * d2;
+          sh[(size_t)o * L.K + k] = make_double2(std::cos(ph), std::sin(ph));
+        }
+      }
+      L.shift = dupload(sh);
+      const LevelDev &C = p->lv[l + 1];
+      tmp_need = std::max(tmp_need, (size_t)C.nbox * (C.nth / 2 + 1) * L.nph);  // M2M rows pass
+      tmp_need = std::max(tmp_need, (size_t)C.nbox * C.nth * (L.nph / 2));      // L2L cols pass
+    }
+  }
+  if (tmp_need) {
+    p->tmp = dalloc<double2>(tmp_need);
+    p->tmp_elems = tmp_need;
+    if (!p->tmp) {
+      p->err = "hfmm_precompute: allocation failed (resample scratch)";
+      return HFMM_E_NOMEM;
+    }
+  }
+  // near field at L_f (neighbour lists) or all pairs at the root
+  p->near_level = p->L_f >= 2 ? p->L_f : 0;
+  {
+    const LevelBoxes &B = t.levels[p->near_level];
+    std::vector<int32_t> row(1, 0), nb;
+    for (int64_t b = 0; b < B.nbox(); ++b) {
+      for (int dx = -1; dx <= 1; ++dx)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dz = -1; dz <= 1; ++dz) {
+            int32_t k = B.find(B.ix[b] + dx, B.iy[b] + dy, B.iz[b] + dz);
+            if (k >= 0) nb.push_back(k);
+          }
+      row.push_back((int32_t)nb.size());
+    }
+    p->nb_row = dupload(row), p->nb_box = dupload(nb);
+    p->first_near = dupload(B.first);
+    int64_t lo = 0, hi = B.nbox();
+    if (p->L_f >= 2) lo = p->lv[p->L_f].own0, hi = p->lv[p->L_f].own1;
+    std::vector<int32_t> tl;
+    std::vector<int64_t> tb;
+    for (int64_t b = lo; b < hi; ++b)
+      for (int64_t s = B.first[b]; s < B.first[b + 1]; s += 128) {
+        if (p->L_f < 0 && (s < p->own_pt0 || s >= p->own_pt1)) continue;
+        tl.push_back((int32_t)b), tb.push_back(s);
+      }
+    p->tile_leaf = dupload(tl), p->tile_begin = dupload(tb);
+    p->ntiles = (int64_t)tl.size();
+    int64_t pairs = 0;
+    for (int64_t b = lo; b < hi; ++b)
+      for (int32_t e = row[b]; e < row[b + 1]; ++e)
+        pairs += (B.first[b + 1] - B.first[b]) * (B.first[nb[e] + 1] - B.first[nb[e]]);
+    p->info.p2p_pairs = pairs;
+  }
+  if (p->L_f >= 2) p->y_far = dalloc<double2>(t.n);
+  CK(cudaStreamSynchronize(p->stream));
+  CK(cudaGetLastError());
+  // info
+  hfmm_info &in = p->info;
+  in.n = t.n, in.depth = D, in.L_f = p->L_f, in.kappa = kappa, in.eps = eps, in.alpha = alpha,
+  in.tau = p->tau, in.rank = p->rank, in.nranks = p->nranks;
+  in.nlevels = 0;
+  for (int l = 2; l <= D && in.nlevels < HFMM_MAX_LEVELS; ++l) {
+    const LevelDev &L = p->lv[l];
+    hfmm_level_info &li = in.level[in.nlevels++];
+    li.level = l, li.a = L.a, li.ell = L.ell, li.n_theta = L.nth, li.n_phi = L.nph, li.K = L.K,
+    li.F = L.F, li.active = L.active ? 1 : 0, li.boxes = L.nbox, li.m2l_pairs = L.il_nnz;
+  }
+  in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->L_f].K : 0;
+  in.owned_points = p->own_pt1 - p->own_pt0;
+  p->have_plan = true;
+  if (p->L_f < 0) {
+    p->err = "no admissible far-field level: matvec is the direct sum";
+    return HFMM_W_NO_FARFIELD;
+  }
+  if (p->L_f < D) {
+    p->err = "levels " + std::to_string(p->L_f + 1) + ".." + std::to_string(D) +
+             " inadmissible (low-frequency breakdown), far-field leaf level L_f = " + std::to_string(p->L_f);
+    return HFMM_W_BREAKDOWN;
+  }
+  return HFMM_OK;
+}
+
+// ---- the matvec ------------------------------------------------------------------------------
+static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
+  if (p->nranks <= 1) return HFMM_OK;
+  // all-gather of M_l over variable-size Morton ranges: one broadcast per root, grouped
+  CKN(ncclGroupStart());
+  for (int r = 0; r < p->nranks; ++r) {
+    size_t cnt = (size_t)(L.rhi[r] - L.rlo[r]) * L.K * 2;
+    if (!cnt) continue;
+    double *buf = (double *)(L.M + L.rlo[r] * L.K);
+    CKN(ncclBroadcast(buf, buf, cnt, ncclDouble, r, p->comm, s));
+  }
+  CKN(ncclGroupEnd());
+  return HFMM_OK;
+}
+
+static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
+  const Tree &t = p->tree;
+  const int64_t n = t.n;
+  const bool prof = p->profile;
+  if (prof) cudaEventRecord(p->sev[0], s);
+  launch_permute_q(q_dev, p->perm, p->q_sorted, n, s);
+  PointsDev pts{p->px, p->py, p->pz, p->q_sorted};
+  // near field on the second stream, concurrent with the far-field chain
+  CK(cudaEventRecord(p->ev_fork, s));
+  CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
+  if (prof) cudaEventRecord(p->sev[7], p->stream2);
+  launch_p2p(pts, p->first_near, p->nb_row, p->nb_box, 0, 0, p->tile_leaf, p->tile_begin, p->ntiles,
+             p->kappa, p->y_near, p->stream2);
+  if (prof) cudaEventRecord(p->sev[8], p->stream2);
+  CK(cudaEventRecord(p->ev_join, p->stream2));
+  const TwiddleSet &tw = global_twiddles(p->device);
+  if (p->L_f >= 2) {
+    const int Lf = p->L_f;
+    LevelDev &F = p->lv[Lf];
+    launch_s2m(pts, p->first_near, F.cx, F.cy, F.cz, (int32_t)F.own0,
+               (int32_t)F.own1, F.ks, F.K, F.M, s);
+    if (prof) cudaEventRecord(p->sev[1], s);
+    for (int l = Lf; l > 2; --l) {  // M2M
+      LevelDev &C = p->lv[l], &P = p->lv[l - 1];
+      if (C.own1 > C.own0) {
+        launch_rows_up(C.M + C.own0 * C.K, C.own1 - C.own0, C.nth, C.nph, P.nph, p->tmp, tw, s);
+        // parents own0..own1 have children C.own0.. (contiguous); child index relative to C.own0
+        launch_cols_up(p->tmp, C.nth, P.nph, P.nth, P.cbeg + P.own0, C.own0, C.oct, P.own1 - P.own0, P.shift,
+                       P.M + P.own0 * P.K, tw, s);
+      }
+    }
+    for (int l = 2; l <= Lf; ++l) {
+      int rc = allgather_level(p, p->lv[l], s);
+      if (rc) return rc;
+    }
+    if (prof) cudaEventRecord(p->sev[2], s);
+    for (int l = 2; l <= Lf; ++l) {  // M2L
+      LevelDev &L = p->lv[l];
+      launch_m2l((int32_t)L.own0, (int32_t)L.own1, L.K, L.il_row, L.il_src, L.il_oid, L.T, L.M, L.I, s);
+    }
+    if (prof) cudaEventRecord(p->sev[3], s);
+    for (int l = 2; l < Lf; ++l) {  // L2L; L_2 = I_2
+      LevelDev &P = p->lv[l], &C = p->lv[l + 1];
+      const double2 *Lp = (l == 2) ? P.I : P.L;
+      if (C.own1 > C.own0) {
+        launch_cols_down(Lp, P.nth, P.nph, C.nth, C.parent + C.own0, C.oct + C.own0, C.own1 - C.own0,
+                         P.shift, p->tmp, tw, s);
+        launch_rows_down(p->tmp, C.own1 - C.own0, C.nth, P.nph, C.nph, C.I + C.own0 * C.K,
+                         C.L + C.own0 * C.K, tw, s);
+      }
+    }
+    if (prof) cudaEventRecord(p->sev[4], s);
+    const double2 *Lf_loc = (Lf == 2) ? F.I : F.L;
+    launch_l2t(pts, p->first_near, F.cx, F.cy, F.cz, p->tile_leaf, p->tile_begin, p->ntiles, F.ks, F.K,
+               Lf_loc, 8.0 * kPi * kPi / ((double)F.nth * (double)F.nph), p->y_far, s);
+    if (prof) cudaEventRecord(p->sev[5], s);
+  } else if (prof) {
+    for (int k = 1; k <= 5; ++k) cudaEventRecord(p->sev[k], s);
+  }
+  CK(cudaStreamWaitEvent(s, p->ev_join, 0));
+  launch_combine(p->y_near, p->L_f >= 2 ? p->y_far : nullptr, p->perm, p->y_out, n, p->own_pt0, p->own_pt1, s);
+  if (prof) cudaEventRecord(p->sev[6], s);
+  CK(cudaGetLastError());
+  return HFMM_OK;
+}
+
+static int gather_y(hfmm_plan *p, cudaStream_t s) {
+  if (p->nranks <= 1) return HFMM_OK;
+  // y is in input order; each rank wrote the entries of its owned sorted range.  Reduce-sum
+  // would be wrong for a partition with zero-initialised gaps only if entries overlap (they
+  // do not), so an all-reduce (sum) of the zero-padded vector is exact.
+  CKN(ncclAllReduce(p->y_out, p->y_out, (size_t)p->tree.n * 2, ncclDouble, ncclSum, p->comm, s));
+  return HFMM_OK;
+}
+
+static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void *stream, bool direct) {
+  if (!p) return HFMM_E_ARG;
+  if (!q || !y) {
+    p->err = "matvec: NULL pointer";
+    return HFMM_E_ARG;
+  }
+  if (!p->have_tree || (!direct && !p->have_plan)) {
+    p->err = "matvec: build_tree and precompute first";
+    return HFMM_E_STATE;
+  }
+  cudaSetDevice(p->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : p->stream;
+  const int64_t n = p->tree.n;
+  const bool host = (mem & 1) == HFMM_HOST;
+  const bool local = (mem & HFMM_Y_LOCAL) != 0;
+  const double2 *qd = (const double2 *)q;
+  if (host) {
+    CK(cudaMemcpyAsync(p->q_in, q, n * sizeof(double2), cudaMemcpyHostToDevice, s));
+    qd = p->q_in;
+  }
+  if (p->nranks > 1 || local) CK(cudaMemsetAsync(p->y_out, 0, n * sizeof(double2), s));
+  if (direct) {
+    launch_permute_q(qd, p->perm, p->q_sorted, n, s);
+    PointsDev pts{p->px, p->py, p->pz, p->q_sorted};
+    launch_p2p(pts, p->dir_first, p->dir_nb_row, p->dir_nb_box, 0, 0, p->dir_tile_leaf, p->dir_tile_begin,
+               p->dir_ntiles, p->kappa > 0 ? p->kappa : 0.0, p->y_near, s);
+    launch_combine(p->y_near, nullptr, p->perm, p->y_out, n, 0, n, s);
+  } else {
+    int rc = run_matvec(p, qd, s);
+    if (rc) return rc;
+    if (!local) {
+      rc = gather_y(p, s);
+      if (rc) return rc;
+    }
+  }
+  if (host) {
+    CK(cudaMemcpyAsync(y, p->y_out, n * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } else {
+    CK(cudaMemcpyAsync(y, p->y_out, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  }
+  if (p->profile && !direct) {
+    CK(cudaStreamSynchronize(s));
+    float ms;
+    cudaEventElapsedTime(&ms, p->sev[0], p->sev[1]); p->stage_ms[0] = ms;
+    cudaEventElapsedTime(&ms, p->sev[1], p->sev[2]); p->stage_ms[1] = ms;
+    cudaEventElapsedTime(&ms, p->sev[2], p->sev[3]); p->stage_ms[2] = ms;
+    cudaEventElapsedTime(&ms, p->sev[3], p->sev[4]); p->stage_ms[3] = ms;
+    cudaEventElapsedTime(&ms, p->sev[4], p->sev[5]); p->stage_ms[4] = ms;
+    cudaEventElapsedTime(&ms, p->sev[7], p->sev[8]); p->stage_ms[5] = ms;
+    cudaEventElapsedTime(&ms, p->sev[0], p->sev[6]); p->stage_ms[6] = ms;
+  }
+  CK(cudaGetLastError());
+  return HFMM_OK;
+}
+
+extern "C" int hfmm_matvec(hfmm_plan *p, const double *q, double *y, int mem, void *stream) {
+  return matvec_common(p, q, y, mem, stream, false);
+}
+
+extern "C" int hfmm_direct(hfmm_plan *p, const double *q, double *y, int mem, void *stream) {
+  if (p && p->kappa <= 0) {
+    p->err = "hfmm_direct: call precompute first (kappa)";
+    return HFMM_E_STATE;
+  }
+  return matvec_common(p, q, y, mem, stream, true);
+}
+
+extern "C" int hfmm_get_info(const hfmm_plan *p, hfmm_info *info) {
+  if (!p || !info) return HFMM_E_ARG;
+  if (!p->have_plan) return HFMM_E_STATE;
+  *info = p->info;
+  return HFMM_OK;
+}
+
+extern "C" int hfmm_stage_times(const hfmm_plan *p, double out[8]) {
+  if (!p || !out) return HFMM_E_ARG;
+  for (int i = 0; i < 8; ++i) out[i] = p->stage_ms[i];
+  return HFMM_OK;
+}
+
+extern "C" int hfmm_debug_copy(const hfmm_plan *p, int what, int level, void *host_out, int64_t nbytes,
+                               int64_t *needed) {
+  if (!p) return HFMM_E_ARG;
+  cudaSetDevice(p->device);
+  const void *src = nullptr;
+  int64_t bytes = 0;
+  std::vector<int64_t> hostbuf;
+  if (what >= 0 && what <= 3) {
+    if (level < 2 || level >= (int)p->lv.size() || (what != 3 && level > p->L_f)) return HFMM_E_ARG;
+    const LevelDev &L = p->lv[level];
+    if (what == 3) {
+      src = L.T, bytes = (int64_t)316 * L.K * 16;
+    } else {
+      const double2 *b = what == 0 ? L.M : what == 1 ? L.I : (level == 2 ? L.I : L.L);
+      src = b, bytes = L.nbox * L.K * 16;
+    }
+  } else if (what == 4) {
+    src = p->y_near, bytes = p->tree.n * 16;
+  } else if (what == 5) {
+    src = p->y_far, bytes = p->y_far ? p->tree.n * 16 : 0;
+  } else if (what == 6) {
+    hostbuf = p->tree.perm;
+  } else if (what == 7) {
+    if (level < 0 || level > p->tree.depth) return HFMM_E_ARG;
+    const LevelBoxes &B = p->tree.levels[level];
+    for (int64_t b = 0; b < B.nbox(); ++b) {
+      hostbuf.push_back(B.ix[b]), hostbuf.push_back(B.iy[b]), hostbuf.push_back(B.iz[b]);
+      hostbuf.push_back(B.first[b]);
+    }
+  } else {
+    return HFMM_E_ARG;
+  }
+  if (what >= 6) bytes = (int64_t)hostbuf.size() * 8;
+  if (needed) *needed = bytes;
+  if (!host_out) return HFMM_OK;
+  if (nbytes < bytes) return HFMM_E_ARG;
+  if (what >= 6) {
+    std::memcpy(host_out, hostbuf.data(), bytes);
+    return HFMM_OK;
+  }
+  if (!src || !bytes) return HFMM_E_STATE;
+  if (cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return HFMM_E_CUDA;
+  return HFMM_OK;
+}
+
+extern "C" const char *hfmm_last_error(const hfmm_plan *p) {
+  return p ? p->err.c_str() : g_create_err.c_str();
+}
+
+extern "C" void hfmm_destroy(hfmm_plan *p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  free_levels(p);
+  free_points(p);
+  if (p->comm) ncclCommDestroy(p->comm);
+  for (auto &e : p->sev)
+    if (e) cudaEventDestroy(e);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->stream2) cudaStreamDestroy(p->stream2);
+  delete p;
+}
+
+// ---- operator entry points (BASELINE config 2 microbench) ------------------------------------
+namespace {
+struct OpCache {
+  int32_t *cbeg = nullptr, *par = nullptr;
+  int8_t *oct = nullptr;
+  int64_t n = 0;
+  void ensure(int64_t nparent) {
+    if (nparent <= n) return;
+    if (cbeg) cudaFree(cbeg), cudaFree(par), cudaFree(oct);
+    std::vector<int32_t> cb(nparent + 1), pr(nparent * 8);
+    std::vector<int8_t> oc(nparent * 8);
+    for (int64_t i = 0; i <= nparent; ++i) cb[i] = (int32_t)(8 * i);
+    for (int64_t c = 0; c < nparent * 8; ++c) pr[c] = (int32_t)(c / 8), oc[c] = (int8_t)(c % 8);
+    cbeg = dupload(cb), par = dupload(pr), oct = dupload(oc);
+    n = nparent;
+  }
+};
+OpCache &op_cache() {
+  static OpCache c;
+  return c;
+}
+int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+bool up_or_down(int nth, int nph, int nth2, int nph2, bool *up) {
+  if (nth2 >= nth && nph2 >= nph) *up = true;
+  else if (nth2 <= nth && nph2 <= nph) *up = false;
+  else return false;
+  return (nth % 2 == 0) && (nth2 % 2 == 0) && (nph % 2 == 0) && (nph2 % 2 == 0) && seven_smooth(nth) &&
+         seven_smooth(nth2) && seven_smooth(nph) && seven_smooth(nph2) && nth < 1024 && nth2 < 1024 &&
+         nph < 1024 && nph2 < 1024;
+}
+}  // namespace
+
+extern "C" int64_t hfmm_resample_workspace(int nbatch, int n_theta, int n_phi, int n_theta2, int n_phi2) {
+  bool up;
+  if (!up_or_down(n_theta, n_phi, n_theta2, n_phi2, &up)) return -1;
+  if (up) return (int64_t)nbatch * (n_theta / 2 + 1) * n_phi2 * 16;
+  return (int64_t)nbatch * n_theta2 * (n_phi / 2) * 16;
+}
+
+extern "C" int hfmm_resample(int nbatch, int nth, int nph, int nth2, int nph2, const double *in, double *out,
+                             void *work, void *stream) {
+  bool up;
+  if (nbatch < 0 || !in || !out || !up_or_down(nth, nph, nth2, nph2, &up)) return HFMM_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const TwiddleSet &tw = global_twiddles(cur_device());
+  double2 *tmp = (double2 *)work;
+  bool own = false;
+  if (!tmp) {
+    if (cudaMalloc(&tmp, hfmm_resample_workspace(nbatch, nth, nph, nth2, nph2)) != cudaSuccess) return HFMM_E_NOMEM;
+    own = true;
+  }
+  if (up) {
+    launch_rows_up((const double2 *)in, nbatch, nth, nph, nph2, tmp, tw, s);
+    launch_cols_up(tmp, nth, nph2, nth2, nullptr, 0, nullptr, nbatch, nullptr, (double2 *)out, tw, s);
+  } else {
+    launch_cols_down((const double2 *)in, nth, nph, nth2, nullptr, nullptr, nbatch, nullptr, tmp, tw, s);
+    launch_rows_down(tmp, nbatch, nth2, nph, nph2, nullptr, (double2 *)out, tw, s);
+  }
+  if (own) {
+    cudaStreamSynchronize(s);
+    cudaFree(tmp);
+  }
+  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
+}
+
+extern "C" int hfmm_m2m_op(int nparent, int nth, int nph, int nth2, int nph2, const double *child,
+                           const double *shift, double *parent, void *work, void *stream) {
+  bool up;
+  if (nparent < 0 || !child || !parent || !up_or_down(nth, nph, nth2, nph2, &up) || !up) return HFMM_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const TwiddleSet &tw = global_twiddles(cur_device());
+  OpCache &c = op_cache();
+  c.ensure(nparent);
+  double2 *tmp = (double2 *)work;
+  bool own = false;
+  if (!tmp) {
+    if (cudaMalloc(&tmp, hfmm_resample_workspace(nparent * 8, nth, nph, nth2, nph2)) != cudaSuccess) return HFMM_E_NOMEM;
+    own = true;
+  }
+  launch_rows_up((const double2 *)child, (int64_t)nparent * 8, nth, nph, nph2, tmp, tw, s);
+  launch_cols_up(tmp, nth, nph2, nth2, c.cbeg, 0, c.oct, nparent, (const double2 *)shift, (double2 *)parent, tw, s);
+  if (own) {
+    cudaStreamSynchronize(s);
+    cudaFree(tmp);
+  }
+  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
+}
+
+extern "C" int hfmm_l2l_op(int nparent, int nth, int nph, int nth2, int nph2, const double *parent,
+                           const double *shift, const double *incoming, double *child_out, void *work,
+                           void *stream) {
+  bool up;
+  if (nparent < 0 || !parent || !child_out || !up_or_down(nth, nph, nth2, nph2, &up) || up) return HFMM_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const TwiddleSet &tw = global_twiddles(cur_device());
+  OpCache &c = op_cache();
+  c.ensure(nparent);
+  double2 *tmp = (double2 *)work;
+  bool own = false;
+  if (!tmp) {
+    if (cudaMalloc(&tmp, hfmm_resample_workspace(nparent * 8, nth, nph, nth2, nph2)) != cudaSuccess) return HFMM_E_NOMEM;
+    own = true;
+  }
+  launch_cols_down((const double2 *)parent, nth, nph, nth2, c.par, c.oct, (int64_t)nparent * 8,
+                   (const double2 *)shift, tmp, tw, s);
+  launch_rows_down(tmp, (int64_t)nparent * 8, nth2, nph, nph2, (const double2 *)incoming, (double2 *)child_out, tw, s);
+  if (own) {
+    cudaStreamSynchronize(s);
+    cudaFree(tmp);
+  }
+  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
+}
+
+extern "C" int hfmm_m2l_op(int nbox, int64_t K, const int *row, const int *src, const int *oid, const double *T,
+                           const double *M, double *out, void *stream) {
+  if (nbox < 0 || K <= 0 || !row || !src || !oid || !T || !M || !out) return HFMM_E_ARG;
+  launch_m2l(0, nbox, K, row, src, oid, (const double2 *)T, (const double2 *)M, (double2 *)out,
+             (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
+}

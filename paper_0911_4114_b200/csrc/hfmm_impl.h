@@ -1,0 +1,141 @@
+// Internal declarations of libhfmm (product code; shares nothing with oracle/).
+// Citations "P:n" = line n of the paper's LaTeX source.
+#pragma once
+
+#include <cstdint>
+#include <complex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace hfmm {
+
+using cplx = std::complex<double>;
+
+// ---------------- host special functions (host_specfun.cpp) ---------------------------------
+// Spherical Bessel j_n (Miller, downward), y_n (upward), cylindrical J_n (Miller).
+void sph_bessel_j(int nmax, double x, std::vector<double> &out);
+void sph_bessel_y(int nmax, double x, std::vector<double> &out);
+void cyl_bessel_J(int nmax, double x, std::vector<double> &out);
+
+// ---------------- host plan (host_plan.cpp) -------------------------------------------------
+// c_n = (i kappa / 4 pi) i^n (2n+1) h_n(kappa |r0|)  (eqn:TransferFn)
+void transfer_series(int ell, double kappa, double r0norm, std::vector<cplx> &c);
+// Alg. 1 for one phi column: T^{s,L}(theta_p, phi), p < n_theta.
+void alg1_column(int ell, const std::vector<cplx> &c, const double r0hat[3], double phi,
+                 int n_theta, std::vector<cplx> &out);
+double collino_bound(int ell, double kappa, double r, double r0);
+int select_ell(double kappa, double r, double r0, double eps, int *ell);
+int select_ntheta(int ell, double kappa, double r, double r0, double eps, int *nth);
+int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth, int *nph,
+                std::vector<int> *ragged);
+bool seven_smooth(int n);
+
+// ---------------- tree (host_tree.cpp) ------------------------------------------------------
+struct LevelBoxes {
+  int level = 0;
+  double a = 0;
+  std::vector<uint32_t> key;       // Morton key of occupied boxes (sorted)
+  std::vector<int32_t> ix, iy, iz; // integer coordinates
+  std::vector<int64_t> first;      // first sorted point of box, size nbox+1
+  std::vector<int32_t> parent;     // index into level l-1 (or -1)
+  std::vector<int32_t> child_begin;// children range in level l+1 (size nbox+1), filled lazily
+  int64_t nbox() const { return (int64_t)key.size(); }
+  int32_t find(int x, int y, int z) const;  // -1 if not occupied
+};
+
+struct Tree {
+  int64_t n = 0;
+  int depth = 0;
+  double lo[3] = {0, 0, 0};
+  double size = 0;
+  std::vector<int64_t> perm;       // sorted position -> input index
+  std::vector<double> xs, ys, zs;  // sorted coordinates
+  std::vector<LevelBoxes> levels;  // index = level (0..depth)
+};
+
+int build_tree(const double *xyz, int64_t n, int depth, const double lo[3], double size, Tree &t,
+               std::string &err);
+uint32_t morton3(uint32_t x, uint32_t y, uint32_t z);
+// offsets: id in [0,316) <-> (ox, oy, oz) in [-3,3]^3 \ [-1,1]^3, lexicographic x, y, z
+int offset_id(int ox, int oy, int oz);
+void offset_vec(int id, int o[3]);
+
+// ---------------- device kernels (kernels_*.cu) ---------------------------------------------
+struct ResampleDims {
+  int nth, nph;    // source grid
+  int nth2, nph2;  // target grid
+};
+
+// twiddle table e^{-2 pi i t / N}, t < N, for every length of a plan (device, concatenated)
+struct TwiddleSet {
+  double2 *d = nullptr;
+  int offset[1024];  // offset[N] into d, -1 if absent (N < 1024)
+  void build(const std::vector<int> &lengths);
+  void free_all();
+};
+
+void launch_permute_q(const double2 *q_in, const int64_t *perm, double2 *q_sorted, int64_t n,
+                      cudaStream_t s);
+void launch_combine(const double2 *y_near, const double2 *y_far, const int64_t *perm,
+                    double2 *y_out, int64_t n, int64_t begin, int64_t end, cudaStream_t s);
+
+struct PointsDev {
+  const double *x, *y, *z;  // sorted coordinates
+  const double2 *q;         // sorted charges
+};
+
+// P2P over target leaves [leaf0, leaf1): targets of leaf b are points [first[b], first[b+1]);
+// sources are the point ranges of its neighbour list nb_row/nb_box (box ids of the same level).
+void launch_p2p(PointsDev pts, const int64_t *first, const int32_t *nb_row, const int32_t *nb_box,
+                int32_t leaf0, int32_t leaf1, const int32_t *tile_leaf, const int64_t *tile_begin,
+                int64_t ntiles, double kappa, double2 *y_near, cudaStream_t s);
+
+// S2M: M[b][k] = sum_j q_j e^{i kappa s_k.(x_j - c_b)}
+void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
+                const double *cz, int32_t box0, int32_t box1, const double *ks /*[3][K]*/,
+                int64_t K, double2 *M, cudaStream_t s);
+
+// L2T: y_far[i] = w sum_k L[b][k] e^{i kappa s_k.(c_b - x_i)}
+void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
+                const double *cz, const int32_t *tile_leaf, const int64_t *tile_begin,
+                int64_t ntiles, const double *ks, int64_t K, const double2 *L, double w,
+                double2 *y_far, cudaStream_t s);
+
+// M2L: I[a][k] = sum_e T[oid_e][k] M[src_e][k]
+void launch_m2l(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
+                const int32_t *oid, const double2 *T, const double2 *M, double2 *I,
+                cudaStream_t s);
+
+// Fourier resampling building blocks, warp-per-sequence shared-memory FFTs.
+// Row pass of an upward resample: for each box b and row n <= nth/2, full row of length nph
+// (stored rows n and (nth-n)%nth) resampled to nph2 -> tmp[b][n][0..nph2).
+void launch_rows_up(const double2 *in, int64_t nbox, int nth, int nph, int nph2, double2 *tmp,
+                    const TwiddleSet &tw, cudaStream_t s);
+// Column pass of an upward resample with child accumulation: for parent p and column
+// m < nph2/2: out[p][.][m] = sum_{c in children(p)} shift[oct(c)][.][m] * R_theta(col_c).
+// child ids of parent p: [cbeg[p], cbeg[p+1]) (cbeg == nullptr: child p only, shift
+// optional), tmp row of child c is c - cbase, oct: child octant (0..7, absolute c) or nullptr.
+void launch_cols_up(const double2 *tmp, int nth, int nph2, int nth2, const int32_t *cbeg,
+                    int64_t cbase, const int8_t *oct, int64_t nparent, const double2 *shift, double2 *out,
+                    const TwiddleSet &tw, cudaStream_t s);
+// Column pass of a downward resample: for child c (parent par[c]) and column m < nph/2:
+// tmp[c][.][m] = R_theta(conj(shift[oct(c)]) * in[par[c]])[.][m]   (nth -> nth2)
+void launch_cols_down(const double2 *in, int nth, int nph, int nth2, const int32_t *par,
+                      const int8_t *oct, int64_t nchild, const double2 *shift, double2 *tmp,
+                      const TwiddleSet &tw, cudaStream_t s);
+// Row pass of a downward resample: rows n <= nth2/2 of tmp (length nph via symmetry),
+// resampled to nph2, written to out (half storage) + add (optional).
+void launch_rows_down(const double2 *tmp, int64_t nbox, int nth2, int nph, int nph2,
+                      const double2 *add, double2 *out, const TwiddleSet &tw, cudaStream_t s);
+
+// Alg. 1 transfer tables on the GPU (precompute).
+void launch_alg1_tables(const double2 *coef /*[nr][ell+1]*/, const int32_t *coef_of_offset,
+                        const double *r0hat /*[316][3]*/, int ell, int nth, int nphf, int qcount,
+                        double2 *out /*[316][nth][qcount]*/, cudaStream_t s);
+void launch_phi_anterp(const double2 *full /*[316][nth][nphf]*/, int nth, int nphf, int nph,
+                       double2 *out /*[316][nth][nph/2]*/, cudaStream_t s);
+void launch_absmax(const double2 *v, int64_t n, double *out /*device, 1 value*/, cudaStream_t s);
+
+}  // namespace hfmm

@@ -1,0 +1,177 @@
+// Octree in Morton order (product code).
+//   P:33   root level 0, a_l = a_0 / 2^l
+//   P:114  boxes B^l_alpha with centres c^l_alpha; leaves own contiguous point ranges
+// Points are sorted by the Morton key of their depth-D box (ties: input index), so every
+// box of every level l <= D owns one contiguous range of the sorted arrays.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <string>
+
+#include "hfmm_impl.h"
+#include "../../include/hfmm.h"
+
+namespace hfmm {
+
+static inline uint32_t spread3(uint32_t v) {  // 10 bits -> every third bit
+  v &= 0x3ff;
+  v = (v | (v << 16)) & 0x030000FF;
+  v = (v | (v << 8)) & 0x0300F00F;
+  v = (v | (v << 4)) & 0x030C30C3;
+  v = (v | (v << 2)) & 0x09249249;
+  return v;
+}
+
+uint32_t morton3(uint32_t x, uint32_t y, uint32_t z) {
+  return (spread3(x) << 2) | (spread3(y) << 1) | spread3(z);
+}
+
+int32_t LevelBoxes::find(int x, int y, int z) const {
+  const int n = 1 << level;
+  if (x < 0 || y < 0 || z < 0 || x >= n || y >= n || z >= n) return -1;
+  uint32_t k = morton3((uint32_t)x, (uint32_t)y, (uint32_t)z);
+  auto it = std::lower_bound(key.begin(), key.end(), k);
+  if (it == key.end() || *it != k) return -1;
+  return (int32_t)(it - key.begin());
+}
+
+int offset_id(int ox, int oy, int oz) {
+  // lexicographic enumeration of [-3,3]^3 minus [-1,1]^3
+  int id = 0;
+  for (int x = -3; x <= 3; ++x)
+    for (int y = -3; y <= 3; ++y)
+      for (int z = -3; z <= 3; ++z) {
+        if (std::max(std::abs(x), std::max(std::abs(y), std::abs(z))) < 2) continue;
+        if (x == ox && y == oy && z == oz) return id;
+        ++id;
+      }
+  return -1;
+}
+
+void offset_vec(int id, int o[3]) {
+  int k = 0;
+  for (int x = -3; x <= 3; ++x)
+    for (int y = -3; y <= 3; ++y)
+      for (int z = -3; z <= 3; ++z) {
+        if (std::max(std::abs(x), std::max(std::abs(y), std::abs(z))) < 2) continue;
+        if (k == id) {
+          o[0] = x, o[1] = y, o[2] = z;
+          return;
+        }
+        ++k;
+      }
+}
+
+int build_tree(const double *xyz, int64_t n, int depth, const double lo[3], double size, Tree &t,
+               std::string &err) {
+  if (n <= 0 || depth < 2 || depth > 10 || !(size > 0) || !std::isfinite(size)) {
+    err = "build_tree: need n > 0, 2 <= depth <= 10, finite size > 0";
+    return HFMM_E_ARG;
+  }
+  for (int d = 0; d < 3; ++d)
+    if (!std::isfinite(lo[d])) {
+      err = "build_tree: non-finite root corner";
+      return HFMM_E_ARG;
+    }
+  t = Tree();
+  t.n = n;
+  t.depth = depth;
+  t.size = size;
+  for (int d = 0; d < 3; ++d) t.lo[d] = lo[d];
+  const int nb = 1 << depth;
+  const double a = size / nb;
+  std::vector<uint32_t> key(n);
+  for (int64_t i = 0; i < n; ++i) {
+    int b[3];
+    for (int d = 0; d < 3; ++d) {
+      double v = xyz[3 * i + d];
+      if (!std::isfinite(v)) {
+        err = "build_tree: non-finite coordinate at point " + std::to_string(i);
+        return HFMM_E_ARG;
+      }
+      double u = std::floor((v - lo[d]) / a);
+      if (u < 0 || v > lo[d] + size) {
+        err = "build_tree: point " + std::to_string(i) + " outside the root cube";
+        return HFMM_E_DOMAIN;
+      }
+      b[d] = std::min((int)u, nb - 1);
+    }
+    key[i] = morton3(b[0], b[1], b[2]);
+  }
+  t.perm.resize(n);
+  std::iota(t.perm.begin(), t.perm.end(), 0);
+  std::stable_sort(t.perm.begin(), t.perm.end(), [&](int64_t u, int64_t v) { return key[u] < key[v]; });
+  t.xs.resize(n), t.ys.resize(n), t.zs.resize(n);
+  std::vector<uint32_t> skey(n);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t j = t.perm[i];
+    t.xs[i] = xyz[3 * j], t.ys[i] = xyz[3 * j + 1], t.zs[i] = xyz[3 * j + 2];
+    skey[i] = key[j];
+  }
+  // exact duplicates (kernel undefined): identical points share a leaf key
+  {
+    int64_t i = 0;
+    while (i < n) {
+      int64_t e = i;
+      while (e < n && skey[e] == skey[i]) ++e;
+      if (e - i > 1) {
+        std::vector<int64_t> idx(e - i);
+        std::iota(idx.begin(), idx.end(), i);
+        std::sort(idx.begin(), idx.end(), [&](int64_t u, int64_t v) {
+          if (t.xs[u] != t.xs[v]) return t.xs[u] < t.xs[v];
+          if (t.ys[u] != t.ys[v]) return t.ys[u] < t.ys[v];
+          return t.zs[u] < t.zs[v];
+        });
+        for (size_t k = 1; k < idx.size(); ++k) {
+          int64_t u = idx[k - 1], v = idx[k];
+          if (t.xs[u] == t.xs[v] && t.ys[u] == t.ys[v] && t.zs[u] == t.zs[v]) {
+            err = "build_tree: coincident points (input " + std::to_string(t.perm[u]) + ", " +
+                  std::to_string(t.perm[v]) + ")";
+            return HFMM_E_COINCIDENT;
+          }
+        }
+      }
+      i = e;
+    }
+  }
+  t.levels.resize(depth + 1);
+  for (int l = 0; l <= depth; ++l) {
+    LevelBoxes &L = t.levels[l];
+    L.level = l;
+    L.a = size / (double)(1 << l);
+    const int shift = 3 * (depth - l);
+    int64_t i = 0;
+    while (i < n) {
+      uint32_t k = skey[i] >> shift;
+      L.key.push_back(k);
+      L.first.push_back(i);
+      while (i < n && (skey[i] >> shift) == k) ++i;
+    }
+    L.first.push_back(n);
+    for (uint32_t k : L.key) {
+      uint32_t x = 0, y = 0, z = 0;
+      for (int b = 0; b < l; ++b) {
+        x |= ((k >> (3 * b + 2)) & 1u) << b;
+        y |= ((k >> (3 * b + 1)) & 1u) << b;
+        z |= ((k >> (3 * b + 0)) & 1u) << b;
+      }
+      L.ix.push_back(x), L.iy.push_back(y), L.iz.push_back(z);
+    }
+  }
+  for (int l = 1; l <= depth; ++l) {
+    LevelBoxes &L = t.levels[l];
+    const LevelBoxes &P = t.levels[l - 1];
+    L.parent.resize(L.nbox());
+    for (int64_t b = 0; b < L.nbox(); ++b) L.parent[b] = P.find(L.ix[b] >> 1, L.iy[b] >> 1, L.iz[b] >> 1);
+  }
+  for (int l = 0; l < depth; ++l) {
+    LevelBoxes &L = t.levels[l];
+    const LevelBoxes &C = t.levels[l + 1];
+    L.child_begin.assign(L.nbox() + 1, 0);
+    for (int64_t c = 0; c < C.nbox(); ++c) L.child_begin[C.parent[c] + 1]++;
+    for (int64_t b = 0; b < L.nbox(); ++b) L.child_begin[b + 1] += L.child_begin[b];
+  }
+  return 0;
+}
+
+}  // namespace hfmm

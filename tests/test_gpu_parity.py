@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the independent CPU oracle.
+
+Tolerances:
+  - whole matvec vs oracle: relative L2 <= 1e-11 (BASELINE north_star), on the same plan
+  - stage buffers (M, I, L, y_near, y_far) vs oracle: relative <= 1e-11 (normwise)
+  - FMM vs direct summation: relative L2 <= eps
+  - integer plan (ell, N_theta, N_phi, L_f): identical
+"""
+import math
+
+import numpy as np
+import pytest
+
+from workloads import CONFIGS, small_config, points_and_charges
+from oracle.plan import make_plan
+from oracle.fmm import OracleFMM
+from oracle.direct import direct_sum
+from oracle.transfer import bmtf_table, offsets316
+
+pytestmark = pytest.mark.gpu
+
+PARITY = 1e-11
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
+
+
+@pytest.fixture(scope="module")
+def hf():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_0911_4114_b200 as mod
+    from paper_0911_4114_b200.build import build
+    build(verbose=False)
+    return mod
+
+
+def gpu_plan(hf, cfg, x, **kw):
+    g = hf.HFMM(0)
+    g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha, **kw)
+    return g
+
+
+def check_plan(g, plan):
+    info = g.info()
+    assert info["L_f"] == plan.L_f
+    for lv in info["levels"]:
+        op = plan.levels[lv["level"]]
+        assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (op.ell, op.n_theta, op.n_phi), lv["level"]
+        if lv["level"] <= (plan.L_f or 1) + 1 and not math.isnan(op.F):
+            assert lv["active"] == op.active
+            assert abs(lv["F"] - op.F) <= 1e-6 * op.F
+    return info
+
+
+def box_map(g, f, level):
+    """GPU (Morton) box order -> oracle box index."""
+    tab = g.debug(7, level)
+    lev = f.levels[level]
+    return np.array([lev.index[(int(r[0]), int(r[1]), int(r[2]))] for r in tab])
+
+
+# ------------------------------------------------------------------------------------------
+def test_c1_policy_run_is_direct_sum(hf):
+    """BASELINE config 0 (C1): no admissible level -> the matvec is the direct sum."""
+    cfg = CONFIGS["C1"]
+    x, q = points_and_charges(cfg)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+    g = gpu_plan(hf, cfg, x)
+    assert g.last_rc == hf.HFMM_W_NO_FARFIELD
+    check_plan(g, plan)
+    y = g.matvec(q)
+    yd = direct_sum(x, q, cfg.kappa)
+    assert rel(y, yd) <= PARITY
+    assert rel(g.direct(q), yd) <= PARITY
+
+
+@pytest.fixture(scope="module")
+def small(hf):
+    cfg = small_config("small", n=777, kappa=32 * math.pi, depth=3, eps=1e-6, seed=21)
+    x, q = points_and_charges(cfg)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+    f = OracleFMM(x, cfg.lo, cfg.size, plan)
+    g = gpu_plan(hf, cfg, x)
+    y = g.matvec(q)
+    return cfg, x, q, plan, f, g, y
+
+
+def test_small_plan_identical(small):
+    cfg, x, q, plan, f, g, y = small
+    assert plan.L_f == 3
+    check_plan(g, plan)
+
+
+def test_small_transfer_tables(small):
+    cfg, x, q, plan, f, g, y = small
+    offs = offsets316()
+    for l in (2, 3):
+        T = g.debug(3, l).reshape(316, -1)
+        lp = plan.levels[l]
+        for oid in (0, 57, 123, 200, 315):
+            ref = bmtf_table(lp.ell, cfg.kappa, offs[oid] * lp.a, lp.n_theta, lp.n_phi).reshape(-1)
+            assert rel(T[oid], ref) <= 1e-12
+
+
+def test_small_stages(small):
+    cfg, x, q, plan, f, g, y = small
+    M, I, Lloc = f.far_locals(q)
+    for l in (2, 3):
+        mp = box_map(g, f, l)
+        K = plan.levels[l].K
+        Mg = g.debug(0, l).reshape(-1, K)
+        Mo = np.stack([M[l][mp[b]] for b in range(len(mp))])
+        assert rel(Mg, Mo) <= PARITY, f"M_{l}"
+        Ig = g.debug(1, l).reshape(-1, K)
+        Io = np.stack([I[l][mp[b]] for b in range(len(mp))])
+        assert rel(Ig, Io) <= PARITY, f"I_{l}"
+        Lg = g.debug(2, l).reshape(-1, K)
+        Lo = np.stack([Lloc[l][mp[b]] for b in range(len(mp))])
+        assert rel(Lg, Lo) <= PARITY, f"L_{l}"
+
+
+def test_small_matvec_parity_and_accuracy(small):
+    cfg, x, q, plan, f, g, y = small
+    yo = f.matvec(q)
+    assert rel(y, yo) <= PARITY
+    yd = direct_sum(x, q, cfg.kappa)
+    assert rel(y, yd) <= cfg.eps
+    perm = g.debug(6)
+    yn_o, yf_o = f.matvec(q, parts=True)
+    assert rel(g.debug(4)[: len(q)], yn_o[perm]) <= PARITY
+    assert rel(g.debug(5)[: len(q)], yf_o[perm]) <= PARITY
+
+
+def test_small_repeat_and_device_path(small, hf):
+    import torch
+    cfg, x, q, plan, f, g, y = small
+    y2 = g.matvec(q)
+    assert np.array_equal(y, y2)                       # run-to-run bitwise reproducible
+    qt = torch.from_numpy(q).cuda()
+    yt = g.matvec(qt)
+    torch.cuda.synchronize()
+    assert np.array_equal(yt.cpu().numpy(), y)
+
+
+def test_small_linearity(small):
+    cfg, x, q, plan, f, g, y = small
+    rng = np.random.default_rng(3)
+    q2 = rng.standard_normal(len(q)) + 1j * rng.standard_normal(len(q))
+    lhs = g.matvec(2.0 * q - 1j * q2)
+    rhs = 2.0 * y - 1j * g.matvec(q2)
+    assert rel(lhs, rhs) < 1e-13
+
+
+def test_single_level_cube(hf):
+    """Cube geometry, one active level (L_f = 2), ragged tail sizes."""
+    cfg = small_config("cube", kind="cube", n=1001, kappa=24 * math.pi, depth=3, eps=1e-6, seed=5)
+    x, q = points_and_charges(cfg)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+    g = gpu_plan(hf, cfg, x)
+    check_plan(g, plan)
+    f = OracleFMM(x, cfg.lo, cfg.size, plan)
+    y = g.matvec(q)
+    assert rel(y, f.matvec(q)) <= PARITY
+    assert rel(y, direct_sum(x, q, cfg.kappa)) <= cfg.eps
+
+
+def test_forced_breakdown_levels_run(hf):
+    """HFMM_FORCE_ALL_LEVELS on C1 (P:833 breakdown demonstration): runs, reports F_l."""
+    cfg = CONFIGS["C1"]
+    x, q = points_and_charges(cfg)
+    g = gpu_plan(hf, cfg, x, flags=hf.HFMM_FORCE_ALL_LEVELS)
+    info = g.info()
+    assert info["L_f"] == 3
+    assert info["levels"][1]["F"] > 1e3          # lambda/4 boxes: roundoff amplification >> 1
+    y = g.matvec(q)
+    assert np.all(np.isfinite(y))
+
+
+def test_edge_cases(hf):
+    g = hf.HFMM(0)
+    # single point: y = 0 (no j != i)
+    g.build_tree(np.array([[0.1, 0.2, 0.3]]), 2, (-1, -1, -1), 2.0)
+    g.precompute(10.0, 1e-6)
+    assert np.all(g.matvec(np.array([1 + 1j])) == 0)
+    # two points
+    x = np.array([[0.0, 0, 0], [0.3, 0.4, 0.0]])
+    g.build_tree(x, 2, (-1, -1, -1), 2.0)
+    g.precompute(7.0, 1e-6)
+    y = g.matvec(np.array([1 + 0j, 2 + 0j]))
+    e = np.exp(1j * 3.5) / 0.5
+    assert np.allclose(y, [2 * e, e], rtol=1e-14)
+    # errors
+    with pytest.raises(hf.HFMMError):
+        g.build_tree(np.array([[3.0, 0, 0]]), 2, (-1, -1, -1), 2.0)      # outside the root cube
+    with pytest.raises(hf.HFMMError):
+        g.build_tree(np.array([[0.1, 0, 0], [0.1, 0, 0]]), 2, (-1, -1, -1), 2.0)  # coincident
+    with pytest.raises(hf.HFMMError):
+        g.build_tree(np.array([[0.1, 0, 0]]), 1, (-1, -1, -1), 2.0)      # depth < 2
+    with pytest.raises(hf.HFMMError):
+        g.matvec(np.array([1 + 0j]))                                     # state: no tree
+    g.build_tree(x, 2, (-1, -1, -1), 2.0)
+    with pytest.raises(hf.HFMMError):
+        g.precompute(-1.0, 1e-6)
+
+
+@pytest.mark.parametrize("up", [True, False])
+@pytest.mark.parametrize("grids", [((16, 16), (24, 28)), ((90, 96), (120, 120)), ((54, 56), (108, 108))])
+def test_resample_operator(hf, up, grids):
+    import torch
+    from oracle.resample import resample_half_batch
+    (a, b) = grids if up else grids[::-1]
+    rng = np.random.default_rng(7)
+    F = rng.standard_normal((5, a[0], a[1] // 2)) + 1j * rng.standard_normal((5, a[0], a[1] // 2))
+    inp = torch.from_numpy(F).cuda()
+    out = torch.empty((5, b[0], b[1] // 2), dtype=torch.complex128, device="cuda")
+    hf.resample(inp, a[0], a[1], b[0], b[1], out)
+    torch.cuda.synchronize()
+    ref = resample_half_batch(F, a[1], b[0], b[1])
+    assert rel(out.cpu().numpy(), ref) <= 1e-13
