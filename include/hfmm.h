@@ -123,9 +123,11 @@ int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double alpha, double
 
 /* y = A q (eqn:HelmholtzMatrixVector).  q: n complex128 in INPUT order, y: n complex128 in
  * input order.  mem = HFMM_HOST or HFMM_DEVICE (optionally | HFMM_Y_LOCAL).  stream: a
- * cudaStream_t on the plan's device, or NULL for the plan's own stream.  For HFMM_HOST the
- * call returns after y is written; for HFMM_DEVICE it returns after enqueueing (y valid once
- * `stream` completes). */
+ * cudaStream_t on the plan's device (cudaStreamLegacy = (void*)1 for the legacy default
+ * stream), or NULL for the plan's own stream.  The call returns after y is written for
+ * HFMM_HOST and for a NULL stream; for HFMM_DEVICE with an explicit stream it returns after
+ * enqueueing (y valid once `stream` reaches that point).  Input q is read, and y written, in
+ * stream order on `stream`. */
 int hfmm_matvec(hfmm_plan *p, const double *q, double *y, int mem, void *stream);
 
 /* Direct O(n^2) sum on the GPU (same P2P kernel over all pairs), same conventions. */

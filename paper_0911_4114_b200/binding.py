@@ -170,13 +170,15 @@ class HFMM:
             if out is None:
                 out = torch.empty_like(q)
             s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+            if not s:
+                s = 1  # torch's default stream is the legacy default stream (cudaStreamLegacy)
             self._check(fn(self.h, q.data_ptr(), out.data_ptr(), HFMM_DEVICE | mem_local, C.c_void_p(s)))
             return out
         if hasattr(q, "data_ptr"):  # CPU torch tensor (pinned or pageable): host path
             import torch
             if out is None:
                 out = torch.empty_like(q)
-            s = None if stream is None else C.c_void_p(stream)
+            s = None if stream is None else C.c_void_p(stream or 1)  # 0 -> cudaStreamLegacy
             self._check(fn(self.h, q.data_ptr(), out.data_ptr(), HFMM_HOST | mem_local, s))
             return out
         q = np.ascontiguousarray(q, dtype=np.complex128)
@@ -227,8 +229,8 @@ class HFMM:
 def _stream(stream):
     if stream is None:
         import torch
-        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    return C.c_void_p(stream)
+        stream = torch.cuda.current_stream().cuda_stream
+    return C.c_void_p(stream or 1)  # 0 (torch default stream) -> cudaStreamLegacy
 
 
 def resample(inp, nth, nph, nth2, nph2, out, work=None, stream=None):

@@ -24,6 +24,7 @@ namespace {
 
 const double kPi = 3.14159265358979323846;
 const double kURound = 1.1102230246251565e-16;  // 2^-53
+const int64_t kTile = 256;                       // targets per P2P / L2T tile (2 per thread)
 
 struct LevelDev {
   int l = 0;
@@ -255,7 +256,7 @@ extern "C" int hfmm_build_tree(hfmm_plan *p, int64_t n, const double *xyz, int d
   {
     std::vector<int32_t> tl;
     std::vector<int64_t> tb;
-    for (int64_t s = 0; s < n; s += 128) tl.push_back(0), tb.push_back(s);
+    for (int64_t s = 0; s < n; s += kTile) tl.push_back(0), tb.push_back(s);
     p->dir_tile_leaf = dupload(tl);
     p->dir_tile_begin = dupload(tb);
     p->dir_ntiles = (int64_t)tl.size();
@@ -363,7 +364,7 @@ static void partition(hfmm_plan *p) {
     const int64_t n = t.n;
     auto cutp = [&](int k) -> int64_t {
       if (k >= R) return n;
-      int64_t c = (n * k / R) / 128 * 128;   // tile-aligned (P2P tiles are 128 targets)
+      int64_t c = (n * k / R) / kTile * kTile;   // tile-aligned (P2P tiles are kTile targets)
       return std::min(c, n);
     };
     p->own_pt0 = cutp(r);
@@ -576,7 +577,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     std::vector<int32_t> tl;
     std::vector<int64_t> tb;
     for (int64_t b = lo; b < hi; ++b)
-      for (int64_t s = B.first[b]; s < B.first[b + 1]; s += 128) {
+      for (int64_t s = B.first[b]; s < B.first[b + 1]; s += kTile) {
         if (p->L_f < 0 && (s < p->own_pt0 || s >= p->own_pt1)) continue;
         tl.push_back((int32_t)b), tb.push_back(s);
       }
@@ -747,6 +748,7 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
     CK(cudaStreamSynchronize(s));
   } else {
     CK(cudaMemcpyAsync(y, p->y_out, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    if (!stream) CK(cudaStreamSynchronize(s));  // plan's own stream: complete before returning
   }
   if (p->profile && !direct) {
     CK(cudaStreamSynchronize(s));

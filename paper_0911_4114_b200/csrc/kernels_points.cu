@@ -3,77 +3,122 @@
 //   S2M  initialisation M^L_a(s) = sum psi_i e^{i kappa s.(x_i - c_a)}
 //   L2T  field computation int L e^{i kappa s.(c_a - x_i)} dS
 //   permute / combine (Morton order <-> caller order)
-// All three main kernels are bound by the FP64 pipe (one complex exponential per pair or per
-// (point, direction)); the exponential is computed by hfmm_cexpi() below: a 2-part Cody-Waite
-// reduction by 2 pi / 256, a 256-entry table of e^{2 pi i t/256} in shared memory and
-// short minimax-free Taylor polynomials on |r| <= pi/256 (|error| < 2 ulp).
+// The three main kernels are bound by the FP64 pipe: one complex exponential per pair or per
+// (point, direction).  e^{ix} (cexpi below): round x to the nearest multiple of 2 pi/1024 with
+// the 1.5 * 2^52 "magic number" (no FRND/F2I), 2-part Cody-Waite remainder |r| <= pi/1024,
+// table e^{2 pi i k/1024} in shared memory, Taylor polynomials of degree 5 (sin) and 4 (cos)
+// whose truncation error (< 2e-18) is below the double rounding of the result.  14 FP64
+// instructions.  Each thread evaluates two items per source (ILP and source-load reuse).
 #include <cuda_runtime.h>
-#include <cstdint>
 #include <algorithm>
+#include <cstdint>
 
 #include "hfmm_impl.h"
 
 namespace hfmm {
 
-#define HFMM_TABLE 256
+constexpr int TAB = 1024;
+constexpr double kInvStep = 162.97466172610082;       // 1024 / (2 pi)
+constexpr double kMagic = 6755399441055744.0;          // 1.5 * 2^52
+constexpr double kS3 = -1.0 / 6.0, kS5 = 1.0 / 120.0;
+constexpr double kC2 = -0.5, kC4 = 1.0 / 24.0;
 
-// 2 pi / 256 split for Cody-Waite: hi has 24 significant bits (a float), so k * hi is exact
-// for |k| < 2^29; lo = 2 pi / 256 - hi.
-static constexpr double kInvStep = 40.743665431525205956834243423364;   // 256 / (2 pi)
 static void step_split(double *hi, double *lo) {
-  const double step = 6.283185307179586476925286766559 / 256.0;
-  *hi = (double)(float)step;
+  const double step = 6.283185307179586476925286766559 / TAB;
+  *hi = (double)(float)step;  // 24 significant bits: k * hi exact for |k| < 2^29
   *lo = step - *hi;
 }
 
-// Exact e^{i 2 pi t / 256} table, filled once per block.
+struct ExpConsts {
+  double shi, slo;
+};
+
 __device__ __forceinline__ void fill_exp_table(double2 *tab) {
-  for (int t = threadIdx.x; t < HFMM_TABLE; t += blockDim.x) {
+  for (int t = threadIdx.x; t < TAB; t += blockDim.x) {
     double s, c;
-    sincospi((double)t / (HFMM_TABLE / 2), &s, &c);
+    sincospi((double)t / (TAB / 2), &s, &c);
     tab[t] = make_double2(c, s);
   }
 }
 
-// e^{i x} for |x| < 2^20: x = k (2 pi / 256) + r, e^{ix} = tab[k mod 256] * e^{ir}
-__device__ __forceinline__ double2 cexpi_tab(double x, const double2 *__restrict__ tab, double shi,
-                                             double slo) {
-  double kd = rint(x * kInvStep);
-  double r = fma(-kd, shi, x);
-  r = fma(-kd, slo, r);
-  int k = ((int)kd) & (HFMM_TABLE - 1);
-  double r2 = r * r;
-  // sin r = r (1 - r^2/6 + r^4/120 - r^6/5040), cos r = 1 - r^2/2 + r^4/24 - r^6/720
-  double sp = fma(r2, fma(r2, fma(r2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), 1.0);
-  double sr = r * sp;
-  double cr = fma(r2, fma(r2, fma(r2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
-  double2 e = tab[k];
-  return make_double2(fma(e.x, cr, -e.y * sr), fma(e.x, sr, e.y * cr));
+__device__ __forceinline__ double2 cexpi(double x, const double2 *__restrict__ tab, const ExpConsts &ec) {
+  const double t = fma(x, kInvStep, kMagic);
+  const int k = __double2loint(t);
+  const double kd = t - kMagic;
+  double r = fma(-kd, ec.shi, x);
+  r = fma(-kd, ec.slo, r);
+  const double r2 = r * r;
+  const double s = fma(r * r2, fma(r2, kS5, kS3), r);
+  const double c = fma(r2, fma(r2, kC4, kC2), 1.0);
+  const double2 e = tab[k & (TAB - 1)];
+  return make_double2(fma(e.x, c, -e.y * s), fma(e.x, s, e.y * c));
+}
+
+// 1/sqrt(r2) for r2 > 0: hardware approximation of the high word, one cubic Newton step.
+__device__ __forceinline__ double rsqrt_fast(double r2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  const double e = fma(-r2, y * y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
 }
 
 // ---------------------------------------------------------------------------------------------
-// P2P: one thread per target, sources of every neighbour box streamed through shared memory.
+// P2P: tile = up to 256 targets of one leaf (2 per thread); sources of every neighbour box
+// streamed through shared memory in chunks of 128.
 // ---------------------------------------------------------------------------------------------
 constexpr int P2P_TPB = 128;
 
-__global__ void __launch_bounds__(P2P_TPB) p2p_kernel(PointsDev pts, const int64_t *__restrict__ first,
-                                                      const int32_t *__restrict__ nb_row,
-                                                      const int32_t *__restrict__ nb_box,
-                                                      const int32_t *__restrict__ tile_leaf,
-                                                      const int64_t *__restrict__ tile_begin,
-                                                      double kappa, double shi, double slo,
-                                                      double2 *__restrict__ y_near) {
-  __shared__ double2 tab[HFMM_TABLE];
+template <bool DIAG>
+__device__ __forceinline__ void p2p_chunk(int cnt, const double *sx, const double *sy, const double *sz,
+                                          const double2 *sq, double x0, double y0, double z0, double x1,
+                                          double y1, double z1, double kappa, const double2 *tab,
+                                          const ExpConsts &ec, double &a0r, double &a0i, double &a1r,
+                                          double &a1i) {
+#pragma unroll 2
+  for (int u = 0; u < cnt; ++u) {
+    const double xs = sx[u], ys = sy[u], zs = sz[u];
+    const double2 q = sq[u];
+    {
+      const double dx = x0 - xs, dy = y0 - ys, dz = z0 - zs;
+      const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+      double ri = rsqrt_fast(r2);
+      if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;  // self pair excluded
+      const double2 e = cexpi(kappa * (r2 * ri), tab, ec);
+      const double gr = e.x * ri, gi = e.y * ri;
+      a0r = fma(gr, q.x, fma(-gi, q.y, a0r));
+      a0i = fma(gr, q.y, fma(gi, q.x, a0i));
+    }
+    {
+      const double dx = x1 - xs, dy = y1 - ys, dz = z1 - zs;
+      const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+      double ri = rsqrt_fast(r2);
+      if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;
+      const double2 e = cexpi(kappa * (r2 * ri), tab, ec);
+      const double gr = e.x * ri, gi = e.y * ri;
+      a1r = fma(gr, q.x, fma(-gi, q.y, a1r));
+      a1i = fma(gr, q.y, fma(gi, q.x, a1i));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(P2P_TPB, 5) p2p_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                         const int32_t *__restrict__ nb_row,
+                                                         const int32_t *__restrict__ nb_box,
+                                                         const int32_t *__restrict__ tile_leaf,
+                                                         const int64_t *__restrict__ tile_begin,
+                                                         double kappa, ExpConsts ec,
+                                                         double2 *__restrict__ y_near) {
+  __shared__ double2 tab[TAB];
   __shared__ double sx[P2P_TPB], sy[P2P_TPB], sz[P2P_TPB];
   __shared__ double2 sq[P2P_TPB];
   fill_exp_table(tab);
   const int32_t leaf = tile_leaf[blockIdx.x];
-  const int64_t t0 = tile_begin[blockIdx.x];
   const int64_t tend = first[leaf + 1];
-  const int64_t i = t0 + threadIdx.x;
-  const bool active = i < tend;
-  const double xi = active ? pts.x[i] : 0.0, yi = active ? pts.y[i] : 0.0, zi = active ? pts.z[i] : 0.0;
-  double ar = 0.0, ai = 0.0;
+  const int64_t i0 = tile_begin[blockIdx.x] + threadIdx.x, i1 = i0 + P2P_TPB;
+  // inactive lanes evaluate far-away dummy targets (results discarded)
+  const double x0 = i0 < tend ? pts.x[i0] : 1e30, y0 = i0 < tend ? pts.y[i0] : 0.0, z0 = i0 < tend ? pts.z[i0] : 0.0;
+  const double x1 = i1 < tend ? pts.x[i1] : 1e30, y1 = i1 < tend ? pts.y[i1] : 0.0, z1 = i1 < tend ? pts.z[i1] : 0.0;
+  double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
   for (int32_t e = nb_row[leaf]; e < nb_row[leaf + 1]; ++e) {
     const int32_t b = nb_box[e];
     const int64_t s0 = first[b], s1 = first[b + 1];
@@ -88,55 +133,48 @@ __global__ void __launch_bounds__(P2P_TPB) p2p_kernel(PointsDev pts, const int64
         sq[threadIdx.x] = pts.q[j];
       }
       __syncthreads();
-#pragma unroll 4
-      for (int u = 0; u < cnt; ++u) {
-        const double dx = xi - sx[u], dy = yi - sy[u], dz = zi - sz[u];
-        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-        const double rinv = (r2 > 0.0) ? rsqrt(r2) : 0.0;       // self pair excluded
-        const double2 e = cexpi_tab(kappa * (r2 * rinv), tab, shi, slo);
-        const double gr = e.x * rinv, gi = e.y * rinv;
-        const double2 q = sq[u];
-        ar = fma(gr, q.x, fma(-gi, q.y, ar));
-        ai = fma(gr, q.y, fma(gi, q.x, ai));
-      }
+      if (b == leaf)
+        p2p_chunk<true>(cnt, sx, sy, sz, sq, x0, y0, z0, x1, y1, z1, kappa, tab, ec, a0r, a0i, a1r, a1i);
+      else
+        p2p_chunk<false>(cnt, sx, sy, sz, sq, x0, y0, z0, x1, y1, z1, kappa, tab, ec, a0r, a0i, a1r, a1i);
     }
   }
-  if (active) y_near[i] = make_double2(ar, ai);
+  if (i0 < tend) y_near[i0] = make_double2(a0r, a0i);
+  if (i1 < tend) y_near[i1] = make_double2(a1r, a1i);
 }
 
 void launch_p2p(PointsDev pts, const int64_t *first, const int32_t *nb_row, const int32_t *nb_box,
                 int32_t, int32_t, const int32_t *tile_leaf, const int64_t *tile_begin,
                 int64_t ntiles, double kappa, double2 *y_near, cudaStream_t s) {
   if (ntiles <= 0) return;
-  double shi, slo;
-  step_split(&shi, &slo);
-  p2p_kernel<<<(unsigned)ntiles, P2P_TPB, 0, s>>>(pts, first, nb_row, nb_box, tile_leaf, tile_begin,
-                                                   kappa, shi, slo, y_near);
+  ExpConsts ec;
+  step_split(&ec.shi, &ec.slo);
+  p2p_kernel<<<(unsigned)ntiles, P2P_TPB, 0, s>>>(pts, first, nb_row, nb_box, tile_leaf, tile_begin, kappa, ec,
+                                                   y_near);
 }
 
 // ---------------------------------------------------------------------------------------------
-// S2M: thread per direction k, leaf points streamed through shared memory.
+// S2M: two directions per thread (k, k + 128), leaf points streamed through shared memory.
 // ---------------------------------------------------------------------------------------------
 constexpr int S2M_TPB = 128;
 
-__global__ void __launch_bounds__(S2M_TPB) s2m_kernel(PointsDev pts, const int64_t *__restrict__ first,
-                                                      const double *__restrict__ cx,
-                                                      const double *__restrict__ cy,
-                                                      const double *__restrict__ cz, int32_t box0,
-                                                      const double *__restrict__ ks, int64_t K,
-                                                      double shi, double slo,
-                                                      double2 *__restrict__ M) {
-  __shared__ double2 tab[HFMM_TABLE];
+__global__ void __launch_bounds__(S2M_TPB, 5) s2m_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                         const double *__restrict__ cx,
+                                                         const double *__restrict__ cy,
+                                                         const double *__restrict__ cz, int32_t box0,
+                                                         const double *__restrict__ ks, int64_t K,
+                                                         ExpConsts ec, double2 *__restrict__ M) {
+  __shared__ double2 tab[TAB];
   __shared__ double sx[S2M_TPB], sy[S2M_TPB], sz[S2M_TPB];
   __shared__ double2 sq[S2M_TPB];
   fill_exp_table(tab);
   const int32_t b = box0 + blockIdx.y;
-  const int64_t k = (int64_t)blockIdx.x * S2M_TPB + threadIdx.x;
-  const bool active = k < K;
-  const double kx = active ? ks[k] : 0.0, ky = active ? ks[K + k] : 0.0, kz = active ? ks[2 * K + k] : 0.0;
+  const int64_t k0 = (int64_t)blockIdx.x * (2 * S2M_TPB) + threadIdx.x, k1 = k0 + S2M_TPB;
+  const double kx0 = k0 < K ? ks[k0] : 0.0, ky0 = k0 < K ? ks[K + k0] : 0.0, kz0 = k0 < K ? ks[2 * K + k0] : 0.0;
+  const double kx1 = k1 < K ? ks[k1] : 0.0, ky1 = k1 < K ? ks[K + k1] : 0.0, kz1 = k1 < K ? ks[2 * K + k1] : 0.0;
   const double c0x = cx[b], c0y = cy[b], c0z = cz[b];
   const int64_t s0 = first[b], s1 = first[b + 1];
-  double ar = 0.0, ai = 0.0;
+  double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
   for (int64_t c0 = s0; c0 < s1; c0 += S2M_TPB) {
     const int cnt = (int)min((int64_t)S2M_TPB, s1 - c0);
     __syncthreads();
@@ -148,55 +186,60 @@ __global__ void __launch_bounds__(S2M_TPB) s2m_kernel(PointsDev pts, const int64
       sq[threadIdx.x] = pts.q[j];
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll 2
     for (int u = 0; u < cnt; ++u) {
-      const double ph = fma(kx, sx[u], fma(ky, sy[u], kz * sz[u]));
-      const double2 e = cexpi_tab(ph, tab, shi, slo);
+      const double dx = sx[u], dy = sy[u], dz = sz[u];
       const double2 q = sq[u];
-      ar = fma(e.x, q.x, fma(-e.y, q.y, ar));
-      ai = fma(e.x, q.y, fma(e.y, q.x, ai));
+      const double2 e0 = cexpi(fma(kx0, dx, fma(ky0, dy, kz0 * dz)), tab, ec);
+      a0r = fma(e0.x, q.x, fma(-e0.y, q.y, a0r));
+      a0i = fma(e0.x, q.y, fma(e0.y, q.x, a0i));
+      const double2 e1 = cexpi(fma(kx1, dx, fma(ky1, dy, kz1 * dz)), tab, ec);
+      a1r = fma(e1.x, q.x, fma(-e1.y, q.y, a1r));
+      a1i = fma(e1.x, q.y, fma(e1.y, q.x, a1i));
     }
   }
-  if (active) M[(int64_t)b * K + k] = make_double2(ar, ai);
+  if (k0 < K) M[(int64_t)b * K + k0] = make_double2(a0r, a0i);
+  if (k1 < K) M[(int64_t)b * K + k1] = make_double2(a1r, a1i);
 }
 
 void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
                 const double *cz, int32_t box0, int32_t box1, const double *ks, int64_t K,
                 double2 *M, cudaStream_t s) {
   if (box1 <= box0) return;
-  double shi, slo;
-  step_split(&shi, &slo);
-  dim3 grid((unsigned)((K + S2M_TPB - 1) / S2M_TPB), (unsigned)(box1 - box0));
-  s2m_kernel<<<grid, S2M_TPB, 0, s>>>(pts, first, cx, cy, cz, box0, ks, K, shi, slo, M);
+  ExpConsts ec;
+  step_split(&ec.shi, &ec.slo);
+  dim3 grid((unsigned)((K + 2 * S2M_TPB - 1) / (2 * S2M_TPB)), (unsigned)(box1 - box0));
+  s2m_kernel<<<grid, S2M_TPB, 0, s>>>(pts, first, cx, cy, cz, box0, ks, K, ec, M);
 }
 
 // ---------------------------------------------------------------------------------------------
-// L2T: thread per target, directions streamed through shared memory.
+// L2T: two targets per thread (tile of 256 targets), directions streamed through shared memory.
 // ---------------------------------------------------------------------------------------------
 constexpr int L2T_TPB = 128;
 
-__global__ void __launch_bounds__(L2T_TPB) l2t_kernel(PointsDev pts, const int64_t *__restrict__ first,
-                                                      const double *__restrict__ cx,
-                                                      const double *__restrict__ cy,
-                                                      const double *__restrict__ cz,
-                                                      const int32_t *__restrict__ tile_leaf,
-                                                      const int64_t *__restrict__ tile_begin,
-                                                      const double *__restrict__ ks, int64_t K,
-                                                      const double2 *__restrict__ L, double w,
-                                                      double shi, double slo,
-                                                      double2 *__restrict__ y_far) {
-  __shared__ double2 tab[HFMM_TABLE];
+__global__ void __launch_bounds__(L2T_TPB, 5) l2t_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                         const double *__restrict__ cx,
+                                                         const double *__restrict__ cy,
+                                                         const double *__restrict__ cz,
+                                                         const int32_t *__restrict__ tile_leaf,
+                                                         const int64_t *__restrict__ tile_begin,
+                                                         const double *__restrict__ ks, int64_t K,
+                                                         const double2 *__restrict__ L, double w,
+                                                         ExpConsts ec, double2 *__restrict__ y_far) {
+  __shared__ double2 tab[TAB];
   __shared__ double skx[L2T_TPB], sky[L2T_TPB], skz[L2T_TPB];
   __shared__ double2 sl[L2T_TPB];
   fill_exp_table(tab);
   const int32_t leaf = tile_leaf[blockIdx.x];
-  const int64_t i = tile_begin[blockIdx.x] + threadIdx.x;
-  const bool active = i < first[leaf + 1];
-  const double dx = active ? cx[leaf] - pts.x[i] : 0.0;   // c_a - x_i
-  const double dy = active ? cy[leaf] - pts.y[i] : 0.0;
-  const double dz = active ? cz[leaf] - pts.z[i] : 0.0;
+  const int64_t tend = first[leaf + 1];
+  const int64_t i0 = tile_begin[blockIdx.x] + threadIdx.x, i1 = i0 + L2T_TPB;
+  const double ccx = cx[leaf], ccy = cy[leaf], ccz = cz[leaf];
+  const double dx0 = i0 < tend ? ccx - pts.x[i0] : 0.0, dy0 = i0 < tend ? ccy - pts.y[i0] : 0.0,
+               dz0 = i0 < tend ? ccz - pts.z[i0] : 0.0;   // c_a - x_i
+  const double dx1 = i1 < tend ? ccx - pts.x[i1] : 0.0, dy1 = i1 < tend ? ccy - pts.y[i1] : 0.0,
+               dz1 = i1 < tend ? ccz - pts.z[i1] : 0.0;
   const double2 *Lb = L + (int64_t)leaf * K;
-  double ar = 0.0, ai = 0.0;
+  double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
   for (int64_t c0 = 0; c0 < K; c0 += L2T_TPB) {
     const int cnt = (int)min((int64_t)L2T_TPB, K - c0);
     __syncthreads();
@@ -208,16 +251,20 @@ __global__ void __launch_bounds__(L2T_TPB) l2t_kernel(PointsDev pts, const int64
       sl[threadIdx.x] = Lb[k];
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll 2
     for (int u = 0; u < cnt; ++u) {
-      const double ph = fma(skx[u], dx, fma(sky[u], dy, skz[u] * dz));
-      const double2 e = cexpi_tab(ph, tab, shi, slo);
+      const double kx = skx[u], ky = sky[u], kz = skz[u];
       const double2 l = sl[u];
-      ar = fma(e.x, l.x, fma(-e.y, l.y, ar));
-      ai = fma(e.x, l.y, fma(e.y, l.x, ai));
+      const double2 e0 = cexpi(fma(kx, dx0, fma(ky, dy0, kz * dz0)), tab, ec);
+      a0r = fma(e0.x, l.x, fma(-e0.y, l.y, a0r));
+      a0i = fma(e0.x, l.y, fma(e0.y, l.x, a0i));
+      const double2 e1 = cexpi(fma(kx, dx1, fma(ky, dy1, kz * dz1)), tab, ec);
+      a1r = fma(e1.x, l.x, fma(-e1.y, l.y, a1r));
+      a1i = fma(e1.x, l.y, fma(e1.y, l.x, a1i));
     }
   }
-  if (active) y_far[i] = make_double2(w * ar, w * ai);
+  if (i0 < tend) y_far[i0] = make_double2(w * a0r, w * a0i);
+  if (i1 < tend) y_far[i1] = make_double2(w * a1r, w * a1i);
 }
 
 void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
@@ -225,10 +272,10 @@ void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const dou
                 int64_t ntiles, const double *ks, int64_t K, const double2 *L, double w,
                 double2 *y_far, cudaStream_t s) {
   if (ntiles <= 0) return;
-  double shi, slo;
-  step_split(&shi, &slo);
-  l2t_kernel<<<(unsigned)ntiles, L2T_TPB, 0, s>>>(pts, first, cx, cy, cz, tile_leaf, tile_begin, ks,
-                                                   K, L, w, shi, slo, y_far);
+  ExpConsts ec;
+  step_split(&ec.shi, &ec.slo);
+  l2t_kernel<<<(unsigned)ntiles, L2T_TPB, 0, s>>>(pts, first, cx, cy, cz, tile_leaf, tile_begin, ks, K, L, w, ec,
+                                                   y_far);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -1,0 +1,106 @@
+"""GPU checks at BASELINE.json's full sizes (C3: 1e5, C4: 1e6, C5: 1e7 points), in the same
+library path bench.py times, on outputs the oracle can compute one by one:
+  - the integer plan (ell, N_theta, N_phi, L_f) equals the oracle's
+  - transfer tables for sampled offsets equal the oracle's Alg. 1 (1e-12)
+  - S2M expansions of sampled leaves equal the oracle's (1e-11)
+  - near-field sums of sampled targets equal the oracle's P2P (1e-11)
+  - sampled y_i agree with the direct sum within eps (relative L2 over the sample)
+"""
+import math
+
+import numpy as np
+import pytest
+
+from workloads import CONFIGS, points_and_charges, sample_indices
+from oracle.plan import make_plan, level_params
+from oracle.direct import direct_sum
+from oracle.transfer import bmtf_table, offsets316
+from oracle.tree import build_level
+from oracle.fmm import OracleFMM
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
+
+
+@pytest.fixture(scope="module")
+def hf():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_0911_4114_b200 as mod
+    from paper_0911_4114_b200.build import build
+    build(verbose=False)
+    return mod
+
+
+_cache = {}
+
+
+def run(hf, name):
+    if name in _cache:
+        return _cache[name]
+    import torch
+    cfg = CONFIGS[name]
+    x, q = points_and_charges(cfg)
+    g = hf.HFMM(0)
+    g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha)
+    y = g.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    _cache[name] = (cfg, x, q, g, y)
+    return _cache[name]
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_fullsize_plan_and_accuracy(hf, name):
+    cfg, x, q, g, y = run(hf, name)
+    info = g.info()
+    # integer plan of every level vs the oracle's level rule
+    for lv in info["levels"]:
+        ell, nth, nph, _ = level_params(cfg.kappa, lv["a"], cfg.eps, cfg.alpha)
+        assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (ell, nth, nph), lv["level"]
+    # sampled targets vs direct summation (eqn:HelmholtzMatrixVector)
+    t = sample_indices(cfg.n, 48, seed=100 + cfg.seed)
+    yd = direct_sum(x, q, cfg.kappa, t)
+    assert rel(y[t], yd) <= cfg.eps, (name, rel(y[t], yd))
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_fullsize_admissibility_matches_oracle(hf, name):
+    cfg, x, q, g, y = run(hf, name)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+    assert g.info()["L_f"] == plan.L_f
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_fullsize_stage_samples(hf, name):
+    cfg, x, q, g, y = run(hf, name)
+    info = g.info()
+    L = info["L_f"]
+    lv = {d["level"]: d for d in info["levels"]}
+    # transfer tables of sampled offsets at level 2
+    T = g.debug(3, 2).reshape(316, -1)
+    offs = offsets316()
+    for oid in (3, 150, 310):
+        ref = bmtf_table(lv[2]["ell"], cfg.kappa, offs[oid] * lv[2]["a"], lv[2]["n_theta"], lv[2]["n_phi"]).reshape(-1)
+        assert rel(T[oid], ref) <= 1e-12
+    # oracle tree at L_f (its own), same plan integers
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+    f = OracleFMM(x, cfg.lo, cfg.size, plan)
+    lev = f.levels[L]
+    tab = g.debug(7, L)
+    gpu_index = {(int(r[0]), int(r[1]), int(r[2])): b for b, r in enumerate(tab)}
+    Mg = g.debug(0, L).reshape(len(tab), -1)
+    rng = np.random.default_rng(1)
+    for ob in rng.choice(len(lev.boxes), size=2, replace=False):
+        Mo = f.s2m(q, boxes=[ob])[ob]
+        assert rel(Mg[gpu_index[lev.boxes[ob]]], Mo) <= 1e-11
+    # near field of sampled targets
+    perm = g.debug(6)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    t = sample_indices(cfg.n, 32, seed=7)
+    yn_gpu = g.debug(4)[inv[t]]
+    yn_or = f.p2p(q, t)
+    assert rel(yn_gpu, yn_or) <= 1e-11
