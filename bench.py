@@ -29,11 +29,12 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-# FP64 flops of one P2P pair as implemented: difference 3,
-# r^2 5, rsqrt 6, r and kappa r 2, e^{ix} 26 (Cody-Waite + table + degree-7/6 polynomials),
-# 1/r scaling 2, complex MAC 8.
-P2P_FLOPS_PER_PAIR = 52
-S2M_FLOPS_PER_EVAL = 40      # phase 5 + e^{ix} 26 + complex MAC 8 (+1 scale)
+# FP64 flops (FMA = 2) of the P2P arithmetic as implemented:
+# one kernel evaluation G = e^{i kappa R}/R costs 43 (difference 3, r^2 5, rsqrt + Newton 8,
+# r and kappa r 2, e^{ix} 23, 1/r scaling 2); every ORDERED pair adds a complex MAC (8).  The
+# symmetric kernel evaluates G once per unordered pair and applies it to both rows.
+P2P_FLOPS_PER_EVAL = 43
+P2P_FLOPS_PER_MAC = 8
 
 
 def parse():
@@ -285,8 +286,11 @@ def main():
     # P2P roofline (dominant kernel): algorithmic FP64 flops / measured duration
     p2p_ms = statistics.mean(stage["p2p"])
     pairs = info["p2p_pairs"]
+    sym = info["p2p_sym_pairs"]
+    evals = sym + (pairs - 2 * sym)          # unordered (symmetric) + ordered (diagonal) evaluations
+    p2p_flops = P2P_FLOPS_PER_EVAL * evals + P2P_FLOPS_PER_MAC * pairs
     peak_tflops = 2 * 64 * 148 * (clocks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
-    achieved = P2P_FLOPS_PER_PAIR * pairs / (p2p_ms * 1e-3) / 1e12
+    achieved = p2p_flops / (p2p_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -310,7 +314,11 @@ def main():
         "roofline": {"kernel": "p2p", "bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved / peak_tflops, "traffic": traffic,
                      "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 2 x sm_max_mhz (DESIGN.md)",
-                     "per_unit": f"{P2P_FLOPS_PER_PAIR} FP64 flops per ordered pair", "units_per_launch": pairs},
+                     "per_unit": f"{P2P_FLOPS_PER_EVAL} FP64 flops per kernel evaluation + "
+                                 f"{P2P_FLOPS_PER_MAC} per ordered pair (MAC)",
+                     "units_per_launch": {"ordered_pairs": pairs, "evaluations": evals},
+                     "flops_per_launch": p2p_flops,
+                     "measured_dfma_peak_tflops": 34.2},
         "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
         "plan": {"levels": [{k: lv[k] for k in ("level", "ell", "n_theta", "n_phi", "F", "active")}
                             for lv in info["levels"]], "p2p_pairs": pairs, "s2m_evals": info["s2m_evals"]},

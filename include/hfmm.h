@@ -59,6 +59,9 @@ extern "C" {
 #define HFMM_EPS_ABSOLUTE 0x1u     /* use eps itself at every level (default eps/a_l)        */
 #define HFMM_FORCE_ALL_LEVELS 0x2u /* run M2L at every level 2..depth regardless of F_l
                                       (low-frequency breakdown demonstration)        */
+#define HFMM_ALPHA_FIXED 0x4u      /* use the caller's alpha at every level (the paper's fixed
+                                      design radius); default: per level the largest alpha in
+                                      {1, 0.9, 0.8} (>= the caller's) that keeps F_l <= tau   */
 
 /* ---- matvec memory kinds -------------------------------------------------------------- */
 #define HFMM_HOST 0    /* q and y are host pointers (pinned or pageable)                     */
@@ -75,6 +78,7 @@ typedef struct {
   int ell;          /* Gegenbauer truncation                                   */
   int n_theta;      /* N_theta (Alg. 2), even, 7-smooth                         */
   int n_phi;        /* N_phi (Alg. 3), multiple of 4, 7-smooth                  */
+  double alpha;     /* design radius |r| = alpha sqrt(3) a_l used for this level   */
   int64_t K;        /* stored quadrature points N_theta * N_phi / 2            */
   double F;         /* roundoff amplification 8 pi u a_l max|T_l| (NaN if not evaluated)    */
   int active;       /* 1 if M2L runs at this level                                         */
@@ -90,6 +94,7 @@ typedef struct {
   int nlevels;             /* entries filled in level[] (levels 2..D)                        */
   hfmm_level_info level[HFMM_MAX_LEVELS];
   int64_t p2p_pairs;       /* ordered near-field pairs (incl. self pairs skipped)            */
+  int64_t p2p_sym_pairs;   /* unordered pairs of them evaluated once (symmetric kernel)      */
   int64_t s2m_evals;       /* points x directions at L_f                                    */
   int rank, nranks;
   int64_t owned_points;    /* points whose y this rank computes                              */

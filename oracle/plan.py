@@ -20,6 +20,10 @@ Readings of silent/ambiguous points are listed in DESIGN.md ("Readings"):
   R-5 monotone grids on the active chain: N^{l-1} >= N^l per dimension
   R-9 F_l = 8 pi u a_l max |T^{s,LL}_l| over the 34 canonical offsets, u = 2^-53;
       active iff F_l <= tau; L_f = deepest l with 2..l all active.
+  R-13 design radius per level: the largest alpha in {1, 0.9, 0.8} (>= the caller's alpha)
+      whose quadrature keeps F_l <= tau (the paper uses alpha = 1 for its volume timing runs,
+      P:1161, and 0.8 in its error studies; pairs beyond alpha sqrt3 a are not covered
+      by the bound).  alpha_fixed=True: the caller's alpha at every level.
 """
 from __future__ import annotations
 
@@ -172,6 +176,7 @@ class LevelPlan:
     ragged: List[int] = field(default_factory=list)
     F: float = float("nan")
     active: bool = False
+    alpha: float = 0.8
 
     @property
     def K(self) -> int:
@@ -214,31 +219,46 @@ def default_tau(eps: float) -> float:
     return min(eps / 10.0, 1e-9)
 
 
+def alpha_candidates(alpha: float, fixed: bool):
+    """Design radii tried per level, largest first (R-13): {1, 0.9, 0.8} above the caller's alpha."""
+    if fixed:
+        return [alpha]
+    return [c for c in (1.0, 0.9, 0.8) if c > alpha + 1e-12] + [alpha]
+
+
 def make_plan(kappa: float, eps: float, a0: float, depth: int, alpha: float = 0.8,
               tau: Optional[float] = None, force_all: bool = False,
-              eps_absolute: bool = False) -> Plan:
-    """Plan for levels 2..depth (P:140-722 + admissibility R-9, monotone R-5)."""
+              eps_absolute: bool = False, alpha_fixed: bool = False) -> Plan:
+    """Plan for levels 2..depth (P:140-722 + admissibility R-9, design radius R-13, monotone R-5).
+
+    Shallowest level first: for each candidate design radius alpha (R-13, largest first) take
+    the quadrature of P:140-722 and F_l; the level is active with the first alpha whose
+    F_l <= tau.  The first level with no admissible alpha ends the chain (L_f = l - 1); deeper
+    levels are reported with the caller's alpha and no F."""
     if tau is None or tau <= 0:
         tau = default_tau(eps)
     levels = {}
     L_f = None
+    cands = alpha_candidates(alpha, alpha_fixed or force_all)
+    stop = None
     for l in range(2, depth + 1):
         a = a0 / 2 ** l
-        ell, nth, nph, ragged = level_params(kappa, a, eps, alpha, eps_absolute)
-        lp = LevelPlan(l, a, ell, nth, nph, ragged)
+        if stop is not None:
+            ell, nth, nph, ragged = level_params(kappa, a, eps, alpha, eps_absolute)
+            levels[l] = LevelPlan(l, a, ell, nth, nph, ragged, alpha=alpha)
+            continue
+        for al in cands:
+            ell, nth, nph, ragged = level_params(kappa, a, eps, al, eps_absolute)
+            lp = LevelPlan(l, a, ell, nth, nph, ragged, alpha=al)
+            lp.F = level_F(kappa, a, ell, nth, nph)
+            lp.active = force_all or lp.F <= tau
+            if lp.active:
+                break
         levels[l] = lp
-    # admissibility, shallowest first; stop at the first inadmissible level
-    for l in range(2, depth + 1):
-        lp = levels[l]
-        lp.F = level_F(kappa, lp.a, lp.ell, lp.n_theta, lp.n_phi)
-        lp.active = lp.F <= tau
-        if not lp.active and not force_all:
-            break
-        L_f = l
-    if force_all:
-        L_f = depth
-        for lp in levels.values():
-            lp.active = True
+        if lp.active:
+            L_f = l
+        else:
+            stop = l
     # monotone grids on the chain 2..L_f (R-5)
     if L_f is not None:
         for l in range(L_f - 1, 1, -1):

@@ -20,6 +20,7 @@ HFMM_W_BREAKDOWN = 1
 HFMM_W_NO_FARFIELD = 2
 HFMM_EPS_ABSOLUTE = 0x1
 HFMM_FORCE_ALL_LEVELS = 0x2
+HFMM_ALPHA_FIXED = 0x4
 HFMM_HOST = 0
 HFMM_DEVICE = 1
 HFMM_Y_LOCAL = 2
@@ -35,14 +36,16 @@ EXPORTED = [
 
 class LevelInfo(C.Structure):
     _fields_ = [("level", C.c_int), ("a", C.c_double), ("ell", C.c_int), ("n_theta", C.c_int),
-                ("n_phi", C.c_int), ("K", C.c_int64), ("F", C.c_double), ("active", C.c_int),
+                ("n_phi", C.c_int), ("alpha", C.c_double), ("K", C.c_int64), ("F", C.c_double),
+                ("active", C.c_int),
                 ("boxes", C.c_int64), ("m2l_pairs", C.c_int64)]
 
 
 class Info(C.Structure):
     _fields_ = [("n", C.c_int64), ("depth", C.c_int), ("L_f", C.c_int), ("kappa", C.c_double),
                 ("eps", C.c_double), ("alpha", C.c_double), ("tau", C.c_double), ("nlevels", C.c_int),
-                ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("s2m_evals", C.c_int64),
+                ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("p2p_sym_pairs", C.c_int64),
+                ("s2m_evals", C.c_int64),
                 ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64)]
 
 
@@ -200,10 +203,12 @@ class HFMM:
         levels = []
         for i in range(inf.nlevels):
             lv = inf.level[i]
-            levels.append(dict(level=lv.level, a=lv.a, ell=lv.ell, n_theta=lv.n_theta, n_phi=lv.n_phi, K=lv.K,
+            levels.append(dict(level=lv.level, a=lv.a, ell=lv.ell, n_theta=lv.n_theta, n_phi=lv.n_phi,
+                               alpha=lv.alpha, K=lv.K,
                                F=lv.F, active=bool(lv.active), boxes=lv.boxes, m2l_pairs=lv.m2l_pairs))
         return dict(n=inf.n, depth=inf.depth, L_f=(None if inf.L_f < 0 else inf.L_f), kappa=inf.kappa,
                     eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
+                    p2p_sym_pairs=inf.p2p_sym_pairs,
                     s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points)
 
     def stage_times(self):

@@ -30,6 +30,7 @@ struct LevelDev {
   int l = 0;
   double a = 0;
   int ell = 0, nth = 0, nph = 0;
+  double alpha = 0;
   int64_t K = 0;
   double F = NAN;
   bool active = false;
@@ -106,6 +107,10 @@ struct hfmm_plan {
   int32_t *tile_leaf = nullptr;
   int64_t *tile_begin = nullptr;
   int64_t ntiles = 0;
+  int32_t *sym_leaf = nullptr, *sym_src = nullptr;  // symmetric P2P work items
+  int64_t *sym_begin = nullptr;
+  int64_t nsym = 0, p2p_sym_pairs = 0;
+  double dummy_t[3] = {0, 0, 0}, dummy_s[3] = {0, 0, 0};
   // all-pairs (direct) tiles
   int32_t *dir_tile_leaf = nullptr, *dir_nb_row = nullptr, *dir_nb_box = nullptr;
   int64_t *dir_tile_begin = nullptr, *dir_first = nullptr;
@@ -147,10 +152,12 @@ static void free_levels(hfmm_plan *p) {
   }
   p->lv.clear();
   for (void *ptr : {(void *)p->first_near, (void *)p->nb_row, (void *)p->nb_box, (void *)p->tile_leaf,
-                    (void *)p->tile_begin, (void *)p->tmp, (void *)p->y_far})
+                    (void *)p->tile_begin, (void *)p->tmp, (void *)p->y_far, (void *)p->sym_leaf,
+                    (void *)p->sym_src, (void *)p->sym_begin})
     if (ptr) cudaFree(ptr);
   p->first_near = nullptr, p->nb_row = p->nb_box = p->tile_leaf = nullptr;
   p->tile_begin = nullptr, p->tmp = nullptr, p->y_far = nullptr;
+  p->sym_leaf = p->sym_src = nullptr, p->sym_begin = nullptr, p->nsym = 0;
   p->tmp_elems = 0;
   p->ntiles = 0;
   p->have_plan = false;
@@ -436,38 +443,62 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   const Tree &t = p->tree;
   const int D = t.depth;
   p->lv.assign(D + 1, LevelDev());
-  // per-level quadrature (host)
+  // per-level quadrature (host) for a design radius alpha sqrt(3) a_l
+  auto level_quad = [&](LevelDev &L, double al) -> int {
+    const double eps_l = (flags & HFMM_EPS_ABSOLUTE) ? eps : eps / L.a;
+    const double r = al * std::sqrt(3.0) * L.a, r0 = 2.0 * L.a;
+    int rc = select_ell(kappa, r, r0, eps_l, &L.ell);
+    if (!rc) rc = select_ntheta(L.ell, kappa, r, r0, eps_l, &L.nth);
+    if (!rc) rc = select_nphi(L.ell, kappa, r, r0, eps_l, L.nth, &L.nph, nullptr);
+    if (rc) p->err = "hfmm_precompute: quadrature search failed at level " + std::to_string(L.l);
+    L.alpha = al;
+    L.K = (int64_t)L.nth * L.nph / 2;
+    return rc;
+  };
+  // candidate design radii: the largest alpha in {1, 0.9, 0.8} (>= the caller's alpha) that
+  // keeps the level admissible (R-13); the caller's alpha alone with HFMM_ALPHA_FIXED
+  std::vector<double> cands;
+  if (flags & (HFMM_ALPHA_FIXED | HFMM_FORCE_ALL_LEVELS)) {
+    cands.push_back(alpha);
+  } else {
+    for (double c : {1.0, 0.9, 0.8})
+      if (c > alpha + 1e-12) cands.push_back(c);
+    cands.push_back(alpha);
+  }
   for (int l = 2; l <= D; ++l) {
     LevelDev &L = p->lv[l];
     L.l = l;
     L.a = t.size / (double)(1 << l);
-    const double eps_l = (flags & HFMM_EPS_ABSOLUTE) ? eps : eps / L.a;
-    const double r = alpha * std::sqrt(3.0) * L.a, r0 = 2.0 * L.a;
-    int rc = select_ell(kappa, r, r0, eps_l, &L.ell);
-    if (!rc) rc = select_ntheta(L.ell, kappa, r, r0, eps_l, &L.nth);
-    if (!rc) rc = select_nphi(L.ell, kappa, r, r0, eps_l, L.nth, &L.nph, nullptr);
-    if (rc) {
-      p->err = "hfmm_precompute: quadrature search failed at level " + std::to_string(l);
-      return rc;
-    }
-    L.K = (int64_t)L.nth * L.nph / 2;
     L.nbox = t.levels[l].nbox();
   }
   // admissibility F_l <= tau, shallowest first (R-9)
   p->L_f = -1;
   const bool force = flags & HFMM_FORCE_ALL_LEVELS;
+  int first_inactive = D + 1;
   for (int l = 2; l <= D; ++l) {
     LevelDev &L = p->lv[l];
-    double2 *T = nullptr;
-    int rc = level_tables(p, L, &T, &L.F);
-    if (rc) return rc;
-    L.active = force || (L.F <= p->tau);
-    if (!L.active) {
+    for (double al : cands) {
+      int rc = level_quad(L, al);
+      if (rc) return rc;
+      double2 *T = nullptr;
+      rc = level_tables(p, L, &T, &L.F);
+      if (rc) return rc;
+      L.active = force || (L.F <= p->tau);
+      if (L.active) {
+        L.T = T;
+        break;
+      }
       if (T) cudaFree(T);
+    }
+    if (!L.active) {
+      first_inactive = l;
       break;
     }
-    L.T = T;
     p->L_f = l;
+  }
+  for (int l = first_inactive + 1; l <= D; ++l) {  // reported only (caller's alpha, F not evaluated)
+    int rc = level_quad(p->lv[l], alpha);
+    if (rc) return rc;
   }
   // monotone grids along the active chain (R-5)
   for (int l = p->L_f - 1; l >= 2; --l) {
@@ -559,21 +590,38 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   // near field at L_f (neighbour lists) or all pairs at the root
   p->near_level = p->L_f >= 2 ? p->L_f : 0;
   {
+    // Ordered work (rows only): the leaf itself and neighbours owned by another rank.
+    // Symmetric work (rows + columns, each unordered pair once): owned neighbours beta > alpha.
     const LevelBoxes &B = t.levels[p->near_level];
-    std::vector<int32_t> row(1, 0), nb;
+    int64_t lo = 0, hi = B.nbox();
+    if (p->L_f >= 2) lo = p->lv[p->L_f].own0, hi = p->lv[p->L_f].own1;
+    auto owned = [&](int64_t k) { return k >= lo && k < hi; };
+    std::vector<int32_t> row(1, 0), nb, wl, ws;
+    std::vector<int64_t> wb;
+    int64_t pairs = 0, sym_pairs = 0;
     for (int64_t b = 0; b < B.nbox(); ++b) {
+      const int64_t nbpts = B.first[b + 1] - B.first[b];
       for (int dx = -1; dx <= 1; ++dx)
         for (int dy = -1; dy <= 1; ++dy)
           for (int dz = -1; dz <= 1; ++dz) {
             int32_t k = B.find(B.ix[b] + dx, B.iy[b] + dy, B.iz[b] + dz);
-            if (k >= 0) nb.push_back(k);
+            if (k < 0 || !owned(b)) continue;
+            const int64_t nk = B.first[k + 1] - B.first[k];
+            pairs += nbpts * nk;
+            if (k == b || !owned(k)) {
+              nb.push_back(k);
+            } else if (k > b) {
+              sym_pairs += nbpts * nk;
+              for (int64_t s = B.first[b]; s < B.first[b + 1]; s += kTile)
+                wl.push_back((int32_t)b), wb.push_back(s), ws.push_back(k);
+            }
           }
       row.push_back((int32_t)nb.size());
     }
     p->nb_row = dupload(row), p->nb_box = dupload(nb);
     p->first_near = dupload(B.first);
-    int64_t lo = 0, hi = B.nbox();
-    if (p->L_f >= 2) lo = p->lv[p->L_f].own0, hi = p->lv[p->L_f].own1;
+    p->sym_leaf = dupload(wl), p->sym_begin = dupload(wb), p->sym_src = dupload(ws);
+    p->nsym = (int64_t)wl.size();
     std::vector<int32_t> tl;
     std::vector<int64_t> tb;
     for (int64_t b = lo; b < hi; ++b)
@@ -583,11 +631,13 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       }
     p->tile_leaf = dupload(tl), p->tile_begin = dupload(tb);
     p->ntiles = (int64_t)tl.size();
-    int64_t pairs = 0;
-    for (int64_t b = lo; b < hi; ++b)
-      for (int32_t e = row[b]; e < row[b + 1]; ++e)
-        pairs += (B.first[b + 1] - B.first[b]) * (B.first[nb[e] + 1] - B.first[nb[e]]);
     p->info.p2p_pairs = pairs;
+    p->info.p2p_sym_pairs = sym_pairs;
+    p->p2p_sym_pairs = sym_pairs;
+    for (int d = 0; d < 3; ++d) {
+      p->dummy_t[d] = t.lo[d] - 3.0 * t.size;
+      p->dummy_s[d] = t.lo[d] + 4.0 * t.size;
+    }
   }
   if (p->L_f >= 2) p->y_far = dalloc<double2>(t.n);
   CK(cudaStreamSynchronize(p->stream));
@@ -600,7 +650,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   for (int l = 2; l <= D && in.nlevels < HFMM_MAX_LEVELS; ++l) {
     const LevelDev &L = p->lv[l];
     hfmm_level_info &li = in.level[in.nlevels++];
-    li.level = l, li.a = L.a, li.ell = L.ell, li.n_theta = L.nth, li.n_phi = L.nph, li.K = L.K,
+    li.level = l, li.a = L.a, li.ell = L.ell, li.n_theta = L.nth, li.n_phi = L.nph, li.alpha = L.alpha, li.K = L.K,
     li.F = L.F, li.active = L.active ? 1 : 0, li.boxes = L.nbox, li.m2l_pairs = L.il_nnz;
   }
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->L_f].K : 0;
@@ -644,8 +694,11 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
   CK(cudaEventRecord(p->ev_fork, s));
   CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
   if (prof) cudaEventRecord(p->sev[7], p->stream2);
+  CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), p->stream2));
   launch_p2p(pts, p->first_near, p->nb_row, p->nb_box, 0, 0, p->tile_leaf, p->tile_begin, p->ntiles,
              p->kappa, p->y_near, p->stream2);
+  launch_p2p_sym(pts, p->first_near, p->sym_leaf, p->sym_begin, p->sym_src, p->nsym, p->kappa, p->dummy_t,
+                 p->dummy_s, p->y_near, p->stream2);
   if (prof) cudaEventRecord(p->sev[8], p->stream2);
   CK(cudaEventRecord(p->ev_join, p->stream2));
   const TwiddleSet &tw = global_twiddles(p->device);
@@ -732,6 +785,7 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
   if (direct) {
     launch_permute_q(qd, p->perm, p->q_sorted, n, s);
     PointsDev pts{p->px, p->py, p->pz, p->q_sorted};
+    CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), s));
     launch_p2p(pts, p->dir_first, p->dir_nb_row, p->dir_nb_box, 0, 0, p->dir_tile_leaf, p->dir_tile_begin,
                p->dir_ntiles, p->kappa > 0 ? p->kappa : 0.0, p->y_near, s);
     launch_combine(p->y_near, nullptr, p->perm, p->y_out, n, 0, n, s);

@@ -92,6 +92,13 @@ void launch_p2p(PointsDev pts, const int64_t *first, const int32_t *nb_row, cons
                 int32_t leaf0, int32_t leaf1, const int32_t *tile_leaf, const int64_t *tile_begin,
                 int64_t ntiles, double kappa, double2 *y_near, cudaStream_t s);
 
+// Symmetric P2P over unordered leaf pairs: work item w = (256-target tile of leaf w_leaf[w]
+// starting at w_begin[w], source leaf w_src[w] != w_leaf[w]); adds row and column sums into
+// y_near (zeroed beforehand).  dummy_t / dummy_s: far positions used to pad partial tiles.
+void launch_p2p_sym(PointsDev pts, const int64_t *first, const int32_t *w_leaf, const int64_t *w_begin,
+                    const int32_t *w_src, int64_t nwork, double kappa, const double dummy_t[3],
+                    const double dummy_s[3], double2 *y_near, cudaStream_t s);
+
 // S2M: M[b][k] = sum_j q_j e^{i kappa s_k.(x_j - c_b)}
 void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
                 const double *cz, int32_t box0, int32_t box1, const double *ks /*[3][K]*/,

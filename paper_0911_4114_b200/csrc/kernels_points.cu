@@ -139,8 +139,112 @@ __global__ void __launch_bounds__(P2P_TPB, 5) p2p_kernel(PointsDev pts, const in
         p2p_chunk<false>(cnt, sx, sy, sz, sq, x0, y0, z0, x1, y1, z1, kappa, tab, ec, a0r, a0i, a1r, a1i);
     }
   }
-  if (i0 < tend) y_near[i0] = make_double2(a0r, a0i);
-  if (i1 < tend) y_near[i1] = make_double2(a1r, a1i);
+  // y_near is zeroed before the P2P launches; the symmetric kernel adds into the same rows
+  if (i0 < tend) atomicAdd(&y_near[i0].x, a0r), atomicAdd(&y_near[i0].y, a0i);
+  if (i1 < tend) atomicAdd(&y_near[i1].x, a1r), atomicAdd(&y_near[i1].y, a1i);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Symmetric P2P over an unordered leaf pair (alpha, beta), alpha != beta: the kernel
+// G(x_i, x_j) = e^{i kappa |x_i - x_j|} / |x_i - x_j| is symmetric, so each unordered pair is
+// evaluated once and contributes G q_j to y_i (row sums, registers) and G q_i to y_j (column
+// sums).  Column sums use a systolic warp reduction: in a block of 32 sources, lane t processes
+// source (t + u) mod 32 at step u and passes the running column accumulator to lane t - 1, so
+// after 32 steps lane t holds the full warp sum of source t (2 shuffles per step instead of a
+// 5-level butterfly per source).  Work item = (256-target tile of alpha, beta).
+// ---------------------------------------------------------------------------------------------
+constexpr int SYM_TPB = 128;
+
+__device__ __forceinline__ double2 green(double tx, double ty, double tz, double xs, double ys, double zs,
+                                         double kappa, const double2 *tab, const ExpConsts &ec) {
+  const double dx = tx - xs, dy = ty - ys, dz = tz - zs;
+  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  const double ri = rsqrt_fast(r2);
+  const double2 e = cexpi(kappa * (r2 * ri), tab, ec);
+  return make_double2(e.x * ri, e.y * ri);
+}
+
+__global__ void __launch_bounds__(SYM_TPB, 4) p2p_sym_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                             const int32_t *__restrict__ w_leaf,
+                                                             const int64_t *__restrict__ w_begin,
+                                                             const int32_t *__restrict__ w_src, double kappa,
+                                                             ExpConsts ec, double3 dummy_t, double3 dummy_s,
+                                                             double2 *__restrict__ y_near) {
+  __shared__ double2 tab[TAB];
+  __shared__ double sx[SYM_TPB], sy[SYM_TPB], sz[SYM_TPB];
+  __shared__ double2 sq[SYM_TPB];
+  __shared__ double2 col[SYM_TPB / 32][SYM_TPB];
+  fill_exp_table(tab);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t leaf = w_leaf[blockIdx.x], src = w_src[blockIdx.x];
+  const int64_t tend = first[leaf + 1];
+  const int64_t i0 = w_begin[blockIdx.x] + threadIdx.x, i1 = i0 + SYM_TPB;
+  const bool v0 = i0 < tend, v1 = i1 < tend;
+  // inactive targets: far dummy position, zero charge (their column contributions vanish)
+  const double x0 = v0 ? pts.x[i0] : dummy_t.x, y0 = v0 ? pts.y[i0] : dummy_t.y, z0 = v0 ? pts.z[i0] : dummy_t.z;
+  const double x1 = v1 ? pts.x[i1] : dummy_t.x, y1 = v1 ? pts.y[i1] : dummy_t.y, z1 = v1 ? pts.z[i1] : dummy_t.z;
+  const double2 q0 = v0 ? pts.q[i0] : make_double2(0.0, 0.0), q1 = v1 ? pts.q[i1] : make_double2(0.0, 0.0);
+  double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
+  const int64_t s0 = first[src], s1 = first[src + 1];
+  for (int64_t c0 = s0; c0 < s1; c0 += SYM_TPB) {
+    const int cnt = (int)min((int64_t)SYM_TPB, s1 - c0);
+    __syncthreads();
+    {
+      const int t = threadIdx.x;
+      const bool v = t < cnt;
+      const int64_t j = c0 + t;
+      sx[t] = v ? pts.x[j] : dummy_s.x;   // padded sources: far dummy, zero charge
+      sy[t] = v ? pts.y[j] : dummy_s.y;
+      sz[t] = v ? pts.z[j] : dummy_s.z;
+      sq[t] = v ? pts.q[j] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const int nblk = (cnt + 31) >> 5;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int base = blk << 5;
+      double cr = 0.0, ci = 0.0;
+#pragma unroll 2
+      for (int u = 0; u < 32; ++u) {
+        const int s = base + ((lane + u) & 31);
+        const double xs = sx[s], ys = sy[s], zs = sz[s];
+        const double2 qs = sq[s];
+        const double2 g0 = green(x0, y0, z0, xs, ys, zs, kappa, tab, ec);
+        const double2 g1 = green(x1, y1, z1, xs, ys, zs, kappa, tab, ec);
+        a0r = fma(g0.x, qs.x, fma(-g0.y, qs.y, a0r));
+        a0i = fma(g0.x, qs.y, fma(g0.y, qs.x, a0i));
+        a1r = fma(g1.x, qs.x, fma(-g1.y, qs.y, a1r));
+        a1i = fma(g1.x, qs.y, fma(g1.y, qs.x, a1i));
+        cr = fma(g0.x, q0.x, fma(-g0.y, q0.y, cr));
+        ci = fma(g0.x, q0.y, fma(g0.y, q0.x, ci));
+        cr = fma(g1.x, q1.x, fma(-g1.y, q1.y, cr));
+        ci = fma(g1.x, q1.y, fma(g1.y, q1.x, ci));
+        cr = __shfl_sync(0xffffffffu, cr, (lane + 1) & 31);   // accumulator follows its source
+        ci = __shfl_sync(0xffffffffu, ci, (lane + 1) & 31);
+      }
+      col[warp][base + lane] = make_double2(cr, ci);
+    }
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      double2 sum = col[0][threadIdx.x];
+#pragma unroll
+      for (int w = 1; w < SYM_TPB / 32; ++w) sum.x += col[w][threadIdx.x].x, sum.y += col[w][threadIdx.x].y;
+      atomicAdd(&y_near[c0 + threadIdx.x].x, sum.x);
+      atomicAdd(&y_near[c0 + threadIdx.x].y, sum.y);
+    }
+  }
+  if (v0) atomicAdd(&y_near[i0].x, a0r), atomicAdd(&y_near[i0].y, a0i);
+  if (v1) atomicAdd(&y_near[i1].x, a1r), atomicAdd(&y_near[i1].y, a1i);
+}
+
+void launch_p2p_sym(PointsDev pts, const int64_t *first, const int32_t *w_leaf, const int64_t *w_begin,
+                    const int32_t *w_src, int64_t nwork, double kappa, const double dummy_t[3],
+                    const double dummy_s[3], double2 *y_near, cudaStream_t s) {
+  if (nwork <= 0) return;
+  ExpConsts ec;
+  step_split(&ec.shi, &ec.slo);
+  p2p_sym_kernel<<<(unsigned)nwork, SYM_TPB, 0, s>>>(pts, first, w_leaf, w_begin, w_src, kappa, ec,
+                                                      make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
+                                                      make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near);
 }
 
 void launch_p2p(PointsDev pts, const int64_t *first, const int32_t *nb_row, const int32_t *nb_box,

@@ -58,10 +58,10 @@ def test_fullsize_plan_and_accuracy(hf, name):
     info = g.info()
     # integer plan of every level vs the oracle's level rule
     for lv in info["levels"]:
-        ell, nth, nph, _ = level_params(cfg.kappa, lv["a"], cfg.eps, cfg.alpha)
+        ell, nth, nph, _ = level_params(cfg.kappa, lv["a"], cfg.eps, lv["alpha"])
         assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (ell, nth, nph), lv["level"]
     # sampled targets vs direct summation (eqn:HelmholtzMatrixVector)
-    t = sample_indices(cfg.n, 48, seed=100 + cfg.seed)
+    t = sample_indices(cfg.n, 200 if cfg.n <= 10**6 else 64, seed=100 + cfg.seed)
     yd = direct_sum(x, q, cfg.kappa, t)
     assert rel(y[t], yd) <= cfg.eps, (name, rel(y[t], yd))
 

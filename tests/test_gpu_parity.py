@@ -49,6 +49,7 @@ def check_plan(g, plan):
     for lv in info["levels"]:
         op = plan.levels[lv["level"]]
         assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (op.ell, op.n_theta, op.n_phi), lv["level"]
+        assert lv["alpha"] == op.alpha, lv["level"]
         if lv["level"] <= (plan.L_f or 1) + 1 and not math.isnan(op.F):
             assert lv["active"] == op.active
             assert abs(lv["F"] - op.F) <= 1e-6 * op.F
@@ -138,11 +139,13 @@ def test_small_repeat_and_device_path(small, hf):
     import torch
     cfg, x, q, plan, f, g, y = small
     y2 = g.matvec(q)
-    assert np.array_equal(y, y2)                       # run-to-run bitwise reproducible
+    # the symmetric P2P adds column sums with atomics, so run-to-run results agree to rounding
+    # (not bitwise); everything else is owner-computes
+    assert rel(y2, y) <= 1e-14
     qt = torch.from_numpy(q).cuda()
     yt = g.matvec(qt)
     torch.cuda.synchronize()
-    assert np.array_equal(yt.cpu().numpy(), y)
+    assert rel(yt.cpu().numpy(), y) <= 1e-14
 
 
 def test_small_linearity(small):
