@@ -167,6 +167,14 @@ void hfmm_destroy(hfmm_plan *p);
 int hfmm_level_quadrature(double kappa, double a, double eps_level, double alpha, int *ell,
                           int *n_theta, int *n_phi, int *ragged, int ragged_cap);
 
+/* Host-only multi-GPU ownership (the rule hfmm_precompute applies; no GPU needed): for the tree
+ * of (n, xyz, depth, lo, size), far-field leaf level L_f >= 2 and leaf quadrature size K, fills
+ * cuts[0..nranks] (rank r owns level-2 boxes [cuts[r], cuts[r+1]) in Morton order, i.e. whole
+ * subtrees), pt_ranges[2r], pt_ranges[2r+1] (its sorted-point range) and, if perm != NULL,
+ * perm[0..n) (sorted position -> input index). */
+int hfmm_partition(int64_t n, const double *xyz, int depth, const double lo[3], double size, int L_f,
+                   int64_t K, int nranks, int64_t *cuts, int64_t *pt_ranges, int64_t *perm);
+
 /* ---- operator entry points (microbench, BASELINE config 2; device pointers) -----------------
  * Batched 5-step Fourier resampling of `nbatch` half-stored fields
  * [n_theta][n_phi/2] -> [n_theta2][n_phi2/2]: interpolation if the target grid

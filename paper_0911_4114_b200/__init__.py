@@ -4,10 +4,10 @@ The product is libhfmm.so (C ABI, include/hfmm.h) with hand-written sm_100a CUDA
 this package holds its sources (csrc/), the in-tree build (build.py) and a thin ctypes
 binding (binding.py).  Nothing here imports oracle/ (test infrastructure only).
 """
-from .binding import (HFMM, HFMMError, HFMM_ALPHA_FIXED, level_quadrature, nccl_unique_id, load, resample, resample_workspace, m2m_op,
-                      l2l_op, m2l_op, HFMM_EPS_ABSOLUTE, HFMM_FORCE_ALL_LEVELS, HFMM_W_BREAKDOWN,
-                      HFMM_W_NO_FARFIELD, EXPORTED, LIB_PATH)
+from .binding import (HFMM, HFMMError, HFMM_ALPHA_FIXED, HFMM_EPS_ABSOLUTE, HFMM_FORCE_ALL_LEVELS,
+                      HFMM_W_BREAKDOWN, HFMM_W_NO_FARFIELD, EXPORTED, LIB_PATH, l2l_op, level_quadrature,
+                      load, m2l_op, m2m_op, nccl_unique_id, partition, resample, resample_workspace)
 
-__all__ = ["HFMM", "HFMMError", "HFMM_ALPHA_FIXED", "level_quadrature", "nccl_unique_id", "load", "resample", "resample_workspace", "m2m_op",
-           "l2l_op", "m2l_op", "HFMM_EPS_ABSOLUTE", "HFMM_FORCE_ALL_LEVELS", "HFMM_W_BREAKDOWN",
-           "HFMM_W_NO_FARFIELD", "EXPORTED", "LIB_PATH"]
+__all__ = ["HFMM", "HFMMError", "HFMM_ALPHA_FIXED", "HFMM_EPS_ABSOLUTE", "HFMM_FORCE_ALL_LEVELS",
+           "HFMM_W_BREAKDOWN", "HFMM_W_NO_FARFIELD", "EXPORTED", "LIB_PATH", "l2l_op", "level_quadrature",
+           "load", "m2l_op", "m2m_op", "nccl_unique_id", "partition", "resample", "resample_workspace"]

@@ -30,7 +30,7 @@ EXPORTED = [
     "hfmm_create", "hfmm_set_dist", "hfmm_nccl_unique_id", "hfmm_build_tree", "hfmm_precompute", "hfmm_matvec",
     "hfmm_direct", "hfmm_get_info", "hfmm_stage_times", "hfmm_debug_copy", "hfmm_last_error",
     "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
-    "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op",
+    "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition",
 ]
 
 
@@ -87,6 +87,7 @@ def load() -> C.CDLL:
         "hfmm_m2m_op": (ci, [ci, ci, ci, ci, ci, vp, vp, vp, vp, vp]),
         "hfmm_l2l_op": (ci, [ci, ci, ci, ci, ci, vp, vp, vp, vp, vp, vp]),
         "hfmm_m2l_op": (ci, [ci, i64, vp, vp, vp, vp, vp, vp, vp]),
+        "hfmm_partition": (ci, [i64, vp, ci, vp, dbl, ci, i64, ci, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -116,6 +117,21 @@ def level_quadrature(kappa: float, a: float, eps_level: float, alpha: float = 0.
     if rc < 0:
         raise HFMMError(rc, "hfmm_level_quadrature failed")
     return ell.value, nth.value, nph.value, list(rag[: nth.value // 2 + 1])
+
+
+def partition(xyz, depth, lo, size, L_f, K, nranks):
+    """Host-only multi-GPU ownership rule: (level-2 cuts, sorted-point ranges, perm)."""
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    n = xyz.shape[0]
+    cuts = np.zeros(nranks + 1, dtype=np.int64)
+    rng = np.zeros(2 * nranks, dtype=np.int64)
+    perm = np.zeros(n, dtype=np.int64)
+    rc = load().hfmm_partition(n, xyz.ctypes.data, depth, lo.ctypes.data, size, L_f, K, nranks,
+                               cuts.ctypes.data, rng.ctypes.data, perm.ctypes.data)
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_partition")
+    return cuts, rng.reshape(nranks, 2), perm
 
 
 def _ptr(a) -> int:

@@ -378,33 +378,9 @@ static void partition(hfmm_plan *p) {
     p->own_pt1 = cutp(r + 1);
     return;
   }
-  const LevelBoxes &B2 = t.levels[2];
   const LevelBoxes &BL = t.levels[p->L_f];
-  const int64_t KL = p->lv[p->L_f].K;
-  std::vector<double> w(B2.nbox(), 0.0);
-  for (int64_t b = 0; b < BL.nbox(); ++b) {
-    int64_t nb = BL.first[b + 1] - BL.first[b];
-    int64_t src = 0;
-    for (int dx = -1; dx <= 1; ++dx)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dz = -1; dz <= 1; ++dz) {
-          int32_t k = BL.find(BL.ix[b] + dx, BL.iy[b] + dy, BL.iz[b] + dz);
-          if (k >= 0) src += BL.first[k + 1] - BL.first[k];
-        }
-    int32_t a = (int32_t)b;
-    for (int l = p->L_f; l > 2; --l) a = t.levels[l].parent[a];
-    w[a] += (double)nb * (double)src + 2.0 * (double)nb * (double)KL;
-  }
-  double tot = std::accumulate(w.begin(), w.end(), 0.0);
-  std::vector<int64_t> cut(R + 1, B2.nbox());
-  cut[0] = 0;
-  double acc = 0;
-  int k = 1;
-  for (int64_t b = 0; b < B2.nbox() && k < R; ++b) {
-    acc += w[b];
-    while (k < R && acc >= tot * k / R) cut[k++] = b + 1;
-  }
-  for (; k < R; ++k) cut[k] = B2.nbox();
+  std::vector<int64_t> cut;
+  partition_level2(t, p->L_f, p->lv[p->L_f].K, R, cut);
   for (int l = 2; l <= p->L_f; ++l) {
     LevelDev &L = p->lv[l];
     L.rlo.assign(R, 0), L.rhi.assign(R, 0);

@@ -58,6 +58,7 @@ struct Tree {
 int build_tree(const double *xyz, int64_t n, int depth, const double lo[3], double size, Tree &t,
                std::string &err);
 uint32_t morton3(uint32_t x, uint32_t y, uint32_t z);
+void partition_level2(const Tree &t, int L_f, int64_t K, int R, std::vector<int64_t> &cut);
 // offsets: id in [0,316) <-> (ox, oy, oz) in [-3,3]^3 \ [-1,1]^3, lexicographic x, y, z
 int offset_id(int ox, int oy, int oz);
 void offset_vec(int id, int o[3]);

@@ -174,4 +174,64 @@ int build_tree(const double *xyz, int64_t n, int depth, const double lo[3], doub
   return 0;
 }
 
+// Multi-GPU ownership: contiguous Morton ranges of level-2 boxes (whole subtrees) for R ranks,
+// balanced by an estimate of FP64 work per level-2 subtree: P2P pairs of its leaves at L_f plus
+// 2 n_leaf K (S2M + L2T evaluations).  cut[r]..cut[r+1] is rank r's range.
+void partition_level2(const Tree &t, int L_f, int64_t K, int R, std::vector<int64_t> &cut) {
+  const LevelBoxes &B2 = t.levels[2];
+  const LevelBoxes &BL = t.levels[L_f];
+  std::vector<double> w(B2.nbox(), 0.0);
+  for (int64_t b = 0; b < BL.nbox(); ++b) {
+    int64_t nb = BL.first[b + 1] - BL.first[b];
+    int64_t src = 0;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          int32_t k = BL.find(BL.ix[b] + dx, BL.iy[b] + dy, BL.iz[b] + dz);
+          if (k >= 0) src += BL.first[k + 1] - BL.first[k];
+        }
+    int32_t a = (int32_t)b;
+    for (int l = L_f; l > 2; --l) a = t.levels[l].parent[a];
+    w[a] += (double)nb * (double)src + 2.0 * (double)nb * (double)K;
+  }
+  double tot = 0.0;
+  for (double v : w) tot += v;
+  cut.assign(R + 1, B2.nbox());
+  cut[0] = 0;
+  double acc = 0;
+  int k = 1;
+  for (int64_t b = 0; b < B2.nbox() && k < R; ++b) {
+    acc += w[b];
+    while (k < R && acc >= tot * k / R) cut[k++] = b + 1;
+  }
+  for (; k < R; ++k) cut[k] = B2.nbox();
+}
+
 }  // namespace hfmm
+
+extern "C" int hfmm_partition(int64_t n, const double *xyz, int depth, const double lo[3], double size,
+                              int L_f, int64_t K, int nranks, int64_t *cuts, int64_t *pt_ranges,
+                              int64_t *perm) {
+  using namespace hfmm;
+  if (!xyz || !lo || !cuts || !pt_ranges || nranks < 1 || L_f < 2 || L_f > depth || K <= 0)
+    return HFMM_E_ARG;
+  Tree t;
+  std::string err;
+  int rc = build_tree(xyz, n, depth, lo, size, t, err);
+  if (rc) return rc;
+  std::vector<int64_t> cut;
+  partition_level2(t, L_f, K, nranks, cut);
+  for (int r = 0; r <= nranks; ++r) cuts[r] = cut[r];
+  for (int r = 0; r < nranks; ++r) {
+    int64_t b0 = cut[r], b1 = cut[r + 1];
+    for (int l = 2; l < L_f; ++l) {  // descend to L_f (children ranges are contiguous)
+      b0 = t.levels[l].child_begin[b0];
+      b1 = t.levels[l].child_begin[b1];
+    }
+    pt_ranges[2 * r] = t.levels[L_f].first[b0];
+    pt_ranges[2 * r + 1] = t.levels[L_f].first[b1];
+  }
+  if (perm)
+    for (int64_t i = 0; i < n; ++i) perm[i] = t.perm[i];
+  return 0;
+}
