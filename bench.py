@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ops", default="8,16,32,64",
+                    help="C2 operator microbench bandwidths B (comma list; '' to skip)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -172,6 +174,91 @@ def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
         desc = (f"oracle passes on {len(leaves)} of {len(lev.boxes)} far-field leaves ({len(pts)} points: S2M, "
                 f"L2T, P2P), M2L on 2 boxes/level, M2M+L2L on 2 children/level; each term scaled by its unit count")
         return total, desc, 1
+
+
+def hbm_peak():
+    """Measured HBM copy bandwidth (GB/s) from MEASURED_PEAKS.json, else the guide's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def bench_operators(bandwidths, reps: int = 5, fp64_peak_tflops: float = 37.2):
+    """BASELINE.json configs[1] ("C2"): operator microbench on 65,536 boxes of random complex128 fields.
+
+    Child grid (2B, 2B) -> parent (4B, 4B), half storage [N_theta][N_phi/2] (SURVEY D-1):
+      interp  65,536 x R_{2B->4B} out of place          anterp  65,536 x R_{4B->2B}
+      m2m     8,192 parents x 8 children, shift + sum    l2l     8,192 parents -> 8 children, conj shift, +I
+      m2l     65,536 targets x 189 partners (periodic 64x32x32 lattice, Morton order), 316 tables
+    Algorithmic bytes: every input read once and every output written once (tables once).
+    Times: CUDA events on the launching stream, mean of `reps` after one warm-up, L2 flushed between."""
+    import torch
+    import paper_0911_4114_b200 as hf
+    from workloads import MICROBENCH, c2_lattice, c2_grids
+    peak, src = hbm_peak()
+    nbox = MICROBENCH["boxes"]
+    _, row, srcs, oid, _ = c2_lattice()
+    row_d, src_d, oid_d = (torch.from_numpy(a).cuda() for a in (row, srcs, oid))
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    out = {"hbm_peak_gbs": peak, "hbm_peak_source": src, "boxes": nbox, "fp64_peak_tflops": fp64_peak_tflops}
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(MICROBENCH["seed"])
+
+    def crandn(*shape):
+        return torch.randn(*shape, 2, dtype=torch.float64, device="cuda", generator=gen).view(torch.complex128)[..., 0]
+
+    def timed(fn):
+        fn()
+        ms = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(reps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return statistics.mean(ms)
+
+    for B in bandwidths:
+        (nth, nph), (nth2, nph2) = c2_grids(B)
+        K, K2 = nth * nph // 2, nth2 * nph2 // 2
+        npar = nbox // 8
+        child = crandn(nbox, K)
+        parent = torch.empty(nbox, K2, dtype=torch.complex128, device="cuda")
+        res = {}
+
+        def rec(name, ms, nbytes, flops=None):
+            d = {"ms": ms, "gbs": nbytes / ms / 1e6, "frac_hbm": nbytes / ms / 1e6 / peak, "bytes": nbytes}
+            if flops is not None:
+                d["tflops"] = flops / ms / 1e9
+                d["frac_fp64"] = d["tflops"] / fp64_peak_tflops
+            res[name] = d
+
+        ws = max(hf.resample_workspace(nbox, nth, nph, nth2, nph2), hf.resample_workspace(nbox, nth2, nph2, nth, nph))
+        work = torch.empty(max(ws, 16), dtype=torch.uint8, device="cuda") if ws > 0 else None
+        rec("interp", timed(lambda: hf.resample(child, nth, nph, nth2, nph2, parent, work=work)), nbox * (K + K2) * 16)
+        child2 = torch.empty_like(child)
+        rec("anterp", timed(lambda: hf.resample(parent, nth2, nph2, nth, nph, child2, work=work)), nbox * (K + K2) * 16)
+        shift = torch.polar(torch.ones(8, K2, dtype=torch.float64, device="cuda"),
+                            2 * math.pi * torch.rand(8, K2, dtype=torch.float64, device="cuda", generator=gen))
+        par = parent[:npar]
+        rec("m2m", timed(lambda: hf.m2m_op(child, shift, par, nth, nph, nth2, nph2, work=work)),
+            (nbox * K + npar * K2 + 8 * K2) * 16)
+        inc = crandn(nbox, K)
+        rec("l2l", timed(lambda: hf.l2l_op(par, shift, inc, child2, nth2, nph2, nth, nph, work=work)),
+            (npar * K2 + 2 * nbox * K + 8 * K2) * 16)
+        del inc, parent, par, work
+        T = crandn(316, K)
+        rec("m2l", timed(lambda: hf.m2l_op(row_d, src_d, oid_d, T, child, child2)),
+            (2 * nbox * K + 316 * K) * 16, flops=8.0 * int(row[-1]) * K)
+        out[f"B{B}"] = res
+        del child, child2, T, shift
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_reference(args, cfg, rank, world):
@@ -328,6 +415,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s, desc, cores = oracle_sample(cfg, x, q)
         line["cpu_baseline"] = {"value": 1.0 / s, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": desc}
+    if world == 1 and args.ops:
+        g.close()
+        del qd, yd, flush, qh, yh
+        torch.cuda.empty_cache()
+        line["operators"] = bench_operators([int(b) for b in args.ops.split(",")], fp64_peak_tflops=peak_tflops)
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.json_out:

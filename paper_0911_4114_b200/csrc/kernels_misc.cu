@@ -23,8 +23,8 @@ __global__ void __launch_bounds__(M2L_TPB) m2l_kernel(int32_t box0, int64_t K, c
                                                       const double2 *__restrict__ T,
                                                       const double2 *__restrict__ M,
                                                       double2 *__restrict__ I) {
-  const int32_t a = box0 + blockIdx.y;
-  const int64_t k = (int64_t)blockIdx.x * M2L_TPB + threadIdx.x;
+  const int32_t a = box0 + blockIdx.x;   // boxes on x (gridDim.y is limited to 65535)
+  const int64_t k = (int64_t)blockIdx.y * M2L_TPB + threadIdx.x;
   if (k >= K) return;
   double2 acc = make_double2(0.0, 0.0);
   const int32_t e0 = row[a], e1 = row[a + 1];
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(M2L_TPB) m2l_kernel(int32_t box0, int64_t K, c
 void launch_m2l(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
                 const int32_t *oid, const double2 *T, const double2 *M, double2 *I, cudaStream_t s) {
   if (box1 <= box0 || K <= 0) return;
-  dim3 grid((unsigned)((K + M2L_TPB - 1) / M2L_TPB), (unsigned)(box1 - box0));
+  dim3 grid((unsigned)(box1 - box0), (unsigned)((K + M2L_TPB - 1) / M2L_TPB));
   m2l_kernel<<<grid, M2L_TPB, 0, s>>>(box0, K, row, src, oid, T, M, I);
 }
 

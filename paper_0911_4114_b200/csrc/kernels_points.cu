@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(S2M_TPB, 5) s2m_kernel(PointsDev pts, const in
   __shared__ double sx[S2M_TPB], sy[S2M_TPB], sz[S2M_TPB];
   __shared__ double2 sq[S2M_TPB];
   fill_exp_table(tab);
-  const int32_t b = box0 + blockIdx.y;
-  const int64_t k0 = (int64_t)blockIdx.x * (2 * S2M_TPB) + threadIdx.x, k1 = k0 + S2M_TPB;
+  const int32_t b = box0 + blockIdx.x;   // boxes on x (gridDim.y is limited to 65535)
+  const int64_t k0 = (int64_t)blockIdx.y * (2 * S2M_TPB) + threadIdx.x, k1 = k0 + S2M_TPB;
   const double kx0 = k0 < K ? ks[k0] : 0.0, ky0 = k0 < K ? ks[K + k0] : 0.0, kz0 = k0 < K ? ks[2 * K + k0] : 0.0;
   const double kx1 = k1 < K ? ks[k1] : 0.0, ky1 = k1 < K ? ks[K + k1] : 0.0, kz1 = k1 < K ? ks[2 * K + k1] : 0.0;
   const double c0x = cx[b], c0y = cy[b], c0z = cz[b];
@@ -312,7 +312,7 @@ void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const dou
   if (box1 <= box0) return;
   ExpConsts ec;
   step_split(&ec.shi, &ec.slo);
-  dim3 grid((unsigned)((K + 2 * S2M_TPB - 1) / (2 * S2M_TPB)), (unsigned)(box1 - box0));
+  dim3 grid((unsigned)(box1 - box0), (unsigned)((K + 2 * S2M_TPB - 1) / (2 * S2M_TPB)));
   s2m_kernel<<<grid, S2M_TPB, 0, s>>>(pts, first, cx, cy, cz, box0, ks, K, ec, M);
 }
 

@@ -1,0 +1,136 @@
+"""GPU parity of the operator entry points at BASELINE config 2 ("C2") sizes.
+
+65,536 boxes of random complex128 fields, child grid (2B, 2B) -> parent (4B, 4B), in the launch
+configuration bench.py's operator microbench times (the same entry points, full batch); checked
+against the oracle on sampled boxes:
+  interp / anterp  oracle.resample.resample_half_batch (5-step procedure)
+  m2m              sum over the 8 children of shift_c * R(child_c)                 (R-10)
+  l2l              R(conj(shift_c) * parent) + I_c                                  (R-10)
+  m2l              sum over oracle.tree.interaction_list on the periodic lattice
+Tolerance: 1e-13 relative (normwise over the sampled boxes): every output is a short sum of
+O(1) terms computed in FP64 by two different algorithms (FFT vs dense DFT matrices).
+"""
+import numpy as np
+import pytest
+
+from workloads import MICROBENCH, c2_lattice, c2_grids
+from oracle.resample import resample_half_batch
+from oracle.tree import Level, interaction_list
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-13
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
+
+
+@pytest.fixture(scope="module")
+def hf():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_0911_4114_b200 as mod
+    from paper_0911_4114_b200.build import build
+    build(verbose=False)
+    return mod
+
+
+@pytest.fixture(scope="module")
+def lattice():
+    return c2_lattice()
+
+
+def crandn(gen, *shape):
+    import torch
+    return torch.randn(*shape, 2, dtype=torch.float64, device="cuda", generator=gen).view(torch.complex128)[..., 0]
+
+
+@pytest.mark.parametrize("B,nbox", [(8, 65536), (16, 65536), (32, 16384), (64, 65536)])
+def test_c2_resample_ops(hf, B, nbox):
+    import torch
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(MICROBENCH["seed"] + B)
+    (nth, nph), (nth2, nph2) = c2_grids(B)
+    K, K2 = nth * nph // 2, nth2 * nph2 // 2
+    child = crandn(gen, nbox, K)
+    parent = torch.empty(nbox, K2, dtype=torch.complex128, device="cuda")
+    hf.resample(child, nth, nph, nth2, nph2, parent)
+    rng = np.random.default_rng(B)
+    s = np.sort(rng.choice(nbox, 6, replace=False))
+    s = np.concatenate([[0], s, [nbox - 1]])                      # first and last box of the batch
+    ch = child[s].cpu().numpy().reshape(-1, nth, nph // 2)
+    ref = resample_half_batch(ch, nph, nth2, nph2).reshape(len(s), -1)
+    assert rel(parent[s].cpu().numpy(), ref) <= TOL
+    # anterpolation of the (band-limited) interpolated fields, and of random parent data
+    back = torch.empty_like(child)
+    pr = crandn(gen, nbox, K2)
+    hf.resample(pr, nth2, nph2, nth, nph, back)
+    refb = resample_half_batch(pr[s].cpu().numpy().reshape(-1, nth2, nph2 // 2), nph2, nth, nph).reshape(len(s), -1)
+    assert rel(back[s].cpu().numpy(), refb) <= TOL
+    del pr
+    # fused M2M: parents p < nbox/8, children 8p..8p+7 (octant = c % 8)
+    npar = nbox // 8
+    shift = torch.polar(torch.ones(8, K2, dtype=torch.float64, device="cuda"),
+                        2 * np.pi * torch.rand(8, K2, dtype=torch.float64, device="cuda", generator=gen))
+    par = parent[:npar]
+    hf.m2m_op(child, shift, par, nth, nph, nth2, nph2)
+    sh = shift.cpu().numpy()
+    ps = np.array([0, npar // 3, npar - 1])
+    for p in ps:
+        chp = child[8 * p: 8 * p + 8].cpu().numpy().reshape(8, nth, nph // 2)
+        R = resample_half_batch(chp, nph, nth2, nph2).reshape(8, -1)
+        assert rel(par[p].cpu().numpy(), (sh * R).sum(0)) <= TOL
+    # fused L2L: children c of parent c // 8, octant c % 8, plus incoming I_c
+    inc = crandn(gen, nbox, K)
+    out = torch.empty_like(child)
+    hf.l2l_op(par, shift, inc, out, nth2, nph2, nth, nph)
+    cs = np.array([0, 5, nbox // 2 + 3, nbox - 1])
+    parh = par.cpu().numpy() if npar * K2 * 16 < 2e9 else None
+    for c in cs:
+        pv = parh[c // 8] if parh is not None else par[c // 8].cpu().numpy()
+        prod = (np.conj(sh[c % 8]) * pv).reshape(1, nth2, nph2 // 2)
+        ref = resample_half_batch(prod, nph2, nth, nph).reshape(-1) + inc[c].cpu().numpy()
+        assert rel(out[c].cpu().numpy(), ref) <= TOL
+
+
+class _Periodic(dict):
+    """Box index of the periodic lattice for oracle.tree.interaction_list (wraps coordinates)."""
+
+    def __init__(self, g, dims):
+        super().__init__()
+        self.dims = dims
+        self.pos = {tuple(int(v) for v in c): k for k, c in enumerate(g)}
+
+    def get(self, c, default=None):
+        return self.pos.get(tuple(int(c[d]) % self.dims[d] for d in range(3)), default)
+
+
+@pytest.mark.parametrize("B", [8, 32])
+def test_c2_m2l(hf, lattice, B):
+    import torch
+    g, row, src, oid, offs = lattice
+    nbox = len(g)
+    assert np.all(np.diff(row) == 189)
+    (nth, nph), _ = c2_grids(B)
+    K = nth * nph // 2
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(MICROBENCH["seed"] + 100 + B)
+    M = crandn(gen, nbox, K)
+    T = crandn(gen, 316, K)
+    I = torch.empty_like(M)
+    r, s_, o_ = (torch.from_numpy(a).cuda() for a in (row, src, oid))
+    hf.m2l_op(r, s_, o_, T, M, I)
+    lev = Level(0, 1.0, [tuple(c) for c in g], _Periodic(g, MICROBENCH["lattice"]), [], np.zeros((nbox, 3)))
+    tid = {tuple(int(v) for v in o): k for k, o in enumerate(offs)}
+    Th = T.cpu().numpy()
+    rng = np.random.default_rng(B)
+    for a in np.concatenate([[0, nbox - 1], rng.choice(nbox, 6, replace=False)]):
+        il = interaction_list(lev, tuple(int(v) for v in g[a]))
+        assert len(il) == 189
+        # the CSR handed to the library is the oracle's list (as a set of (source, offset))
+        assert sorted((int(k), tid[o]) for k, o in il) == sorted(zip(src[row[a]:row[a + 1]].tolist(),
+                                                                     oid[row[a]:row[a + 1]].tolist()))
+        ks = [k for k, _ in il]
+        Mh = M[ks].cpu().numpy()
+        ref = sum(Th[tid[o]] * Mh[j] for j, (_, o) in enumerate(il))
+        assert rel(I[a].cpu().numpy(), ref) <= TOL

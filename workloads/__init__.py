@@ -125,3 +125,44 @@ def microbench_fields(nbox: int, nth: int, nph_half: int, seed: int) -> np.ndarr
     re = rng.standard_normal((nbox, nth, nph_half))
     im = rng.standard_normal((nbox, nth, nph_half))
     return re + 1j * im
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE.json configs[1] (operator microbench, "C2"): a periodic 64 x 32 x 32 lattice of boxes
+# at one level, boxes numbered in Morton order.  The interaction list of every box has exactly 189
+# entries on a periodic lattice (not a neighbour, parent is a neighbour of the parent;
+# 189).  This is the *input* of the M2L operator entry point (a CSR it takes as
+# arguments); the oracle-side test checks it against oracle/tree.py's own rule on sampled boxes.
+# Offset ids: lexicographic (x, then y, then z) over [-3,3]^3 minus [-1,1]^3 (316 offsets).
+def _spread3(v: np.ndarray) -> np.ndarray:
+    out = np.zeros_like(v, dtype=np.int64)
+    for bit in range(10):
+        out |= ((v >> bit) & 1) << (3 * bit)
+    return out
+
+
+def c2_lattice(dims=MICROBENCH["lattice"]):
+    """Box coordinates [nbox, 3] (Morton order) and the periodic interaction CSR (row, src, oid)."""
+    nx, ny, nz = dims
+    g = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1).reshape(-1, 3)
+    key = (_spread3(g[:, 0]) << 2) | (_spread3(g[:, 1]) << 1) | _spread3(g[:, 2])
+    g = g[np.argsort(key, kind="stable")]
+    lin = np.empty(nx * ny * nz, dtype=np.int64)                 # (x, y, z) -> Morton position
+    lin[(g[:, 0] * ny + g[:, 1]) * nz + g[:, 2]] = np.arange(len(g))
+    offs = np.array([(a, b, c) for a in range(-3, 4) for b in range(-3, 4) for c in range(-3, 4)
+                     if max(abs(a), abs(b), abs(c)) >= 2], dtype=np.int64)        # 316, lexicographic
+    tgt = g[:, None, :]                                                           # [nbox, 1, 3]
+    src = tgt + offs[None, :, :]                                                  # unwrapped
+    ok = np.all(np.abs((src >> 1) - (tgt >> 1)) <= 1, axis=2)                     # parents adjacent
+    dimv = np.array(dims)
+    w = src % dimv
+    sidx = lin[(w[..., 0] * ny + w[..., 1]) * nz + w[..., 2]]
+    oid = np.broadcast_to(np.arange(len(offs)), ok.shape)
+    counts = ok.sum(axis=1)
+    row = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    return g, row, sidx[ok].astype(np.int32), oid[ok].astype(np.int32), offs
+
+
+def c2_grids(B: int):
+    """Child grid (N_theta, N_phi) = (2B, 2B) and parent grid (4B, 4B) of bandwidth B (SURVEY D-1)."""
+    return (2 * B, 2 * B), (4 * B, 4 * B)
