@@ -29,11 +29,12 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-# FP64 flops (FMA = 2) of the P2P arithmetic as implemented:
-# one kernel evaluation G = e^{i kappa R}/R costs 43 (difference 3, r^2 5, rsqrt + Newton 8,
-# r and kappa r 2, e^{ix} 23, 1/r scaling 2); every ORDERED pair adds a complex MAC (8).  The
+# FP64 flops (FMA = 2) of the P2P arithmetic as implemented (DESIGN.md "Kernels and their
+# rooflines"): one kernel evaluation G = e^{i kappa R}/R on positions pre-scaled to table steps
+# costs 38 (difference 3, r^2 5, rsqrt Newton step 8, R 1, e^{ih R_u} 19, 1/R scaling 2; the
+# MUFU.RSQ64H seed is not an FP64-pipe op); every ORDERED pair adds a complex MAC (8).  The
 # symmetric kernel evaluates G once per unordered pair and applies it to both rows.
-P2P_FLOPS_PER_EVAL = 43
+P2P_FLOPS_PER_EVAL = 38
 P2P_FLOPS_PER_MAC = 8
 
 

@@ -93,7 +93,7 @@ typedef struct {
   double kappa, eps, alpha, tau;
   int nlevels;             /* entries filled in level[] (levels 2..D)                        */
   hfmm_level_info level[HFMM_MAX_LEVELS];
-  int64_t p2p_pairs;       /* ordered near-field pairs (incl. self pairs skipped)            */
+  int64_t p2p_pairs;       /* ordered near-field pairs i != j (owned targets)                */
   int64_t p2p_sym_pairs;   /* unordered pairs of them evaluated once (symmetric kernel)      */
   int64_t s2m_evals;       /* points x directions at L_f                                    */
   int rank, nranks;

@@ -13,7 +13,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhfmm.so")
+# HFMM_LIB: an alternative in-tree build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("HFMM_LIB") or os.path.join(_HERE, "libhfmm.so")
 
 HFMM_OK = 0
 HFMM_W_BREAKDOWN = 1

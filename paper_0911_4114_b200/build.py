@@ -45,14 +45,16 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = True, defines=(), out: str = None) -> str:
+    """Compile every source for sm_100a and link libhfmm.so (or `out`, with extra -D `defines`)."""
+    if out is None and not force and not needs_build():
         return LIB
     inc, lib = _nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-              "-Xcompiler", "-fPIC,-fopenmp", "-I", os.path.join(ROOT, "include"), "-I", inc]
+              "-Xcompiler", "-fPIC,-fopenmp", "-I", os.path.join(ROOT, "include"), "-I", inc] + \
+             ["-D" + d for d in defines]
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
@@ -65,12 +67,12 @@ def build(force: bool = False, verbose: bool = True) -> str:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
         objs.append(obj)
-    link = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + \
+    link = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out or LIB] + objs + \
            ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib, "-Xcompiler", "-fopenmp", "-lgomp"]
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.check_call(link)
-    return LIB
+    return out or LIB
 
 
 if __name__ == "__main__":

@@ -103,18 +103,19 @@ struct hfmm_plan {
   int near_level = 0;        // level of the near-field boxes (L_f or 0)
   int64_t own_pt0 = 0, own_pt1 = 0;
   int64_t *first_near = nullptr;  // point ranges of near-level boxes
-  int32_t *nb_row = nullptr, *nb_box = nullptr;
-  int32_t *tile_leaf = nullptr;
+  int32_t *tile_leaf = nullptr;    // L2T tiles (kTile targets of one far-field leaf)
   int64_t *tile_begin = nullptr;
   int64_t ntiles = 0;
-  int32_t *sym_leaf = nullptr, *sym_src = nullptr;  // symmetric P2P work items
-  int64_t *sym_begin = nullptr;
-  int64_t nsym = 0, p2p_sym_pairs = 0;
+  // P2P work items [n][4] = (t0, t1, s0, s1) by kind (P2P_SYM, P2P_DIAG, P2P_ORD), and the
+  // all-pairs items of hfmm_direct; positions pre-scaled to table steps (kappa-dependent)
+  int64_t *p2p_items[3] = {nullptr, nullptr, nullptr};
+  int64_t p2p_nitems[3] = {0, 0, 0};
+  int64_t *dir_items = nullptr;
+  int64_t dir_nitems = 0;
+  double *ux = nullptr, *uy = nullptr, *uz = nullptr;
+  double uscale = 0;               // kappa TAB / (2 pi)
+  int64_t p2p_sym_pairs = 0;
   double dummy_t[3] = {0, 0, 0}, dummy_s[3] = {0, 0, 0};
-  // all-pairs (direct) tiles
-  int32_t *dir_tile_leaf = nullptr, *dir_nb_row = nullptr, *dir_nb_box = nullptr;
-  int64_t *dir_tile_begin = nullptr, *dir_first = nullptr;
-  int64_t dir_ntiles = 0;
   double2 *tmp = nullptr;
   size_t tmp_elems = 0;
   hfmm_info info{};
@@ -151,13 +152,15 @@ static void free_levels(hfmm_plan *p) {
       if (ptr) cudaFree(ptr);
   }
   p->lv.clear();
-  for (void *ptr : {(void *)p->first_near, (void *)p->nb_row, (void *)p->nb_box, (void *)p->tile_leaf,
-                    (void *)p->tile_begin, (void *)p->tmp, (void *)p->y_far, (void *)p->sym_leaf,
-                    (void *)p->sym_src, (void *)p->sym_begin})
+  for (void *ptr : {(void *)p->first_near, (void *)p->tile_leaf, (void *)p->tile_begin, (void *)p->tmp,
+                    (void *)p->y_far, (void *)p->p2p_items[0], (void *)p->p2p_items[1], (void *)p->p2p_items[2],
+                    (void *)p->dir_items, (void *)p->ux, (void *)p->uy, (void *)p->uz})
     if (ptr) cudaFree(ptr);
-  p->first_near = nullptr, p->nb_row = p->nb_box = p->tile_leaf = nullptr;
+  p->first_near = nullptr, p->tile_leaf = nullptr;
   p->tile_begin = nullptr, p->tmp = nullptr, p->y_far = nullptr;
-  p->sym_leaf = p->sym_src = nullptr, p->sym_begin = nullptr, p->nsym = 0;
+  for (int k = 0; k < 3; ++k) p->p2p_items[k] = nullptr, p->p2p_nitems[k] = 0;
+  p->dir_items = nullptr, p->dir_nitems = 0;
+  p->ux = p->uy = p->uz = nullptr;
   p->tmp_elems = 0;
   p->ntiles = 0;
   p->have_plan = false;
@@ -165,15 +168,11 @@ static void free_levels(hfmm_plan *p) {
 
 static void free_points(hfmm_plan *p) {
   for (void *ptr : {(void *)p->px, (void *)p->py, (void *)p->pz, (void *)p->perm, (void *)p->q_in,
-                    (void *)p->q_sorted, (void *)p->y_out, (void *)p->y_near, (void *)p->dir_tile_leaf,
-                    (void *)p->dir_nb_row, (void *)p->dir_nb_box, (void *)p->dir_tile_begin,
-                    (void *)p->dir_first})
+                    (void *)p->q_sorted, (void *)p->y_out, (void *)p->y_near})
     if (ptr) cudaFree(ptr);
   p->px = p->py = p->pz = nullptr;
   p->perm = nullptr;
   p->q_in = p->q_sorted = p->y_out = p->y_near = nullptr;
-  p->dir_tile_leaf = p->dir_nb_row = p->dir_nb_box = nullptr;
-  p->dir_tile_begin = p->dir_first = nullptr;
   p->have_tree = false;
 }
 
@@ -258,18 +257,6 @@ extern "C" int hfmm_build_tree(hfmm_plan *p, int64_t n, const double *xyz, int d
   if (!p->px || !p->py || !p->pz || !p->perm || !p->q_in || !p->q_sorted || !p->y_out || !p->y_near) {
     p->err = "hfmm_build_tree: device allocation failed";
     return HFMM_E_NOMEM;
-  }
-  // all-pairs tiles for hfmm_direct: one box (the root) containing every point
-  {
-    std::vector<int32_t> tl;
-    std::vector<int64_t> tb;
-    for (int64_t s = 0; s < n; s += kTile) tl.push_back(0), tb.push_back(s);
-    p->dir_tile_leaf = dupload(tl);
-    p->dir_tile_begin = dupload(tb);
-    p->dir_ntiles = (int64_t)tl.size();
-    p->dir_nb_row = dupload(std::vector<int32_t>{0, 1});
-    p->dir_nb_box = dupload(std::vector<int32_t>{0});
-    p->dir_first = dupload(std::vector<int64_t>{0, n});
   }
   p->have_tree = true;
   return HFMM_OK;
@@ -502,7 +489,11 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     L.cx = dupload(cx), L.cy = dupload(cy), L.cz = dupload(cz);
     std::vector<double> ks;
     grid_dirs(L.nth, L.nph, kappa, ks);
-    L.ks = dupload(ks);
+    {
+      std::vector<double> ksu(ks);  // kernels take kappa s in table steps (h = 2 pi / TAB_STEPS)
+      for (auto &v : ksu) v *= (double)TAB_STEPS / (2.0 * kPi);
+      L.ks = dupload(ksu);
+    }
     L.M = dalloc<double2>((size_t)L.nbox * L.K);
     L.I = dalloc<double2>((size_t)L.nbox * L.K);
     L.L = dalloc<double2>((size_t)L.nbox * L.K);
@@ -563,56 +554,103 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       return HFMM_E_NOMEM;
     }
   }
-  // near field at L_f (neighbour lists) or all pairs at the root
+  // near field at L_f (neighbour lists) or all pairs at the root, as P2P work items
   p->near_level = p->L_f >= 2 ? p->L_f : 0;
   {
-    // Ordered work (rows only): the leaf itself and neighbours owned by another rank.
-    // Symmetric work (rows + columns, each unordered pair once): owned neighbours beta > alpha.
     const LevelBoxes &B = t.levels[p->near_level];
-    int64_t lo = 0, hi = B.nbox();
-    if (p->L_f >= 2) lo = p->lv[p->L_f].own0, hi = p->lv[p->L_f].own1;
-    auto owned = [&](int64_t k) { return k >= lo && k < hi; };
-    std::vector<int32_t> row(1, 0), nb, wl, ws;
-    std::vector<int64_t> wb;
+    const double kTwoPi = 2.0 * kPi;
+    p->uscale = kappa * (double)TAB_STEPS / kTwoPi;
+    std::vector<double> ux(t.n), uy(t.n), uz(t.n);
+    for (int64_t i = 0; i < t.n; ++i)
+      ux[i] = t.xs[i] * p->uscale, uy[i] = t.ys[i] * p->uscale, uz[i] = t.zs[i] * p->uscale;
+    p->ux = dupload(ux), p->uy = dupload(uy), p->uz = dupload(uz);
+    // Owned target ranges: owned near-level boxes (far field), or the rank's point range of the
+    // root (no far field).  Every target tile (<= kTile points of one box) gets
+    //   DIAG (tile, tile);  SYM (tile, later tile of the same box);
+    //   SYM (tile, owned neighbour box beta > alpha);  ORD (tile, neighbour range owned elsewhere).
+    std::vector<int64_t> it[3];
     int64_t pairs = 0, sym_pairs = 0;
-    for (int64_t b = 0; b < B.nbox(); ++b) {
-      const int64_t nbpts = B.first[b + 1] - B.first[b];
-      for (int dx = -1; dx <= 1; ++dx)
-        for (int dy = -1; dy <= 1; ++dy)
-          for (int dz = -1; dz <= 1; ++dz) {
-            int32_t k = B.find(B.ix[b] + dx, B.iy[b] + dy, B.iz[b] + dz);
-            if (k < 0 || !owned(b)) continue;
-            const int64_t nk = B.first[k + 1] - B.first[k];
-            pairs += nbpts * nk;
-            if (k == b || !owned(k)) {
-              nb.push_back(k);
-            } else if (k > b) {
-              sym_pairs += nbpts * nk;
-              for (int64_t s = B.first[b]; s < B.first[b + 1]; s += kTile)
-                wl.push_back((int32_t)b), wb.push_back(s), ws.push_back(k);
+    auto add = [&](int kind, int64_t t0, int64_t t1, int64_t s0, int64_t s1) {
+      if (t1 <= t0 || s1 <= s0) return;
+      it[kind].insert(it[kind].end(), {t0, t1, s0, s1});
+    };
+    auto own_box = [&](int64_t A0, int64_t A1, const std::vector<std::pair<int64_t, int64_t>> &others_owned,
+                       const std::vector<std::pair<int64_t, int64_t>> &others_foreign) {
+      // targets [A0, A1) of one owned box; others_* = neighbour ranges (sym: only beta > alpha)
+      for (int64_t t0 = A0; t0 < A1; t0 += kTile) {
+        const int64_t t1 = std::min(t0 + kTile, A1);
+        add(P2P_DIAG, t0, t1, t0, t1);
+        for (int64_t u0 = t1; u0 < A1; u0 += kTile) add(P2P_SYM, t0, t1, u0, std::min(u0 + kTile, A1));
+        for (auto &r : others_owned) add(P2P_SYM, t0, t1, r.first, r.second);
+        for (auto &r : others_foreign) add(P2P_ORD, t0, t1, r.first, r.second);
+      }
+    };
+    if (p->L_f >= 2) {
+      const int64_t lo = p->lv[p->L_f].own0, hi = p->lv[p->L_f].own1;
+      for (int64_t b = lo; b < hi; ++b) {
+        std::vector<std::pair<int64_t, int64_t>> ow, fo;
+        const int64_t nb = B.first[b + 1] - B.first[b];
+        for (int dx = -1; dx <= 1; ++dx)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dz = -1; dz <= 1; ++dz) {
+              int32_t k = B.find(B.ix[b] + dx, B.iy[b] + dy, B.iz[b] + dz);
+              if (k < 0) continue;
+              const int64_t nk = B.first[k + 1] - B.first[k];
+              pairs += nb * nk - (k == b ? nb : 0);
+              if (k == b) continue;
+              if (k < lo || k >= hi) {
+                fo.push_back({B.first[k], B.first[k + 1]});
+              } else if (k > b) {
+                ow.push_back({B.first[k], B.first[k + 1]});
+              }
             }
-          }
-      row.push_back((int32_t)nb.size());
+        own_box(B.first[b], B.first[b + 1], ow, fo);
+      }
+    } else {
+      const int64_t A0 = p->own_pt0, A1 = p->own_pt1, n = t.n;
+      std::vector<std::pair<int64_t, int64_t>> fo;
+      if (A0 > 0) fo.push_back({0, A0});
+      if (A1 < n) fo.push_back({A1, n});
+      own_box(A0, A1, {}, fo);
+      pairs = (A1 - A0) * (n - 1);
     }
-    p->nb_row = dupload(row), p->nb_box = dupload(nb);
-    p->first_near = dupload(B.first);
-    p->sym_leaf = dupload(wl), p->sym_begin = dupload(wb), p->sym_src = dupload(ws);
-    p->nsym = (int64_t)wl.size();
+    // longest items first (LPT order against the tail of the grid)
+    for (int k = 0; k < 3; ++k) {
+      const int64_t m = (int64_t)it[k].size() / 4;
+      std::vector<int64_t> ord(m);
+      std::iota(ord.begin(), ord.end(), 0);
+      auto cost = [&](int64_t i) { return (it[k][4 * i + 1] - it[k][4 * i]) * (it[k][4 * i + 3] - it[k][4 * i + 2]); };
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return cost(x) > cost(y); });
+      std::vector<int64_t> sorted(4 * m);
+      for (int64_t i = 0; i < m; ++i)
+        for (int c = 0; c < 4; ++c) sorted[4 * i + c] = it[k][4 * ord[i] + c];
+      if (k == P2P_SYM)
+        for (int64_t i = 0; i < m; ++i) sym_pairs += cost(i);
+      p->p2p_items[k] = dupload(sorted);
+      p->p2p_nitems[k] = m;
+    }
+    // hfmm_direct: every target tile against all points (self pair masked)
+    {
+      std::vector<int64_t> d;
+      for (int64_t t0 = 0; t0 < t.n; t0 += kTile) d.insert(d.end(), {t0, std::min(t0 + kTile, t.n), 0, t.n});
+      p->dir_items = dupload(d);
+      p->dir_nitems = (int64_t)d.size() / 4;
+    }
+    // L2T tiles: kTile targets of one owned far-field leaf
     std::vector<int32_t> tl;
     std::vector<int64_t> tb;
-    for (int64_t b = lo; b < hi; ++b)
-      for (int64_t s = B.first[b]; s < B.first[b + 1]; s += kTile) {
-        if (p->L_f < 0 && (s < p->own_pt0 || s >= p->own_pt1)) continue;
-        tl.push_back((int32_t)b), tb.push_back(s);
-      }
+    if (p->L_f >= 2)
+      for (int64_t b = p->lv[p->L_f].own0; b < p->lv[p->L_f].own1; ++b)
+        for (int64_t s0 = B.first[b]; s0 < B.first[b + 1]; s0 += kTile) tl.push_back((int32_t)b), tb.push_back(s0);
+    p->first_near = dupload(B.first);
     p->tile_leaf = dupload(tl), p->tile_begin = dupload(tb);
     p->ntiles = (int64_t)tl.size();
     p->info.p2p_pairs = pairs;
     p->info.p2p_sym_pairs = sym_pairs;
     p->p2p_sym_pairs = sym_pairs;
     for (int d = 0; d < 3; ++d) {
-      p->dummy_t[d] = t.lo[d] - 3.0 * t.size;
-      p->dummy_s[d] = t.lo[d] + 4.0 * t.size;
+      p->dummy_t[d] = (t.lo[d] - 3.0 * t.size) * p->uscale;
+      p->dummy_s[d] = (t.lo[d] + 4.0 * t.size) * p->uscale;
     }
   }
   if (p->L_f >= 2) p->y_far = dalloc<double2>(t.n);
@@ -671,10 +709,12 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
   CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
   if (prof) cudaEventRecord(p->sev[7], p->stream2);
   CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), p->stream2));
-  launch_p2p(pts, p->first_near, p->nb_row, p->nb_box, 0, 0, p->tile_leaf, p->tile_begin, p->ntiles,
-             p->kappa, p->y_near, p->stream2);
-  launch_p2p_sym(pts, p->first_near, p->sym_leaf, p->sym_begin, p->sym_src, p->nsym, p->kappa, p->dummy_t,
-                 p->dummy_s, p->y_near, p->stream2);
+  {
+    PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
+    for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD})
+      launch_p2p_items(pu, p->p2p_items[k], p->p2p_nitems[k], k, p->uscale, p->dummy_t, p->dummy_s, p->y_near,
+                       p->stream2);
+  }
   if (prof) cudaEventRecord(p->sev[8], p->stream2);
   CK(cudaEventRecord(p->ev_join, p->stream2));
   const TwiddleSet &tw = global_twiddles(p->device);
@@ -760,10 +800,9 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
   if (p->nranks > 1 || local) CK(cudaMemsetAsync(p->y_out, 0, n * sizeof(double2), s));
   if (direct) {
     launch_permute_q(qd, p->perm, p->q_sorted, n, s);
-    PointsDev pts{p->px, p->py, p->pz, p->q_sorted};
+    PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
     CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), s));
-    launch_p2p(pts, p->dir_first, p->dir_nb_row, p->dir_nb_box, 0, 0, p->dir_tile_leaf, p->dir_tile_begin,
-               p->dir_ntiles, p->kappa > 0 ? p->kappa : 0.0, p->y_near, s);
+    launch_p2p_items(pu, p->dir_items, p->dir_nitems, P2P_DIAG, p->uscale, p->dummy_t, p->dummy_s, p->y_near, s);
     launch_combine(p->y_near, nullptr, p->perm, p->y_out, n, 0, n, s);
   } else {
     int rc = run_matvec(p, qd, s);
@@ -800,8 +839,8 @@ extern "C" int hfmm_matvec(hfmm_plan *p, const double *q, double *y, int mem, vo
 }
 
 extern "C" int hfmm_direct(hfmm_plan *p, const double *q, double *y, int mem, void *stream) {
-  if (p && p->kappa <= 0) {
-    p->err = "hfmm_direct: call precompute first (kappa)";
+  if (p && !p->have_plan) {
+    p->err = "hfmm_direct: call precompute first (kappa, scaled positions)";
     return HFMM_E_STATE;
   }
   return matvec_common(p, q, y, mem, stream, true);

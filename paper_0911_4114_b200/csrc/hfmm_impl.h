@@ -87,25 +87,30 @@ struct PointsDev {
   const double2 *q;         // sorted charges
 };
 
-// P2P over target leaves [leaf0, leaf1): targets of leaf b are points [first[b], first[b+1]);
-// sources are the point ranges of its neighbour list nb_row/nb_box (box ids of the same level).
-void launch_p2p(PointsDev pts, const int64_t *first, const int32_t *nb_row, const int32_t *nb_box,
-                int32_t leaf0, int32_t leaf1, const int32_t *tile_leaf, const int64_t *tile_begin,
-                int64_t ntiles, double kappa, double2 *y_near, cudaStream_t s);
+// Positions pre-scaled to table steps (u = x kappa TAB / 2 pi) and sorted charges, for P2P.
+struct PointsU {
+  const double *ux, *uy, *uz;
+  const double2 *q;
+};
+#ifndef HFMM_P2P_MINB
+#define HFMM_P2P_MINB 4  // resident CTAs per SM requested from ptxas (register budget)
+#endif
+constexpr int TAB_STEPS = 1024;  // e^{i h k} table size; h = 2 pi / TAB_STEPS
+enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2 };
+// P2P work items, int64 [nitems][4] = (t0, t1, s0, s1): targets [t0, t1) (<= 256), sources
+// [s0, s1).  P2P_SYM: disjoint ranges, rows and columns (each unordered pair once);
+// P2P_DIAG: rows only, self pair masked (sources contain the targets); P2P_ORD: rows only.
+// Adds scale * sum into y_near (zeroed beforehand); scale = kappa TAB / (2 pi) (see kernel).
+// dummy_t / dummy_s (scaled units): far positions used to pad partial symmetric tiles.
+void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
+                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s);
 
-// Symmetric P2P over unordered leaf pairs: work item w = (256-target tile of leaf w_leaf[w]
-// starting at w_begin[w], source leaf w_src[w] != w_leaf[w]); adds row and column sums into
-// y_near (zeroed beforehand).  dummy_t / dummy_s: far positions used to pad partial tiles.
-void launch_p2p_sym(PointsDev pts, const int64_t *first, const int32_t *w_leaf, const int64_t *w_begin,
-                    const int32_t *w_src, int64_t nwork, double kappa, const double dummy_t[3],
-                    const double dummy_s[3], double2 *y_near, cudaStream_t s);
-
-// S2M: M[b][k] = sum_j q_j e^{i kappa s_k.(x_j - c_b)}
+// S2M: M[b][k] = sum_j q_j e^{i kappa s_k.(x_j - c_b)}; ks = kappa s / h (table steps)
 void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
                 const double *cz, int32_t box0, int32_t box1, const double *ks /*[3][K]*/,
                 int64_t K, double2 *M, cudaStream_t s);
 
-// L2T: y_far[i] = w sum_k L[b][k] e^{i kappa s_k.(c_b - x_i)}
+// L2T: y_far[i] = w sum_k L[b][k] e^{i kappa s_k.(c_b - x_i)}; ks as for S2M
 void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
                 const double *cz, const int32_t *tile_leaf, const int64_t *tile_begin,
                 int64_t ntiles, const double *ks, int64_t K, const double2 *L, double w,

@@ -4,11 +4,13 @@
 //   L2T  field computation int L e^{i kappa s.(c_a - x_i)} dS
 //   permute / combine (Morton order <-> caller order)
 // The three main kernels are bound by the FP64 pipe: one complex exponential per pair or per
-// (point, direction).  e^{ix} (cexpi below): round x to the nearest multiple of 2 pi/1024 with
-// the 1.5 * 2^52 "magic number" (no FRND/F2I), 2-part Cody-Waite remainder |r| <= pi/1024,
-// table e^{2 pi i k/1024} in shared memory, Taylor polynomials of degree 5 (sin) and 4 (cos)
-// whose truncation error (< 2e-18) is below the double rounding of the result.  14 FP64
-// instructions.  Each thread evaluates two items per source (ILP and source-load reuse).
+// (point, direction).  Every phase arrives in units of the table step h = 2 pi/1024 (positions
+// pre-scaled by kappa/h for P2P, directions kappa s/h for S2M/L2T, both at precompute), so e^{ix}
+// (cexpi_u below) needs no range-reduction multiply: round to the nearest step with the
+// 1.5 * 2^52 "magic number" (no FRND/F2I), exact remainder |r| <= 1/2 step, table
+// e^{2 pi i k/1024} in shared memory, Taylor polynomials of degree 5 (sin) and 4 (cos) whose
+// truncation error (< 2e-18) is below the double rounding of the result: 13 FP64 instructions.
+// Each thread evaluates two items per source (ILP and source-load reuse).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
@@ -17,21 +19,13 @@
 
 namespace hfmm {
 
-constexpr int TAB = 1024;
-constexpr double kInvStep = 162.97466172610082;       // 1024 / (2 pi)
+constexpr int TAB = TAB_STEPS;
 constexpr double kMagic = 6755399441055744.0;          // 1.5 * 2^52
-constexpr double kS3 = -1.0 / 6.0, kS5 = 1.0 / 120.0;
-constexpr double kC2 = -0.5, kC4 = 1.0 / 24.0;
-
-static void step_split(double *hi, double *lo) {
-  const double step = 6.283185307179586476925286766559 / TAB;
-  *hi = (double)(float)step;  // 24 significant bits: k * hi exact for |k| < 2^29
-  *lo = step - *hi;
-}
-
-struct ExpConsts {
-  double shi, slo;
-};
+// Taylor coefficients in table-step units h = 2 pi / TAB:  sin(h r) = r (S1 + r^2 (S3 + r^2 S5)),
+// cos(h r) = 1 + r^2 (C2 + r^2 C4), |r| <= 1/2 (|h r| <= pi/1024, truncation < 2e-18).
+constexpr double kH = 6.283185307179586476925286766559 / TAB;
+constexpr double kS1 = kH, kS3 = -kH * kH * kH / 6.0, kS5 = kH * kH * kH * kH * kH / 120.0;
+constexpr double kC2 = -kH * kH / 2.0, kC4 = kH * kH * kH * kH / 24.0;
 
 __device__ __forceinline__ void fill_exp_table(double2 *tab) {
   for (int t = threadIdx.x; t < TAB; t += blockDim.x) {
@@ -41,14 +35,15 @@ __device__ __forceinline__ void fill_exp_table(double2 *tab) {
   }
 }
 
-__device__ __forceinline__ double2 cexpi(double x, const double2 *__restrict__ tab, const ExpConsts &ec) {
-  const double t = fma(x, kInvStep, kMagic);
+// e^{i h u} for a phase u given in table steps (h = 2 pi / TAB): u is rounded to the nearest
+// integer k with the 1.5 * 2^52 magic number (exact for |u| < 2^51), the remainder r = u - k is
+// exact (Sterbenz), and e^{i h u} = e^{2 pi i k / TAB} * e^{i h r}.  13 FP64 instructions.
+__device__ __forceinline__ double2 cexpi_u(double u, const double2 *__restrict__ tab) {
+  const double t = u + kMagic;
   const int k = __double2loint(t);
-  const double kd = t - kMagic;
-  double r = fma(-kd, ec.shi, x);
-  r = fma(-kd, ec.slo, r);
+  const double r = u - (t - kMagic);
   const double r2 = r * r;
-  const double s = fma(r * r2, fma(r2, kS5, kS3), r);
+  const double s = r * fma(r2, fma(r2, kS5, kS3), kS1);
   const double c = fma(r2, fma(r2, kC4, kC2), 1.0);
   const double2 e = tab[k & (TAB - 1)];
   return make_double2(fma(e.x, c, -e.y * s), fma(e.x, s, e.y * c));
@@ -63,139 +58,119 @@ __device__ __forceinline__ double rsqrt_fast(double r2) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// P2P: tile = up to 256 targets of one leaf (2 per thread); sources of every neighbour box
+// P2P.  Positions are stored pre-scaled to table steps, u = x * S with
+// S = kappa TAB / (2 pi), so that kappa R = h |u_i - u_j| and
+//     G = e^{i kappa R} / R = S * e^{i h R_u} / R_u,      R_u = |u_i - u_j|;
+// the kernels accumulate e^{i h R_u} / R_u and multiply by S once per target (per item).
+// Work items are (t0, t1, s0, s1): targets [t0, t1) (<= 256, 2 per thread), sources [s0, s1)
 // streamed through shared memory in chunks of 128.
+//   ordered   rows only; DIAG masks the self pair (R = 0 <=> i = j: coincident distinct
+//             points are rejected at build_tree) when the source range contains the targets
+//   symmetric disjoint ranges: each unordered pair evaluated once, G q_j added to y_i (rows, in
+//             registers) and G q_i to y_j (columns: systolic warp reduction, below)
 // ---------------------------------------------------------------------------------------------
 constexpr int P2P_TPB = 128;
 
-template <bool DIAG>
-__device__ __forceinline__ void p2p_chunk(int cnt, const double *sx, const double *sy, const double *sz,
-                                          const double2 *sq, double x0, double y0, double z0, double x1,
-                                          double y1, double z1, double kappa, const double2 *tab,
-                                          const ExpConsts &ec, double &a0r, double &a0i, double &a1r,
-                                          double &a1i) {
-#pragma unroll 2
-  for (int u = 0; u < cnt; ++u) {
-    const double xs = sx[u], ys = sy[u], zs = sz[u];
-    const double2 q = sq[u];
-    {
-      const double dx = x0 - xs, dy = y0 - ys, dz = z0 - zs;
-      const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-      double ri = rsqrt_fast(r2);
-      if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;  // self pair excluded
-      const double2 e = cexpi(kappa * (r2 * ri), tab, ec);
-      const double gr = e.x * ri, gi = e.y * ri;
-      a0r = fma(gr, q.x, fma(-gi, q.y, a0r));
-      a0i = fma(gr, q.y, fma(gi, q.x, a0i));
-    }
-    {
-      const double dx = x1 - xs, dy = y1 - ys, dz = z1 - zs;
-      const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-      double ri = rsqrt_fast(r2);
-      if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;
-      const double2 e = cexpi(kappa * (r2 * ri), tab, ec);
-      const double gr = e.x * ri, gi = e.y * ri;
-      a1r = fma(gr, q.x, fma(-gi, q.y, a1r));
-      a1i = fma(gr, q.y, fma(gi, q.x, a1i));
-    }
-  }
+__device__ __forceinline__ double2 green_u(double tx, double ty, double tz, double xs, double ys, double zs,
+                                           const double2 *tab) {
+  const double dx = tx - xs, dy = ty - ys, dz = tz - zs;
+  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  const double ri = rsqrt_fast(r2);
+  const double2 e = cexpi_u(r2 * ri, tab);
+  return make_double2(e.x * ri, e.y * ri);
 }
 
-__global__ void __launch_bounds__(P2P_TPB, 5) p2p_kernel(PointsDev pts, const int64_t *__restrict__ first,
-                                                         const int32_t *__restrict__ nb_row,
-                                                         const int32_t *__restrict__ nb_box,
-                                                         const int32_t *__restrict__ tile_leaf,
-                                                         const int64_t *__restrict__ tile_begin,
-                                                         double kappa, ExpConsts ec,
-                                                         double2 *__restrict__ y_near) {
+template <bool DIAG>
+__global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU pts,
+                                                                        const int64_t *__restrict__ items,
+                                                                        double scale, double2 *__restrict__ y_near) {
   __shared__ double2 tab[TAB];
   __shared__ double sx[P2P_TPB], sy[P2P_TPB], sz[P2P_TPB];
   __shared__ double2 sq[P2P_TPB];
   fill_exp_table(tab);
-  const int32_t leaf = tile_leaf[blockIdx.x];
-  const int64_t tend = first[leaf + 1];
-  const int64_t i0 = tile_begin[blockIdx.x] + threadIdx.x, i1 = i0 + P2P_TPB;
+  const int64_t *it = items + 4 * (int64_t)blockIdx.x;
+  const int64_t t1 = it[1], s0 = it[2], s1 = it[3];
+  const int64_t i0 = it[0] + threadIdx.x, i1 = i0 + P2P_TPB;
   // inactive lanes evaluate far-away dummy targets (results discarded)
-  const double x0 = i0 < tend ? pts.x[i0] : 1e30, y0 = i0 < tend ? pts.y[i0] : 0.0, z0 = i0 < tend ? pts.z[i0] : 0.0;
-  const double x1 = i1 < tend ? pts.x[i1] : 1e30, y1 = i1 < tend ? pts.y[i1] : 0.0, z1 = i1 < tend ? pts.z[i1] : 0.0;
+  const double x0 = i0 < t1 ? pts.ux[i0] : 1e30, y0 = i0 < t1 ? pts.uy[i0] : 0.0, z0 = i0 < t1 ? pts.uz[i0] : 0.0;
+  const double x1 = i1 < t1 ? pts.ux[i1] : 1e30, y1 = i1 < t1 ? pts.uy[i1] : 0.0, z1 = i1 < t1 ? pts.uz[i1] : 0.0;
   double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
-  for (int32_t e = nb_row[leaf]; e < nb_row[leaf + 1]; ++e) {
-    const int32_t b = nb_box[e];
-    const int64_t s0 = first[b], s1 = first[b + 1];
-    for (int64_t c0 = s0; c0 < s1; c0 += P2P_TPB) {
-      const int cnt = (int)min((int64_t)P2P_TPB, s1 - c0);
-      __syncthreads();
-      if (threadIdx.x < cnt) {
-        const int64_t j = c0 + threadIdx.x;
-        sx[threadIdx.x] = pts.x[j];
-        sy[threadIdx.x] = pts.y[j];
-        sz[threadIdx.x] = pts.z[j];
-        sq[threadIdx.x] = pts.q[j];
+  for (int64_t c0 = s0; c0 < s1; c0 += P2P_TPB) {
+    const int cnt = (int)min((int64_t)P2P_TPB, s1 - c0);
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const int64_t j = c0 + threadIdx.x;
+      sx[threadIdx.x] = pts.ux[j];
+      sy[threadIdx.x] = pts.uy[j];
+      sz[threadIdx.x] = pts.uz[j];
+      sq[threadIdx.x] = pts.q[j];
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int u = 0; u < cnt; ++u) {
+      const double xs = sx[u], ys = sy[u], zs = sz[u];
+      const double2 q = sq[u];
+      {
+        const double dx = x0 - xs, dy = y0 - ys, dz = z0 - zs;
+        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+        double ri = rsqrt_fast(r2);
+        if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;  // self pair excluded
+        const double2 e = cexpi_u(r2 * ri, tab);
+        const double gr = e.x * ri, gi = e.y * ri;
+        a0r = fma(gr, q.x, fma(-gi, q.y, a0r));
+        a0i = fma(gr, q.y, fma(gi, q.x, a0i));
       }
-      __syncthreads();
-      if (b == leaf)
-        p2p_chunk<true>(cnt, sx, sy, sz, sq, x0, y0, z0, x1, y1, z1, kappa, tab, ec, a0r, a0i, a1r, a1i);
-      else
-        p2p_chunk<false>(cnt, sx, sy, sz, sq, x0, y0, z0, x1, y1, z1, kappa, tab, ec, a0r, a0i, a1r, a1i);
+      {
+        const double dx = x1 - xs, dy = y1 - ys, dz = z1 - zs;
+        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+        double ri = rsqrt_fast(r2);
+        if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;
+        const double2 e = cexpi_u(r2 * ri, tab);
+        const double gr = e.x * ri, gi = e.y * ri;
+        a1r = fma(gr, q.x, fma(-gi, q.y, a1r));
+        a1i = fma(gr, q.y, fma(gi, q.x, a1i));
+      }
     }
   }
-  // y_near is zeroed before the P2P launches; the symmetric kernel adds into the same rows
-  if (i0 < tend) atomicAdd(&y_near[i0].x, a0r), atomicAdd(&y_near[i0].y, a0i);
-  if (i1 < tend) atomicAdd(&y_near[i1].x, a1r), atomicAdd(&y_near[i1].y, a1i);
+  // y_near is zeroed before the P2P launches; every item adds into its target rows
+  if (i0 < t1) atomicAdd(&y_near[i0].x, scale * a0r), atomicAdd(&y_near[i0].y, scale * a0i);
+  if (i1 < t1) atomicAdd(&y_near[i1].x, scale * a1r), atomicAdd(&y_near[i1].y, scale * a1i);
 }
 
-// ---------------------------------------------------------------------------------------------
-// Symmetric P2P over an unordered leaf pair (alpha, beta), alpha != beta: the kernel
-// G(x_i, x_j) = e^{i kappa |x_i - x_j|} / |x_i - x_j| is symmetric, so each unordered pair is
-// evaluated once and contributes G q_j to y_i (row sums, registers) and G q_i to y_j (column
-// sums).  Column sums use a systolic warp reduction: in a block of 32 sources, lane t processes
-// source (t + u) mod 32 at step u and passes the running column accumulator to lane t - 1, so
-// after 32 steps lane t holds the full warp sum of source t (2 shuffles per step instead of a
-// 5-level butterfly per source).  Work item = (256-target tile of alpha, beta).
-// ---------------------------------------------------------------------------------------------
-constexpr int SYM_TPB = 128;
-
-__device__ __forceinline__ double2 green(double tx, double ty, double tz, double xs, double ys, double zs,
-                                         double kappa, const double2 *tab, const ExpConsts &ec) {
-  const double dx = tx - xs, dy = ty - ys, dz = tz - zs;
-  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-  const double ri = rsqrt_fast(r2);
-  const double2 e = cexpi(kappa * (r2 * ri), tab, ec);
-  return make_double2(e.x * ri, e.y * ri);
-}
-
-__global__ void __launch_bounds__(SYM_TPB, 4) p2p_sym_kernel(PointsDev pts, const int64_t *__restrict__ first,
-                                                             const int32_t *__restrict__ w_leaf,
-                                                             const int64_t *__restrict__ w_begin,
-                                                             const int32_t *__restrict__ w_src, double kappa,
-                                                             ExpConsts ec, double3 dummy_t, double3 dummy_s,
-                                                             double2 *__restrict__ y_near) {
+// Symmetric item: column sums use a systolic warp reduction -- in a block of 32 sources, lane t
+// processes source (t + u) mod 32 at step u and passes the running column accumulator to lane
+// t - 1, so after 32 steps lane t holds the warp sum of source t (2 shuffles per step instead of
+// a 5-level butterfly per source); the 4 warps combine in shared memory, one atomic per source.
+__global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU pts,
+                                                                        const int64_t *__restrict__ items,
+                                                                        double scale, double3 dummy_t,
+                                                                        double3 dummy_s,
+                                                                        double2 *__restrict__ y_near) {
   __shared__ double2 tab[TAB];
-  __shared__ double sx[SYM_TPB], sy[SYM_TPB], sz[SYM_TPB];
-  __shared__ double2 sq[SYM_TPB];
-  __shared__ double2 col[SYM_TPB / 32][SYM_TPB];
+  __shared__ double sx[P2P_TPB], sy[P2P_TPB], sz[P2P_TPB];
+  __shared__ double2 sq[P2P_TPB];
+  __shared__ double2 col[P2P_TPB / 32][P2P_TPB];
   fill_exp_table(tab);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t leaf = w_leaf[blockIdx.x], src = w_src[blockIdx.x];
-  const int64_t tend = first[leaf + 1];
-  const int64_t i0 = w_begin[blockIdx.x] + threadIdx.x, i1 = i0 + SYM_TPB;
-  const bool v0 = i0 < tend, v1 = i1 < tend;
+  const int64_t *it = items + 4 * (int64_t)blockIdx.x;
+  const int64_t t1 = it[1], s0 = it[2], s1 = it[3];
+  const int64_t i0 = it[0] + threadIdx.x, i1 = i0 + P2P_TPB;
+  const bool v0 = i0 < t1, v1 = i1 < t1;
   // inactive targets: far dummy position, zero charge (their column contributions vanish)
-  const double x0 = v0 ? pts.x[i0] : dummy_t.x, y0 = v0 ? pts.y[i0] : dummy_t.y, z0 = v0 ? pts.z[i0] : dummy_t.z;
-  const double x1 = v1 ? pts.x[i1] : dummy_t.x, y1 = v1 ? pts.y[i1] : dummy_t.y, z1 = v1 ? pts.z[i1] : dummy_t.z;
+  const double x0 = v0 ? pts.ux[i0] : dummy_t.x, y0 = v0 ? pts.uy[i0] : dummy_t.y, z0 = v0 ? pts.uz[i0] : dummy_t.z;
+  const double x1 = v1 ? pts.ux[i1] : dummy_t.x, y1 = v1 ? pts.uy[i1] : dummy_t.y, z1 = v1 ? pts.uz[i1] : dummy_t.z;
   const double2 q0 = v0 ? pts.q[i0] : make_double2(0.0, 0.0), q1 = v1 ? pts.q[i1] : make_double2(0.0, 0.0);
   double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
-  const int64_t s0 = first[src], s1 = first[src + 1];
-  for (int64_t c0 = s0; c0 < s1; c0 += SYM_TPB) {
-    const int cnt = (int)min((int64_t)SYM_TPB, s1 - c0);
+  for (int64_t c0 = s0; c0 < s1; c0 += P2P_TPB) {
+    const int cnt = (int)min((int64_t)P2P_TPB, s1 - c0);
     __syncthreads();
     {
       const int t = threadIdx.x;
       const bool v = t < cnt;
       const int64_t j = c0 + t;
-      sx[t] = v ? pts.x[j] : dummy_s.x;   // padded sources: far dummy, zero charge
-      sy[t] = v ? pts.y[j] : dummy_s.y;
-      sz[t] = v ? pts.z[j] : dummy_s.z;
+      sx[t] = v ? pts.ux[j] : dummy_s.x;   // padded sources: far dummy, zero charge
+      sy[t] = v ? pts.uy[j] : dummy_s.y;
+      sz[t] = v ? pts.uz[j] : dummy_s.z;
       sq[t] = v ? pts.q[j] : make_double2(0.0, 0.0);
     }
     __syncthreads();
@@ -208,8 +183,8 @@ __global__ void __launch_bounds__(SYM_TPB, 4) p2p_sym_kernel(PointsDev pts, cons
         const int s = base + ((lane + u) & 31);
         const double xs = sx[s], ys = sy[s], zs = sz[s];
         const double2 qs = sq[s];
-        const double2 g0 = green(x0, y0, z0, xs, ys, zs, kappa, tab, ec);
-        const double2 g1 = green(x1, y1, z1, xs, ys, zs, kappa, tab, ec);
+        const double2 g0 = green_u(x0, y0, z0, xs, ys, zs, tab);
+        const double2 g1 = green_u(x1, y1, z1, xs, ys, zs, tab);
         a0r = fma(g0.x, qs.x, fma(-g0.y, qs.y, a0r));
         a0i = fma(g0.x, qs.y, fma(g0.y, qs.x, a0i));
         a1r = fma(g1.x, qs.x, fma(-g1.y, qs.y, a1r));
@@ -227,34 +202,26 @@ __global__ void __launch_bounds__(SYM_TPB, 4) p2p_sym_kernel(PointsDev pts, cons
     if (threadIdx.x < cnt) {
       double2 sum = col[0][threadIdx.x];
 #pragma unroll
-      for (int w = 1; w < SYM_TPB / 32; ++w) sum.x += col[w][threadIdx.x].x, sum.y += col[w][threadIdx.x].y;
-      atomicAdd(&y_near[c0 + threadIdx.x].x, sum.x);
-      atomicAdd(&y_near[c0 + threadIdx.x].y, sum.y);
+      for (int w = 1; w < P2P_TPB / 32; ++w) sum.x += col[w][threadIdx.x].x, sum.y += col[w][threadIdx.x].y;
+      atomicAdd(&y_near[c0 + threadIdx.x].x, scale * sum.x);
+      atomicAdd(&y_near[c0 + threadIdx.x].y, scale * sum.y);
     }
   }
-  if (v0) atomicAdd(&y_near[i0].x, a0r), atomicAdd(&y_near[i0].y, a0i);
-  if (v1) atomicAdd(&y_near[i1].x, a1r), atomicAdd(&y_near[i1].y, a1i);
+  if (v0) atomicAdd(&y_near[i0].x, scale * a0r), atomicAdd(&y_near[i0].y, scale * a0i);
+  if (v1) atomicAdd(&y_near[i1].x, scale * a1r), atomicAdd(&y_near[i1].y, scale * a1i);
 }
 
-void launch_p2p_sym(PointsDev pts, const int64_t *first, const int32_t *w_leaf, const int64_t *w_begin,
-                    const int32_t *w_src, int64_t nwork, double kappa, const double dummy_t[3],
-                    const double dummy_s[3], double2 *y_near, cudaStream_t s) {
-  if (nwork <= 0) return;
-  ExpConsts ec;
-  step_split(&ec.shi, &ec.slo);
-  p2p_sym_kernel<<<(unsigned)nwork, SYM_TPB, 0, s>>>(pts, first, w_leaf, w_begin, w_src, kappa, ec,
-                                                      make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
-                                                      make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near);
-}
-
-void launch_p2p(PointsDev pts, const int64_t *first, const int32_t *nb_row, const int32_t *nb_box,
-                int32_t, int32_t, const int32_t *tile_leaf, const int64_t *tile_begin,
-                int64_t ntiles, double kappa, double2 *y_near, cudaStream_t s) {
-  if (ntiles <= 0) return;
-  ExpConsts ec;
-  step_split(&ec.shi, &ec.slo);
-  p2p_kernel<<<(unsigned)ntiles, P2P_TPB, 0, s>>>(pts, first, nb_row, nb_box, tile_leaf, tile_begin, kappa, ec,
-                                                   y_near);
+void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
+                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s) {
+  if (nitems <= 0) return;
+  if (kind == P2P_SYM)
+    p2p_sym_kernel<<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale,
+                                                        make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
+                                                        make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near);
+  else if (kind == P2P_DIAG)
+    p2p_ord_kernel<true><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
+  else
+    p2p_ord_kernel<false><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -267,7 +234,7 @@ __global__ void __launch_bounds__(S2M_TPB, 5) s2m_kernel(PointsDev pts, const in
                                                          const double *__restrict__ cy,
                                                          const double *__restrict__ cz, int32_t box0,
                                                          const double *__restrict__ ks, int64_t K,
-                                                         ExpConsts ec, double2 *__restrict__ M) {
+                                                         double2 *__restrict__ M) {
   __shared__ double2 tab[TAB];
   __shared__ double sx[S2M_TPB], sy[S2M_TPB], sz[S2M_TPB];
   __shared__ double2 sq[S2M_TPB];
@@ -294,10 +261,10 @@ __global__ void __launch_bounds__(S2M_TPB, 5) s2m_kernel(PointsDev pts, const in
     for (int u = 0; u < cnt; ++u) {
       const double dx = sx[u], dy = sy[u], dz = sz[u];
       const double2 q = sq[u];
-      const double2 e0 = cexpi(fma(kx0, dx, fma(ky0, dy, kz0 * dz)), tab, ec);
+      const double2 e0 = cexpi_u(fma(kx0, dx, fma(ky0, dy, kz0 * dz)), tab);
       a0r = fma(e0.x, q.x, fma(-e0.y, q.y, a0r));
       a0i = fma(e0.x, q.y, fma(e0.y, q.x, a0i));
-      const double2 e1 = cexpi(fma(kx1, dx, fma(ky1, dy, kz1 * dz)), tab, ec);
+      const double2 e1 = cexpi_u(fma(kx1, dx, fma(ky1, dy, kz1 * dz)), tab);
       a1r = fma(e1.x, q.x, fma(-e1.y, q.y, a1r));
       a1i = fma(e1.x, q.y, fma(e1.y, q.x, a1i));
     }
@@ -310,10 +277,8 @@ void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const dou
                 const double *cz, int32_t box0, int32_t box1, const double *ks, int64_t K,
                 double2 *M, cudaStream_t s) {
   if (box1 <= box0) return;
-  ExpConsts ec;
-  step_split(&ec.shi, &ec.slo);
   dim3 grid((unsigned)(box1 - box0), (unsigned)((K + 2 * S2M_TPB - 1) / (2 * S2M_TPB)));
-  s2m_kernel<<<grid, S2M_TPB, 0, s>>>(pts, first, cx, cy, cz, box0, ks, K, ec, M);
+  s2m_kernel<<<grid, S2M_TPB, 0, s>>>(pts, first, cx, cy, cz, box0, ks, K, M);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -329,7 +294,7 @@ __global__ void __launch_bounds__(L2T_TPB, 5) l2t_kernel(PointsDev pts, const in
                                                          const int64_t *__restrict__ tile_begin,
                                                          const double *__restrict__ ks, int64_t K,
                                                          const double2 *__restrict__ L, double w,
-                                                         ExpConsts ec, double2 *__restrict__ y_far) {
+                                                         double2 *__restrict__ y_far) {
   __shared__ double2 tab[TAB];
   __shared__ double skx[L2T_TPB], sky[L2T_TPB], skz[L2T_TPB];
   __shared__ double2 sl[L2T_TPB];
@@ -359,10 +324,10 @@ __global__ void __launch_bounds__(L2T_TPB, 5) l2t_kernel(PointsDev pts, const in
     for (int u = 0; u < cnt; ++u) {
       const double kx = skx[u], ky = sky[u], kz = skz[u];
       const double2 l = sl[u];
-      const double2 e0 = cexpi(fma(kx, dx0, fma(ky, dy0, kz * dz0)), tab, ec);
+      const double2 e0 = cexpi_u(fma(kx, dx0, fma(ky, dy0, kz * dz0)), tab);
       a0r = fma(e0.x, l.x, fma(-e0.y, l.y, a0r));
       a0i = fma(e0.x, l.y, fma(e0.y, l.x, a0i));
-      const double2 e1 = cexpi(fma(kx, dx1, fma(ky, dy1, kz * dz1)), tab, ec);
+      const double2 e1 = cexpi_u(fma(kx, dx1, fma(ky, dy1, kz * dz1)), tab);
       a1r = fma(e1.x, l.x, fma(-e1.y, l.y, a1r));
       a1i = fma(e1.x, l.y, fma(e1.y, l.x, a1i));
     }
@@ -376,9 +341,7 @@ void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const dou
                 int64_t ntiles, const double *ks, int64_t K, const double2 *L, double w,
                 double2 *y_far, cudaStream_t s) {
   if (ntiles <= 0) return;
-  ExpConsts ec;
-  step_split(&ec.shi, &ec.slo);
-  l2t_kernel<<<(unsigned)ntiles, L2T_TPB, 0, s>>>(pts, first, cx, cy, cz, tile_leaf, tile_begin, ks, K, L, w, ec,
+  l2t_kernel<<<(unsigned)ntiles, L2T_TPB, 0, s>>>(pts, first, cx, cy, cz, tile_leaf, tile_begin, ks, K, L, w,
                                                    y_far);
 }
 
