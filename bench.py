@@ -111,11 +111,13 @@ def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
     directions, pairs, children, interaction-list entries).  Returns (seconds per matvec,
     description, cores)."""
     from threadpoolctl import threadpool_limits
-    from oracle.plan import make_plan
+    from oracle.plan import make_plan, choose_source_level, set_source_level
     from oracle.fmm import OracleFMM
     from oracle.tree import interaction_list, neighbours
     with threadpool_limits(1):
         plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+        if plan.L_f is not None:   # the same source level as the library's default policy (R-14)
+            set_source_level(plan, choose_source_level(x, cfg.lo, cfg.size, cfg.depth, plan.L_f))
         f = OracleFMM(x, cfg.lo, cfg.size, plan)
         rng = np.random.default_rng(seed)
         total = 0.0
@@ -127,13 +129,16 @@ def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
             dt = time.perf_counter() - t0
             total = dt * len(x) / len(t)
             return total, f"direct sum for {len(t)} sampled targets, x{len(x) / len(t):.0f}", 1
-        L = plan.L_f
+        L, S = plan.L_f, plan.source_level
         lev = f.levels[L]
         leaves = rng.choice(len(lev.boxes), size=min(budget_leaves, len(lev.boxes)), replace=False)
         pts = np.concatenate([lev.members[b] for b in leaves])
-        # S2M
+        # S2M on the source-level boxes inside the sampled far-field leaves
+        levS = f.levels[S]
+        sbox = sorted({levS.index[tuple(c)] for c in np.minimum(np.floor((x[pts] - np.asarray(cfg.lo)) / levS.a)
+                                                               .astype(np.int64), 2 ** S - 1).tolist()})
         t0 = time.perf_counter()
-        f.s2m(q, boxes=list(leaves))
+        f.s2m(q, boxes=sbox)
         ts2m = (time.perf_counter() - t0) * len(x) / len(pts)
         # P2P (pairs-weighted)
         pairs_s = sum(len(lev.members[b]) * sum(len(lev.members[c]) for c in neighbours(lev, lev.boxes[b]))
@@ -144,36 +149,39 @@ def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
         f.p2p(q, pts)
         tp2p = (time.perf_counter() - t0) * pairs_all / pairs_s
         # L2T with a random local field
-        Kf = plan.levels[L].K
-        Lf = {b: rng.standard_normal(Kf) + 1j * rng.standard_normal(Kf) for b in leaves}
+        Kf = plan.levels[S].K
+        Lf = {b: rng.standard_normal(Kf) + 1j * rng.standard_normal(Kf) for b in sbox}
         t0 = time.perf_counter()
         f.l2t(Lf, pts)
         tl2t = (time.perf_counter() - t0) * len(x) / len(pts)
         # M2M / M2L / L2L per level with random fields
         tmid = 0.0
-        for l in range(2, L + 1):
+        for l in range(2, S + 1):
             K = plan.levels[l].K
             levl = f.levels[l]
-            M = {b: rng.standard_normal(K) + 1j * rng.standard_normal(K) for b in range(len(levl.boxes))}
-            tg = list(range(min(2, len(levl.boxes))))
-            nnz_s = sum(len(interaction_list(levl, levl.boxes[a])) for a in tg)
-            nnz = sum(len(interaction_list(levl, levl.boxes[a])) for a in range(len(levl.boxes)))
-            t0 = time.perf_counter()
-            f.m2l(M, l, targets=tg)
-            tmid += (time.perf_counter() - t0) * nnz / max(nnz_s, 1)
-            if l > 2:
-                sub = {b: M[b] for b in list(M)[:2]}
+            nb = len(levl.boxes)
+            sub = list(range(min(2, nb)))
+            M = {b: rng.standard_normal(K) + 1j * rng.standard_normal(K) for b in sub}
+            if l <= L:
+                Mall = {b: rng.standard_normal(K) + 1j * rng.standard_normal(K) for b in range(nb)}
+                nnz_s = sum(len(interaction_list(levl, levl.boxes[a])) for a in sub)
+                nnz = sum(len(interaction_list(levl, levl.boxes[a])) for a in range(nb))
                 t0 = time.perf_counter()
-                f.m2m(sub, l)
-                tmid += (time.perf_counter() - t0) * len(levl.boxes) / 2
+                f.m2l(Mall, l, targets=sub)
+                tmid += (time.perf_counter() - t0) * nnz / max(nnz_s, 1)
+            if l > 2:
+                t0 = time.perf_counter()
+                f.m2m(M, l)
+                tmid += (time.perf_counter() - t0) * nb / len(sub)
                 Kp = plan.levels[l - 1].K
                 Lp = {p: rng.standard_normal(Kp) + 1j * rng.standard_normal(Kp) for p in range(len(f.levels[l - 1].boxes))}
                 t0 = time.perf_counter()
-                f.l2l(Lp, {c: M[c] for c in list(M)[:2]}, l - 1)
-                tmid += (time.perf_counter() - t0) * len(levl.boxes) / 2
+                f.l2l(Lp, M, l - 1)
+                tmid += (time.perf_counter() - t0) * nb / len(sub)
         total = ts2m + tp2p + tl2t + tmid
-        desc = (f"oracle passes on {len(leaves)} of {len(lev.boxes)} far-field leaves ({len(pts)} points: S2M, "
-                f"L2T, P2P), M2L on 2 boxes/level, M2M+L2L on 2 children/level; each term scaled by its unit count")
+        desc = (f"oracle passes on {len(leaves)} of {len(lev.boxes)} far-field leaves ({len(pts)} points: S2M and "
+                f"L2T at source level {S}, P2P at L_f={L}), M2L on 2 boxes/level, M2M+L2L on 2 children/level; "
+                f"each term scaled by its unit count")
         return total, desc, 1
 
 

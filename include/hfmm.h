@@ -62,6 +62,14 @@ extern "C" {
 #define HFMM_ALPHA_FIXED 0x4u      /* use the caller's alpha at every level (the paper's fixed
                                       design radius); default: per level the largest alpha in
                                       {1, 0.9, 0.8} (>= the caller's) that keeps F_l <= tau   */
+#define HFMM_SOURCE_AT_LF 0x8u     /* S2M / L2T at L_f (the paper's setup, no translation-only
+                                      levels); default: source level D_s by the policy below */
+#define HFMM_SOURCE_AT_DEPTH 0x10u /* S2M / L2T at the configured depth D.  Default policy
+                                      (R-14): the deepest level <= D whose occupied
+                                      boxes hold >= 8 points on average; levels L_f < l <= D_s
+                                      are translation-only (M2M up / L2L down, no M2L)
+                                      on grids whose dropped Jacobi-Anger tail of
+                                      eqn:PlaneWaveSpec is <= eps / 100        */
 
 /* ---- matvec memory kinds -------------------------------------------------------------- */
 #define HFMM_HOST 0    /* q and y are host pointers (pinned or pageable)                     */
@@ -84,6 +92,7 @@ typedef struct {
   int active;       /* 1 if M2L runs at this level                                         */
   int64_t boxes;    /* occupied boxes at this level                                        */
   int64_t m2l_pairs;/* interaction-list entries at this level (all ranks)                  */
+  int rep;          /* 1: translation-only level L_f < l <= D_s (R-14; ell = 0, F = NaN)   */
 } hfmm_level_info;
 
 typedef struct {
@@ -95,9 +104,10 @@ typedef struct {
   hfmm_level_info level[HFMM_MAX_LEVELS];
   int64_t p2p_pairs;       /* ordered near-field pairs i != j (owned targets)                */
   int64_t p2p_sym_pairs;   /* unordered pairs of them evaluated once (symmetric kernel)      */
-  int64_t s2m_evals;       /* points x directions at L_f                                    */
+  int64_t s2m_evals;       /* owned points x directions at the source level D_s             */
   int rank, nranks;
   int64_t owned_points;    /* points whose y this rank computes                              */
+  int source_level;        /* D_s: level of S2M / L2T (R-14), -1 if no far field             */
 } hfmm_info;
 
 /* Create a plan on CUDA device `device` (-1: the current device).  *out receives the plan. */
@@ -159,6 +169,13 @@ const char *hfmm_last_error(const hfmm_plan *p);
 
 /* Free everything owned by the plan, including the NCCL communicator. */
 void hfmm_destroy(hfmm_plan *p);
+
+/* Host-only (no GPU needed): grid (N_theta, N_phi) of a translation-only level of box size a
+ * (R-14; eqn:PlaneWaveSpec): smallest even 7-smooth N_theta >= 4 and
+ * smallest 7-smooth multiple of 4 N_phi whose dropped Jacobi-Anger tail
+ * 2 sum_{n >= N/2} |J_n(kappa (sqrt3/2) a)| is <= eps / 100.  Returns 0, HFMM_E_ARG or
+ * HFMM_E_SEARCH. */
+int hfmm_rep_grid(double kappa, double a, double eps, int *n_theta, int *n_phi);
 
 /* ---- host-only plan helpers (no GPU needed) ---------------------------------------------
  * The per-level quadrature of P:140-722 for box size a: returns ell, N_theta, N_phi

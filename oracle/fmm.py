@@ -12,6 +12,9 @@
   P2P  sum over j != i in the neighbour list N(B^L_a) of e^{i kappa R}/R psi_j
 If no level is admissible (L_f is None) the near field is every pair (direct sum).
 Highest M2L level is l = 2; no work at levels 0-1.
+Source level D_s = plan.source_level (reading R-14): S2M and L2T at D_s; the levels
+L_f < l <= D_s are translation-only (M2M up, L2L down with I = 0); M2L at 2..L_f and the
+near field (P2P) over the neighbour lists of L_f, exactly as for D_s = L_f.
 """
 from __future__ import annotations
 
@@ -34,9 +37,10 @@ class OracleFMM:
         self.plan = plan
         self.kappa = plan.kappa
         self.L = plan.L_f
+        self.S = plan.source_level if plan.source_level is not None else plan.L_f
         self.levels = {}
         if self.L is not None:
-            for l in range(2, self.L + 1):
+            for l in range(2, self.S + 1):
                 self.levels[l] = build_level(self.x, self.lo, self.a0, l)
         self._tables: Dict[tuple, np.ndarray] = {}
 
@@ -58,8 +62,8 @@ class OracleFMM:
 
     # ---- passes ---------------------------------------------------------------
     def s2m(self, q: np.ndarray, boxes=None) -> Dict[int, np.ndarray]:
-        lev = self.levels[self.L]
-        S = self.grid(self.L)
+        lev = self.levels[self.S]
+        S = self.grid(self.S)
         out = {}
         for b in (range(len(lev.boxes)) if boxes is None else boxes):
             idx = lev.members[b]
@@ -107,12 +111,12 @@ class OracleFMM:
         return out
 
     def l2t(self, Lf: Dict[int, np.ndarray], targets: np.ndarray) -> np.ndarray:
-        lev = self.levels[self.L]
-        lp = self.plan.levels[self.L]
-        S = self.grid(self.L)
+        lev = self.levels[self.S]
+        lp = self.plan.levels[self.S]
+        S = self.grid(self.S)
         w = 8 * math.pi ** 2 / (lp.n_theta * lp.n_phi)
         y = np.zeros(len(targets), dtype=np.complex128)
-        box_of = self._box_of_points(targets)
+        box_of = self._box_of_points(targets, self.S)
         for a in np.unique(box_of):
             sel = np.nonzero(box_of == a)[0]
             d = lev.centers[a] - self.x[targets[sel]]                            # c_a - x_i
@@ -127,7 +131,7 @@ class OracleFMM:
             groups = {None: np.arange(len(targets))}
         else:
             lev = self.levels[self.L]
-            box_of = self._box_of_points(targets)
+            box_of = self._box_of_points(targets, self.L)
             groups, src_sets = {}, {}
             for a in np.unique(box_of):
                 groups[a] = np.nonzero(box_of == a)[0]
@@ -145,22 +149,25 @@ class OracleFMM:
             y[sel] = G @ q[src]
         return y
 
-    def _box_of_points(self, idx: np.ndarray) -> np.ndarray:
-        lev = self.levels[self.L]
-        n = 2 ** self.L
+    def _box_of_points(self, idx: np.ndarray, level: int) -> np.ndarray:
+        lev = self.levels[level]
+        n = 2 ** level
         b = np.minimum(np.floor((self.x[idx] - self.lo) / lev.a).astype(np.int64), n - 1)
         return np.array([lev.index[tuple(v)] for v in b], dtype=np.int64)
 
     # ---- the matvec ------------------------------------------------------------
     def far_locals(self, q: np.ndarray):
-        """Run S2M, M2M, M2L, L2L; return (M per level, I per level, L at L_f)."""
-        L = self.L
-        M = {L: self.s2m(q)}
-        for l in range(L, 2, -1):
+        """Run S2M, M2M, M2L, L2L; return (M per level, I per level, L per level down to D_s)."""
+        L, S = self.L, self.S
+        M = {S: self.s2m(q)}
+        for l in range(S, 2, -1):
             M[l - 1] = self.m2m(M[l], l)
         I = {l: self.m2l(M[l], l) for l in range(2, L + 1)}
+        for l in range(L + 1, S + 1):                 # translation-only levels: no M2L (R-14)
+            K = self.plan.levels[l].K
+            I[l] = {b: np.zeros(K, dtype=np.complex128) for b in range(len(self.levels[l].boxes))}
         Lloc = {2: I[2]}
-        for l in range(2, L):
+        for l in range(2, S):
             Lloc[l + 1] = self.l2l(Lloc[l], I[l + 1], l)
         return M, I, Lloc
 
@@ -174,7 +181,7 @@ class OracleFMM:
             y_far = np.zeros_like(y_near)
         else:
             _, _, Lloc = self.far_locals(q)
-            y_far = self.l2t(Lloc[self.L], targets)
+            y_far = self.l2t(Lloc[self.S], targets)
         if parts:
             return y_near, y_far
         return y_near + y_far

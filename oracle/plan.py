@@ -24,6 +24,16 @@ Readings of silent/ambiguous points are listed in DESIGN.md ("Readings"):
       whose quadrature keeps F_l <= tau (the paper uses alpha = 1 for its volume timing runs,
       P:1161, and 0.8 in its error studies; pairs beyond alpha sqrt3 a are not covered
       by the bound).  alpha_fixed=True: the caller's alpha at every level.
+  R-14 source level ("additional translation steps"): S2M and L2T
+      run at a source level D_s in [L_f, depth]; the levels L_f < l <= D_s are translation-only
+      (M2M up, L2L down with I = 0, no M2L).  Their grid represents the outgoing field of a box,
+      a sum of plane waves e^{i kappa s.(x - c)} with |x - c| <= rho_l = (sqrt3/2) a_l, whose
+      Fourier series in theta (and phi) is the Jacobi-Anger series of eqn:PlaneWaveSpec
+       with argument <= kappa rho_l: N_theta = smallest even 7-smooth N >= 4 and
+      N_phi = smallest 7-smooth multiple of 4 whose dropped band |n| >= N/2 has
+      2 sum_{n >= N/2} |J_n(kappa rho_l)| <= eps / 100.  R-5 (monotone grids) holds on the
+      whole chain 2..D_s.  Policy for D_s (choose_source_level): the deepest level <= depth whose
+      occupied boxes hold >= 8 points on average (L_f if none); D_s = L_f is the paper's setup.
 """
 from __future__ import annotations
 
@@ -177,6 +187,7 @@ class LevelPlan:
     F: float = float("nan")
     active: bool = False
     alpha: float = 0.8
+    rep: bool = False        # translation-only level below L_f (R-14): no ell, no M2L
 
     @property
     def K(self) -> int:
@@ -193,6 +204,7 @@ class Plan:
     depth: int
     levels: dict            # level -> LevelPlan
     L_f: Optional[int]      # None: no admissible level -> P2P over all pairs
+    source_level: Optional[int] = None   # S2M / L2T level D_s (R-14); None iff L_f is None
 
 
 def level_params(kappa: float, a: float, eps: float, alpha: float, eps_absolute: bool = False):
@@ -215,6 +227,39 @@ def level_F(kappa: float, a: float, ell: int, nth: int, nph: int) -> float:
     return 8 * math.pi * U_ROUND * a * mx
 
 
+REP_EPS_FACTOR = 1e-2       # R-14: representation tail <= eps / 100
+MIN_MEAN_POINTS = 8.0       # R-14: source-level policy
+
+
+def rep_tail(z: float, N: int) -> float:
+    """Jacobi-Anger mass dropped by keeping |n| <= N/2 - 1 (eqn:PlaneWaveSpec)."""
+    J = np.abs(besselJ(N + 2 * int(math.ceil(z)) + 40, z))
+    return 2.0 * float(np.sum(J[N // 2:]))
+
+
+def rep_grid(kappa: float, a: float, eps: float):
+    """(N_theta, N_phi) of a translation-only level of box size a (R-14)."""
+    z = kappa * math.sqrt(3.0) / 2.0 * a
+    thr = eps * REP_EPS_FACTOR
+    nth = next(N for N in range(4, 100000, 2) if is_7smooth(N) and rep_tail(z, N) <= thr)
+    nph = next(N for N in range(4, 100000, 4) if is_7smooth(N) and rep_tail(z, N) <= thr)
+    return nth, nph
+
+
+def choose_source_level(x: np.ndarray, lo, a0: float, depth: int, L_f: Optional[int],
+                        min_mean: float = MIN_MEAN_POINTS) -> Optional[int]:
+    """R-14 policy: deepest l in [L_f, depth] whose occupied boxes hold >= min_mean points on average."""
+    if L_f is None:
+        return None
+    from .tree import box_coords
+    for l in range(depth, L_f, -1):
+        b = box_coords(np.asarray(x), lo, a0, l)
+        nocc = len(np.unique(b[:, 0] * 4 ** l + b[:, 1] * 2 ** l + b[:, 2]))
+        if len(x) / nocc >= min_mean:
+            return l
+    return L_f
+
+
 def default_tau(eps: float) -> float:
     return min(eps / 10.0, 1e-9)
 
@@ -228,7 +273,8 @@ def alpha_candidates(alpha: float, fixed: bool):
 
 def make_plan(kappa: float, eps: float, a0: float, depth: int, alpha: float = 0.8,
               tau: Optional[float] = None, force_all: bool = False,
-              eps_absolute: bool = False, alpha_fixed: bool = False) -> Plan:
+              eps_absolute: bool = False, alpha_fixed: bool = False,
+              source_level: Optional[int] = None) -> Plan:
     """Plan for levels 2..depth (P:140-722 + admissibility R-9, design radius R-13, monotone R-5).
 
     Shallowest level first: for each candidate design radius alpha (R-13, largest first) take
@@ -259,13 +305,27 @@ def make_plan(kappa: float, eps: float, a0: float, depth: int, alpha: float = 0.
             L_f = l
         else:
             stop = l
-    # monotone grids on the chain 2..L_f (R-5)
+    plan = Plan(kappa, eps, alpha, tau, a0, depth, levels, L_f, L_f)
     if L_f is not None:
-        for l in range(L_f - 1, 1, -1):
-            up, dn = levels[l], levels[l + 1]
-            nth = max(up.n_theta, dn.n_theta)
-            nph = max(up.n_phi, dn.n_phi)
-            if (nth, nph) != (up.n_theta, up.n_phi):
-                up.n_theta, up.n_phi = nth, nph
+        set_source_level(plan, L_f if source_level is None else source_level)
+    return plan
+
+
+def set_source_level(plan: Plan, source_level: int) -> Plan:
+    """Translation-only levels L_f < l <= D_s (R-14) and monotone grids on the chain 2..D_s (R-5)."""
+    L_f, kappa, eps, a0, levels = plan.L_f, plan.kappa, plan.eps, plan.a0, plan.levels
+    D_s = max(L_f, min(int(source_level), plan.depth))
+    for l in range(L_f + 1, D_s + 1):
+        a = a0 / 2 ** l
+        nth, nph = rep_grid(kappa, a, eps)
+        levels[l] = LevelPlan(l, a, 0, nth, nph, [], alpha=plan.alpha, rep=True)
+    for l in range(D_s - 1, 1, -1):
+        up, dn = levels[l], levels[l + 1]
+        nth = max(up.n_theta, dn.n_theta)
+        nph = max(up.n_phi, dn.n_phi)
+        if (nth, nph) != (up.n_theta, up.n_phi):
+            up.n_theta, up.n_phi = nth, nph
+            if not up.rep:
                 up.F = level_F(kappa, up.a, up.ell, nth, nph)
-    return Plan(kappa, eps, alpha, tau, a0, depth, levels, L_f)
+    plan.source_level = D_s
+    return plan

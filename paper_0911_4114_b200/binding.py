@@ -22,6 +22,8 @@ HFMM_W_NO_FARFIELD = 2
 HFMM_EPS_ABSOLUTE = 0x1
 HFMM_FORCE_ALL_LEVELS = 0x2
 HFMM_ALPHA_FIXED = 0x4
+HFMM_SOURCE_AT_LF = 0x8
+HFMM_SOURCE_AT_DEPTH = 0x10
 HFMM_HOST = 0
 HFMM_DEVICE = 1
 HFMM_Y_LOCAL = 2
@@ -31,7 +33,7 @@ EXPORTED = [
     "hfmm_create", "hfmm_set_dist", "hfmm_nccl_unique_id", "hfmm_build_tree", "hfmm_precompute", "hfmm_matvec",
     "hfmm_direct", "hfmm_get_info", "hfmm_stage_times", "hfmm_debug_copy", "hfmm_last_error",
     "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
-    "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition",
+    "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
 ]
 
 
@@ -39,7 +41,7 @@ class LevelInfo(C.Structure):
     _fields_ = [("level", C.c_int), ("a", C.c_double), ("ell", C.c_int), ("n_theta", C.c_int),
                 ("n_phi", C.c_int), ("alpha", C.c_double), ("K", C.c_int64), ("F", C.c_double),
                 ("active", C.c_int),
-                ("boxes", C.c_int64), ("m2l_pairs", C.c_int64)]
+                ("boxes", C.c_int64), ("m2l_pairs", C.c_int64), ("rep", C.c_int)]
 
 
 class Info(C.Structure):
@@ -47,7 +49,8 @@ class Info(C.Structure):
                 ("eps", C.c_double), ("alpha", C.c_double), ("tau", C.c_double), ("nlevels", C.c_int),
                 ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("p2p_sym_pairs", C.c_int64),
                 ("s2m_evals", C.c_int64),
-                ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64)]
+                ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64),
+                ("source_level", C.c_int)]
 
 
 class HFMMError(RuntimeError):
@@ -89,6 +92,7 @@ def load() -> C.CDLL:
         "hfmm_l2l_op": (ci, [ci, ci, ci, ci, ci, vp, vp, vp, vp, vp, vp]),
         "hfmm_m2l_op": (ci, [ci, i64, vp, vp, vp, vp, vp, vp, vp]),
         "hfmm_partition": (ci, [i64, vp, ci, vp, dbl, ci, i64, ci, vp, vp, vp]),
+        "hfmm_rep_grid": (ci, [dbl, dbl, dbl, C.POINTER(ci), C.POINTER(ci)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -118,6 +122,15 @@ def level_quadrature(kappa: float, a: float, eps_level: float, alpha: float = 0.
     if rc < 0:
         raise HFMMError(rc, "hfmm_level_quadrature failed")
     return ell.value, nth.value, nph.value, list(rag[: nth.value // 2 + 1])
+
+
+def rep_grid(kappa: float, a: float, eps: float):
+    """Host-only: (N_theta, N_phi) of a translation-only level (include/hfmm.h hfmm_rep_grid)."""
+    nth, nph = C.c_int(), C.c_int()
+    rc = load().hfmm_rep_grid(kappa, a, eps, C.byref(nth), C.byref(nph))
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_rep_grid")
+    return nth.value, nph.value
 
 
 def partition(xyz, depth, lo, size, L_f, K, nranks):
@@ -222,11 +235,13 @@ class HFMM:
             lv = inf.level[i]
             levels.append(dict(level=lv.level, a=lv.a, ell=lv.ell, n_theta=lv.n_theta, n_phi=lv.n_phi,
                                alpha=lv.alpha, K=lv.K,
-                               F=lv.F, active=bool(lv.active), boxes=lv.boxes, m2l_pairs=lv.m2l_pairs))
+                               F=lv.F, active=bool(lv.active), boxes=lv.boxes, m2l_pairs=lv.m2l_pairs,
+                               rep=bool(lv.rep)))
         return dict(n=inf.n, depth=inf.depth, L_f=(None if inf.L_f < 0 else inf.L_f), kappa=inf.kappa,
                     eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
                     p2p_sym_pairs=inf.p2p_sym_pairs,
-                    s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points)
+                    s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points,
+                    source_level=(None if inf.source_level < 0 else inf.source_level))
 
     def stage_times(self):
         out = (C.c_double * 8)()

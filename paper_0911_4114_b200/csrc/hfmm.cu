@@ -34,6 +34,7 @@ struct LevelDev {
   int64_t K = 0;
   double F = NAN;
   bool active = false;
+  bool rep = false;              // translation-only level L_f < l <= D_s (R-14)
   int64_t nbox = 0;
   int64_t own0 = 0, own1 = 0;  // owned box range (Morton order)
   std::vector<int64_t> rlo, rhi; // every rank's owned range (for the all-gather)
@@ -99,6 +100,9 @@ struct hfmm_plan {
   double kappa = 0, eps = 0, alpha = 0, tau = 0;
   unsigned flags = 0;
   int L_f = -1;
+  int D_s = -1;              // source level (S2M / L2T), R-14; -1 without far field
+  bool small_src = false;    // source boxes small: warp-per-box S2M / L2T kernels
+  int64_t *first_src = nullptr;  // point ranges of source-level boxes
   std::vector<LevelDev> lv;  // index = level
   int near_level = 0;        // level of the near-field boxes (L_f or 0)
   int64_t own_pt0 = 0, own_pt1 = 0;
@@ -152,11 +156,11 @@ static void free_levels(hfmm_plan *p) {
       if (ptr) cudaFree(ptr);
   }
   p->lv.clear();
-  for (void *ptr : {(void *)p->first_near, (void *)p->tile_leaf, (void *)p->tile_begin, (void *)p->tmp,
+  for (void *ptr : {(void *)p->first_near, (void *)p->first_src, (void *)p->tile_leaf, (void *)p->tile_begin, (void *)p->tmp,
                     (void *)p->y_far, (void *)p->p2p_items[0], (void *)p->p2p_items[1], (void *)p->p2p_items[2],
                     (void *)p->dir_items, (void *)p->ux, (void *)p->uy, (void *)p->uz})
     if (ptr) cudaFree(ptr);
-  p->first_near = nullptr, p->tile_leaf = nullptr;
+  p->first_near = nullptr, p->first_src = nullptr, p->tile_leaf = nullptr;
   p->tile_begin = nullptr, p->tmp = nullptr, p->y_far = nullptr;
   for (int k = 0; k < 3; ++k) p->p2p_items[k] = nullptr, p->p2p_nitems[k] = 0;
   p->dir_items = nullptr, p->dir_nitems = 0;
@@ -368,7 +372,7 @@ static void partition(hfmm_plan *p) {
   const LevelBoxes &BL = t.levels[p->L_f];
   std::vector<int64_t> cut;
   partition_level2(t, p->L_f, p->lv[p->L_f].K, R, cut);
-  for (int l = 2; l <= p->L_f; ++l) {
+  for (int l = 2; l <= std::max(p->L_f, p->D_s); ++l) {
     LevelDev &L = p->lv[l];
     L.rlo.assign(R, 0), L.rhi.assign(R, 0);
     for (int q = 0; q < R; ++q) {
@@ -463,21 +467,47 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     int rc = level_quad(p->lv[l], alpha);
     if (rc) return rc;
   }
-  // monotone grids along the active chain (R-5)
-  for (int l = p->L_f - 1; l >= 2; --l) {
+  // source level D_s and the translation-only levels L_f < l <= D_s (R-14)
+  p->D_s = -1;
+  if (p->L_f >= 2) {
+    int Ds = p->L_f;
+    if (flags & HFMM_SOURCE_AT_DEPTH) {
+      Ds = D;
+    } else if (!(flags & HFMM_SOURCE_AT_LF)) {
+      for (int l = D; l > p->L_f; --l)
+        if ((double)t.n / (double)t.levels[l].nbox() >= 8.0) {
+          Ds = l;
+          break;
+        }
+    }
+    for (int l = p->L_f + 1; l <= Ds; ++l) {
+      LevelDev &L = p->lv[l];
+      if (select_rep_grid(kappa, L.a, eps, &L.nth, &L.nph)) {
+        p->err = "hfmm_precompute: representation grid search failed at level " + std::to_string(l);
+        return HFMM_E_SEARCH;
+      }
+      L.rep = true, L.active = false, L.ell = 0, L.F = NAN, L.alpha = alpha;
+      L.K = (int64_t)L.nth * L.nph / 2;
+    }
+    p->D_s = Ds;
+  }
+  // monotone grids along the chain 2..D_s (R-5)
+  for (int l = p->D_s - 1; l >= 2; --l) {
     LevelDev &U = p->lv[l], &Dn = p->lv[l + 1];
     int nth = std::max(U.nth, Dn.nth), nph = std::max(U.nph, Dn.nph);
     if (nth != U.nth || nph != U.nph) {
       U.nth = nth, U.nph = nph, U.K = (int64_t)nth * nph / 2;
-      cudaFree(U.T);
-      int rc = level_tables(p, U, &U.T, &U.F);
-      if (rc) return rc;
+      if (!U.rep) {
+        cudaFree(U.T);
+        int rc = level_tables(p, U, &U.T, &U.F);
+        if (rc) return rc;
+      }
     }
   }
   partition(p);
-  // device data of the active levels
+  // device data of the levels 2..D_s (M2L data only on the active levels 2..L_f)
   size_t tmp_need = 0;
-  for (int l = 2; l <= p->L_f; ++l) {
+  for (int l = 2; l <= p->D_s; ++l) {
     LevelDev &L = p->lv[l];
     const LevelBoxes &B = t.levels[l];
     std::vector<double> cx(B.nbox()), cy(B.nbox()), cz(B.nbox());
@@ -495,15 +525,15 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       L.ks = dupload(ksu);
     }
     L.M = dalloc<double2>((size_t)L.nbox * L.K);
-    L.I = dalloc<double2>((size_t)L.nbox * L.K);
+    L.I = L.active ? dalloc<double2>((size_t)L.nbox * L.K) : nullptr;
     L.L = dalloc<double2>((size_t)L.nbox * L.K);
-    if (!L.M || !L.I || !L.L || !L.ks) {
+    if (!L.M || (L.active && !L.I) || !L.L || !L.ks) {
       p->err = "hfmm_precompute: allocation failed (level buffers)";
       return HFMM_E_NOMEM;
     }
-    // interaction lists for every box of the level
+    // interaction lists for every box of an active level
     std::vector<int32_t> row(1, 0), src, oid;
-    for (int64_t b = 0; b < B.nbox(); ++b) {
+    for (int64_t b = 0; b < (L.active ? B.nbox() : 0); ++b) {
       const int px = B.ix[b] >> 1, py = B.iy[b] >> 1, pz = B.iz[b] >> 1;
       for (int dx = -3; dx <= 3; ++dx)
         for (int dy = -3; dy <= 3; ++dy)
@@ -527,7 +557,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     for (int64_t b = 0; b < B.nbox(); ++b) oc[b] = (int8_t)(((B.ix[b] & 1) << 2) | ((B.iy[b] & 1) << 1) | (B.iz[b] & 1));
     L.parent = dupload(par);
     L.oct = dupload(oc);
-    if (l < p->L_f) {
+    if (l < p->D_s) {
       std::vector<int32_t> cb(B.child_begin.begin(), B.child_begin.end());
       L.cbeg = dupload(cb);
       // translation tables on this grid for children at level l+1
@@ -636,12 +666,21 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       p->dir_items = dupload(d);
       p->dir_nitems = (int64_t)d.size() / 4;
     }
-    // L2T tiles: kTile targets of one owned far-field leaf
+    // source level: box point ranges; L2T tiles (kTile targets of one owned source box) unless
+    // the boxes are small (< 64 points on average: warp-per-box S2M / L2T kernels)
     std::vector<int32_t> tl;
     std::vector<int64_t> tb;
-    if (p->L_f >= 2)
-      for (int64_t b = p->lv[p->L_f].own0; b < p->lv[p->L_f].own1; ++b)
-        for (int64_t s0 = B.first[b]; s0 < B.first[b + 1]; s0 += kTile) tl.push_back((int32_t)b), tb.push_back(s0);
+    p->small_src = false;
+    if (p->L_f >= 2) {
+      const LevelBoxes &Bs = t.levels[p->D_s];
+      const LevelDev &Ls = p->lv[p->D_s];
+      const int64_t nown = Ls.own1 - Ls.own0;
+      p->small_src = nown > 0 && (double)(Bs.first[Ls.own1] - Bs.first[Ls.own0]) < 64.0 * (double)nown;
+      if (!p->small_src)
+        for (int64_t b = Ls.own0; b < Ls.own1; ++b)
+          for (int64_t s0 = Bs.first[b]; s0 < Bs.first[b + 1]; s0 += kTile) tl.push_back((int32_t)b), tb.push_back(s0);
+      p->first_src = dupload(Bs.first);
+    }
     p->first_near = dupload(B.first);
     p->tile_leaf = dupload(tl), p->tile_begin = dupload(tb);
     p->ntiles = (int64_t)tl.size();
@@ -666,8 +705,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     hfmm_level_info &li = in.level[in.nlevels++];
     li.level = l, li.a = L.a, li.ell = L.ell, li.n_theta = L.nth, li.n_phi = L.nph, li.alpha = L.alpha, li.K = L.K,
     li.F = L.F, li.active = L.active ? 1 : 0, li.boxes = L.nbox, li.m2l_pairs = L.il_nnz;
+    li.rep = L.rep ? 1 : 0;
   }
-  in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->L_f].K : 0;
+  in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
+  in.source_level = p->D_s;
   in.owned_points = p->own_pt1 - p->own_pt0;
   p->have_plan = true;
   if (p->L_f < 0) {
@@ -719,12 +760,14 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
   CK(cudaEventRecord(p->ev_join, p->stream2));
   const TwiddleSet &tw = global_twiddles(p->device);
   if (p->L_f >= 2) {
-    const int Lf = p->L_f;
-    LevelDev &F = p->lv[Lf];
-    launch_s2m(pts, p->first_near, F.cx, F.cy, F.cz, (int32_t)F.own0,
-               (int32_t)F.own1, F.ks, F.K, F.M, s);
+    const int Lf = p->L_f, Ds = p->D_s;
+    LevelDev &F = p->lv[Ds];
+    if (p->small_src)
+      launch_s2m_small(pts, p->first_src, F.cx, F.cy, F.cz, (int32_t)F.own0, (int32_t)F.own1, F.ks, F.K, F.M, s);
+    else
+      launch_s2m(pts, p->first_src, F.cx, F.cy, F.cz, (int32_t)F.own0, (int32_t)F.own1, F.ks, F.K, F.M, s);
     if (prof) cudaEventRecord(p->sev[1], s);
-    for (int l = Lf; l > 2; --l) {  // M2M
+    for (int l = Ds; l > 2; --l) {  // M2M, through the translation-only levels too
       LevelDev &C = p->lv[l], &P = p->lv[l - 1];
       if (C.own1 > C.own0) {
         launch_rows_up(C.M + C.own0 * C.K, C.own1 - C.own0, C.nth, C.nph, P.nph, p->tmp, tw, s);
@@ -743,20 +786,25 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
       launch_m2l((int32_t)L.own0, (int32_t)L.own1, L.K, L.il_row, L.il_src, L.il_oid, L.T, L.M, L.I, s);
     }
     if (prof) cudaEventRecord(p->sev[3], s);
-    for (int l = 2; l < Lf; ++l) {  // L2L; L_2 = I_2
+    for (int l = 2; l < Ds; ++l) {  // L2L; L_2 = I_2; I = 0 below L_f (R-14)
       LevelDev &P = p->lv[l], &C = p->lv[l + 1];
       const double2 *Lp = (l == 2) ? P.I : P.L;
       if (C.own1 > C.own0) {
         launch_cols_down(Lp, P.nth, P.nph, C.nth, C.parent + C.own0, C.oct + C.own0, C.own1 - C.own0,
                          P.shift, p->tmp, tw, s);
-        launch_rows_down(p->tmp, C.own1 - C.own0, C.nth, P.nph, C.nph, C.I + C.own0 * C.K,
+        launch_rows_down(p->tmp, C.own1 - C.own0, C.nth, P.nph, C.nph, C.I ? C.I + C.own0 * C.K : nullptr,
                          C.L + C.own0 * C.K, tw, s);
       }
     }
     if (prof) cudaEventRecord(p->sev[4], s);
-    const double2 *Lf_loc = (Lf == 2) ? F.I : F.L;
-    launch_l2t(pts, p->first_near, F.cx, F.cy, F.cz, p->tile_leaf, p->tile_begin, p->ntiles, F.ks, F.K,
-               Lf_loc, 8.0 * kPi * kPi / ((double)F.nth * (double)F.nph), p->y_far, s);
+    const double2 *Lf_loc = (Ds == 2) ? F.I : F.L;
+    const double wq = 8.0 * kPi * kPi / ((double)F.nth * (double)F.nph);
+    if (p->small_src)
+      launch_l2t_small(pts, p->first_src, F.cx, F.cy, F.cz, (int32_t)F.own0, (int32_t)F.own1, F.ks, F.K, Lf_loc, wq,
+                       p->y_far, s);
+    else
+      launch_l2t(pts, p->first_src, F.cx, F.cy, F.cz, p->tile_leaf, p->tile_begin, p->ntiles, F.ks, F.K, Lf_loc, wq,
+                 p->y_far, s);
     if (prof) cudaEventRecord(p->sev[5], s);
   } else if (prof) {
     for (int k = 1; k <= 5; ++k) cudaEventRecord(p->sev[k], s);
@@ -867,7 +915,8 @@ extern "C" int hfmm_debug_copy(const hfmm_plan *p, int what, int level, void *ho
   int64_t bytes = 0;
   std::vector<int64_t> hostbuf;
   if (what >= 0 && what <= 3) {
-    if (level < 2 || level >= (int)p->lv.size() || (what != 3 && level > p->L_f)) return HFMM_E_ARG;
+    if (level < 2 || level >= (int)p->lv.size() || (what != 3 && level > std::max(p->L_f, p->D_s)))
+      return HFMM_E_ARG;
     const LevelDev &L = p->lv[level];
     if (what == 3) {
       src = L.T, bytes = (int64_t)316 * L.K * 16;

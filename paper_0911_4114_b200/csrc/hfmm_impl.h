@@ -31,6 +31,7 @@ int select_ntheta(int ell, double kappa, double r, double r0, double eps, int *n
 int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth, int *nph,
                 std::vector<int> *ragged);
 bool seven_smooth(int n);
+int select_rep_grid(double kappa, double a, double eps, int *nth, int *nph);  // R-14
 
 // ---------------- tree (host_tree.cpp) ------------------------------------------------------
 struct LevelBoxes {
@@ -115,6 +116,13 @@ void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const dou
                 const double *cz, const int32_t *tile_leaf, const int64_t *tile_begin,
                 int64_t ntiles, const double *ks, int64_t K, const double2 *L, double w,
                 double2 *y_far, cudaStream_t s);
+
+// Small-box variants (source level below L_f, R-14): one warp per box, persistent grid.
+void launch_s2m_small(PointsDev pts, const int64_t *first, const double *cx, const double *cy, const double *cz,
+                      int32_t box0, int32_t box1, const double *ks, int64_t K, double2 *M, cudaStream_t s);
+void launch_l2t_small(PointsDev pts, const int64_t *first, const double *cx, const double *cy, const double *cz,
+                      int32_t box0, int32_t box1, const double *ks, int64_t K, const double2 *L, double w,
+                      double2 *y_far, cudaStream_t s);
 
 // M2L: I[a][k] = sum_e T[oid_e][k] M[src_e][k]
 void launch_m2l(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,

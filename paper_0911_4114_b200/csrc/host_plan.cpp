@@ -242,7 +242,39 @@ int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth,
   return HFMM_E_SEARCH;
 }
 
+// Translation-only level (R-14): the outgoing field of a box is a sum of plane waves
+// e^{i kappa s.(x - c)}, |x - c| <= rho = (sqrt3/2) a, whose Fourier series in theta and in phi is
+// the Jacobi-Anger series of eqn:PlaneWaveSpec with argument <= kappa rho.  Keeping
+// |n| <= N/2 - 1 (R-6) drops 2 sum_{n >= N/2} |J_n(kappa rho)|; take the smallest even 7-smooth
+// N_theta >= 4 and the smallest 7-smooth multiple of 4 N_phi with that tail <= eps / 100.
+int select_rep_grid(double kappa, double a, double eps, int *nth, int *nph) {
+  const double z = kappa * std::sqrt(3.0) / 2.0 * a, thr = eps * 1e-2;
+  const int nmax = 4 * (int)std::ceil(z) + 256;
+  std::vector<double> J;
+  cyl_bessel_J(nmax + 40, z, J);
+  std::vector<double> tail(nmax + 2, 0.0);  // tail[m] = 2 sum_{n >= m} |J_n|
+  for (int m = nmax + 40; m >= nmax + 1; --m) tail[nmax + 1] += 2.0 * std::fabs(J[m]);
+  for (int m = nmax; m >= 0; --m) tail[m] = tail[m + 1] + 2.0 * std::fabs(J[m]);
+  *nth = *nph = 0;
+  for (int N = 4; N <= 2 * nmax; N += 2)
+    if (seven_smooth(N) && tail[N / 2] <= thr) {
+      *nth = N;
+      break;
+    }
+  for (int N = 4; N <= 2 * nmax; N += 4)
+    if (seven_smooth(N) && tail[N / 2] <= thr) {
+      *nph = N;
+      break;
+    }
+  return (*nth && *nph) ? 0 : HFMM_E_SEARCH;
+}
+
 }  // namespace hfmm
+
+extern "C" int hfmm_rep_grid(double kappa, double a, double eps, int *n_theta, int *n_phi) {
+  if (!(kappa > 0) || !(a > 0) || !(eps > 0) || !n_theta || !n_phi) return HFMM_E_ARG;
+  return hfmm::select_rep_grid(kappa, a, eps, n_theta, n_phi);
+}
 
 extern "C" int hfmm_level_quadrature(double kappa, double a, double eps_level, double alpha,
                                      int *ell, int *n_theta, int *n_phi, int *ragged,

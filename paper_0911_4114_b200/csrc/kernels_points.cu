@@ -346,6 +346,147 @@ void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const dou
 }
 
 // ---------------------------------------------------------------------------------------------
+// Small-box S2M / L2T (source level D_s below L_f, R-14: a few to a few tens of points
+// per box, K of a few hundred).  Persistent CTAs (the e^{ih k} table is filled once per CTA),
+// one warp per box.
+//   S2M: lanes over directions (k0 + lane, k0 + 32 + lane), the box's points staged 32 at a
+//        time in a per-warp shared buffer (positions relative to the centre) and broadcast.
+//   L2T: lane = (point p = lane % P, slice = lane / P) with P = the next power of two >= the
+//        box's points (<= 32) and 32/P slices of the directions; slices reduced by shuffles.
+// ---------------------------------------------------------------------------------------------
+constexpr int SMALL_TPB = 128;
+constexpr int SMALL_WARPS = SMALL_TPB / 32;
+
+__global__ void __launch_bounds__(SMALL_TPB) s2m_warp_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                             const double *__restrict__ cx,
+                                                             const double *__restrict__ cy,
+                                                             const double *__restrict__ cz, int32_t box0,
+                                                             int32_t box1, const double *__restrict__ ks,
+                                                             int64_t K, double2 *__restrict__ M) {
+  __shared__ double2 tab[TAB];
+  __shared__ double wx[SMALL_WARPS][32], wy[SMALL_WARPS][32], wz[SMALL_WARPS][32];
+  __shared__ double2 wq[SMALL_WARPS][32];
+  fill_exp_table(tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * SMALL_WARPS;
+  for (int64_t b = box0 + (int64_t)blockIdx.x * SMALL_WARPS + warp; b < box1; b += nwarps) {
+    const int64_t s0 = first[b], s1 = first[b + 1];
+    const double c0x = cx[b], c0y = cy[b], c0z = cz[b];
+    const bool one_chunk = s1 - s0 <= 32;
+    for (int64_t k0 = 0; k0 < K; k0 += 64) {
+      const int64_t ka = k0 + lane, kb = ka + 32;
+      const double kxa = ka < K ? ks[ka] : 0.0, kya = ka < K ? ks[K + ka] : 0.0, kza = ka < K ? ks[2 * K + ka] : 0.0;
+      const double kxb = kb < K ? ks[kb] : 0.0, kyb = kb < K ? ks[K + kb] : 0.0, kzb = kb < K ? ks[2 * K + kb] : 0.0;
+      double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+      for (int64_t j0 = s0; j0 < s1; j0 += 32) {
+        const int cnt = (int)min((int64_t)32, s1 - j0);
+        if (!one_chunk || k0 == 0) {
+          __syncwarp();
+          if (lane < cnt) {
+            const int64_t j = j0 + lane;
+            wx[warp][lane] = pts.x[j] - c0x;
+            wy[warp][lane] = pts.y[j] - c0y;
+            wz[warp][lane] = pts.z[j] - c0z;
+            wq[warp][lane] = pts.q[j];
+          }
+          __syncwarp();
+        }
+#pragma unroll 2
+        for (int u = 0; u < cnt; ++u) {
+          const double dx = wx[warp][u], dy = wy[warp][u], dz = wz[warp][u];
+          const double2 q = wq[warp][u];
+          const double2 ea = cexpi_u(fma(kxa, dx, fma(kya, dy, kza * dz)), tab);
+          ar = fma(ea.x, q.x, fma(-ea.y, q.y, ar));
+          ai = fma(ea.x, q.y, fma(ea.y, q.x, ai));
+          const double2 eb = cexpi_u(fma(kxb, dx, fma(kyb, dy, kzb * dz)), tab);
+          br = fma(eb.x, q.x, fma(-eb.y, q.y, br));
+          bi = fma(eb.x, q.y, fma(eb.y, q.x, bi));
+        }
+      }
+      if (ka < K) M[b * K + ka] = make_double2(ar, ai);
+      if (kb < K) M[b * K + kb] = make_double2(br, bi);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(SMALL_TPB) l2t_warp_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                             const double *__restrict__ cx,
+                                                             const double *__restrict__ cy,
+                                                             const double *__restrict__ cz, int32_t box0,
+                                                             int32_t box1, const double *__restrict__ ks,
+                                                             int64_t K, const double2 *__restrict__ L, double w,
+                                                             double2 *__restrict__ y_far) {
+  __shared__ double2 tab[TAB];
+  fill_exp_table(tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * SMALL_WARPS;
+  for (int64_t b = box0 + (int64_t)blockIdx.x * SMALL_WARPS + warp; b < box1; b += nwarps) {
+    const int64_t s0 = first[b], s1 = first[b + 1];
+    const int64_t nb = s1 - s0;
+    int P = 1;
+    while (P < nb && P < 32) P <<= 1;
+    const int S = 32 / P, slice = lane / P;
+    const double ccx = cx[b], ccy = cy[b], ccz = cz[b];
+    const double2 *Lb = L + b * K;
+    for (int64_t p0 = s0; p0 < s1; p0 += P) {
+      const int64_t i = p0 + (lane & (P - 1));
+      const bool valid = i < s1;
+      const double dx = valid ? ccx - pts.x[i] : 0.0, dy = valid ? ccy - pts.y[i] : 0.0,
+                   dz = valid ? ccz - pts.z[i] : 0.0;   // c_a - x_i
+      double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+      for (int64_t k = slice; k < K; k += 2 * S) {
+        {
+          const double2 l = Lb[k];
+          const double2 e = cexpi_u(fma(ks[k], dx, fma(ks[K + k], dy, ks[2 * K + k] * dz)), tab);
+          ar = fma(e.x, l.x, fma(-e.y, l.y, ar));
+          ai = fma(e.x, l.y, fma(e.y, l.x, ai));
+        }
+        const int64_t k2 = k + S;
+        if (k2 < K) {
+          const double2 l = Lb[k2];
+          const double2 e = cexpi_u(fma(ks[k2], dx, fma(ks[K + k2], dy, ks[2 * K + k2] * dz)), tab);
+          br = fma(e.x, l.x, fma(-e.y, l.y, br));
+          bi = fma(e.x, l.y, fma(e.y, l.x, bi));
+        }
+      }
+      ar += br, ai += bi;
+      for (int off = P; off < 32; off <<= 1) {
+        ar += __shfl_xor_sync(0xffffffffu, ar, off);
+        ai += __shfl_xor_sync(0xffffffffu, ai, off);
+      }
+      if (slice == 0 && valid) y_far[i] = make_double2(w * ar, w * ai);
+    }
+  }
+}
+
+static unsigned persistent_grid(int64_t nbox, const void *fn) {
+  int per_sm = 0, dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SMALL_TPB, 0);
+  const int64_t need = (nbox + SMALL_WARPS - 1) / SMALL_WARPS;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)nsm * std::max(per_sm, 1)));
+}
+
+void launch_s2m_small(PointsDev pts, const int64_t *first, const double *cx, const double *cy, const double *cz,
+                      int32_t box0, int32_t box1, const double *ks, int64_t K, double2 *M, cudaStream_t s) {
+  if (box1 <= box0) return;
+  s2m_warp_kernel<<<persistent_grid(box1 - box0, (const void *)s2m_warp_kernel), SMALL_TPB, 0, s>>>(
+      pts, first, cx, cy, cz, box0, box1, ks, K, M);
+}
+
+void launch_l2t_small(PointsDev pts, const int64_t *first, const double *cx, const double *cy, const double *cz,
+                      int32_t box0, int32_t box1, const double *ks, int64_t K, const double2 *L, double w,
+                      double2 *y_far, cudaStream_t s) {
+  if (box1 <= box0) return;
+  l2t_warp_kernel<<<persistent_grid(box1 - box0, (const void *)l2t_warp_kernel), SMALL_TPB, 0, s>>>(
+      pts, first, cx, cy, cz, box0, box1, ks, K, L, w, y_far);
+}
+
+// ---------------------------------------------------------------------------------------------
 __global__ void permute_kernel(const double2 *__restrict__ q_in, const int64_t *__restrict__ perm,
                                double2 *__restrict__ q_sorted, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

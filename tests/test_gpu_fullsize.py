@@ -2,7 +2,8 @@
 library path bench.py times, on outputs the oracle can compute one by one:
   - the integer plan (ell, N_theta, N_phi, L_f) equals the oracle's
   - transfer tables for sampled offsets equal the oracle's Alg. 1 (1e-12)
-  - S2M expansions of sampled leaves equal the oracle's (1e-11)
+  - the source level D_s and the translation-only grids equal the oracle's (R-14)
+  - S2M expansions of sampled source-level boxes equal the oracle's (1e-11)
   - near-field sums of sampled targets equal the oracle's P2P (1e-11)
   - sampled y_i agree with the direct sum within eps (relative L2 over the sample)
 """
@@ -12,7 +13,7 @@ import numpy as np
 import pytest
 
 from workloads import CONFIGS, points_and_charges, sample_indices
-from oracle.plan import make_plan, level_params
+from oracle.plan import make_plan, level_params, rep_grid, choose_source_level
 from oracle.direct import direct_sum
 from oracle.transfer import bmtf_table, offsets316
 from oracle.tree import build_level
@@ -56,8 +57,12 @@ def run(hf, name):
 def test_fullsize_plan_and_accuracy(hf, name):
     cfg, x, q, g, y = run(hf, name)
     info = g.info()
-    # integer plan of every level vs the oracle's level rule
+    # integer plan of every level vs the oracle's level rules (translation-only levels: R-14)
+    assert info["source_level"] == choose_source_level(x, cfg.lo, cfg.size, cfg.depth, info["L_f"])
     for lv in info["levels"]:
+        if lv["rep"]:
+            assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (0,) + rep_grid(cfg.kappa, lv["a"], cfg.eps)
+            continue
         ell, nth, nph, _ = level_params(cfg.kappa, lv["a"], cfg.eps, lv["alpha"])
         assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (ell, nth, nph), lv["level"]
     # sampled targets vs direct summation (eqn:HelmholtzMatrixVector)
@@ -85,13 +90,14 @@ def test_fullsize_stage_samples(hf, name):
     for oid in (3, 150, 310):
         ref = bmtf_table(lv[2]["ell"], cfg.kappa, offs[oid] * lv[2]["a"], lv[2]["n_theta"], lv[2]["n_phi"]).reshape(-1)
         assert rel(T[oid], ref) <= 1e-12
-    # oracle tree at L_f (its own), same plan integers
-    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
+    # S2M at the source level D_s: oracle tree (its own), same plan integers
+    Ds = info["source_level"]
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=Ds)
     f = OracleFMM(x, cfg.lo, cfg.size, plan)
-    lev = f.levels[L]
-    tab = g.debug(7, L)
+    lev = f.levels[Ds]
+    tab = g.debug(7, Ds)
     gpu_index = {(int(r[0]), int(r[1]), int(r[2])): b for b, r in enumerate(tab)}
-    Mg = g.debug(0, L).reshape(len(tab), -1)
+    Mg = g.debug(0, Ds).reshape(len(tab), -1)
     rng = np.random.default_rng(1)
     for ob in rng.choice(len(lev.boxes), size=2, replace=False):
         Mo = f.s2m(q, boxes=[ob])[ob]

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from workloads import CONFIGS, small_config, points_and_charges
-from oracle.plan import make_plan
+from oracle.plan import make_plan, choose_source_level
 from oracle.fmm import OracleFMM
 from oracle.direct import direct_sum
 from oracle.transfer import bmtf_table, offsets316
@@ -46,9 +46,11 @@ def gpu_plan(hf, cfg, x, **kw):
 def check_plan(g, plan):
     info = g.info()
     assert info["L_f"] == plan.L_f
+    assert info["source_level"] == plan.source_level
     for lv in info["levels"]:
         op = plan.levels[lv["level"]]
         assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (op.ell, op.n_theta, op.n_phi), lv["level"]
+        assert lv["rep"] == op.rep, lv["level"]
         assert lv["alpha"] == op.alpha, lv["level"]
         if lv["level"] <= (plan.L_f or 1) + 1 and not math.isnan(op.F):
             assert lv["active"] == op.active
@@ -91,8 +93,64 @@ def small(hf):
 
 def test_small_plan_identical(small):
     cfg, x, q, plan, f, g, y = small
-    assert plan.L_f == 3
+    assert plan.L_f == 3 and plan.source_level == 3
     check_plan(g, plan)
+
+
+# ---- translation-only levels below L_f (R-14) -------------------------------------
+@pytest.fixture(scope="module")
+def deep(hf):
+    cfg = small_config("deep", n=3000, kappa=16 * math.pi, depth=5, eps=1e-6, seed=5)
+    x, q = points_and_charges(cfg)
+    g = gpu_plan(hf, cfg, x, flags=hf.HFMM_SOURCE_AT_DEPTH)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=cfg.depth)
+    f = OracleFMM(x, cfg.lo, cfg.size, plan)
+    y = g.matvec(q)
+    return cfg, x, q, plan, f, g, y
+
+
+def test_deep_plan_identical(deep):
+    cfg, x, q, plan, f, g, y = deep
+    assert plan.L_f == 2 and plan.source_level == 5
+    check_plan(g, plan)
+
+
+def test_deep_stages(deep):
+    """M, L at every level 2..D_s (translation-only levels 3..5), I at the active level."""
+    cfg, x, q, plan, f, g, y = deep
+    M, I, Lloc = f.far_locals(q)
+    for l in range(2, plan.source_level + 1):
+        mp = box_map(g, f, l)
+        K = plan.levels[l].K
+        Mg = g.debug(0, l).reshape(-1, K)
+        assert rel(Mg, np.stack([M[l][mp[b]] for b in range(len(mp))])) <= PARITY, f"M_{l}"
+        Lg = g.debug(2, l).reshape(-1, K)
+        assert rel(Lg, np.stack([Lloc[l][mp[b]] for b in range(len(mp))])) <= PARITY, f"L_{l}"
+
+
+def test_deep_matvec_parity_and_accuracy(deep):
+    cfg, x, q, plan, f, g, y = deep
+    assert rel(y, f.matvec(q)) <= PARITY
+    assert rel(y, direct_sum(x, q, cfg.kappa)) <= cfg.eps
+
+
+def test_default_source_level_policy(hf):
+    """Default policy (no flag) picks the oracle's choose_source_level; result still parity-green."""
+    cfg = small_config("pol", n=6000, kappa=16 * math.pi, depth=5, eps=1e-6, seed=9)
+    x, q = points_and_charges(cfg)
+    g = gpu_plan(hf, cfg, x)
+    info = g.info()
+    Ds = choose_source_level(x, cfg.lo, cfg.size, cfg.depth, info["L_f"])
+    assert info["source_level"] == Ds and Ds > info["L_f"]
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=Ds)
+    check_plan(g, plan)
+    t = np.arange(0, cfg.n, 5)
+    y = g.matvec(q)
+    assert rel(y[t], OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q, t)) <= PARITY
+    # the paper's setup (S2M at L_f) agrees with the translation-only route within eps / 10
+    g0 = gpu_plan(hf, cfg, x, flags=hf.HFMM_SOURCE_AT_LF)
+    assert g0.info()["source_level"] == info["L_f"]
+    assert rel(g0.matvec(q), y) <= cfg.eps / 10
 
 
 def test_small_transfer_tables(small):

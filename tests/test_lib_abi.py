@@ -67,6 +67,15 @@ def test_host_plan_equals_oracle_plan(ka, eps):
     assert g[3] == o[3]          # ragged per-row N_phi(theta_n) too
 
 
+@pytest.mark.parametrize("ka,a,eps", [(32 * math.pi, 2 / 128, 1e-8), (32 * math.pi, 2 / 16, 1e-8),
+                                      (128 * math.pi, 1 / 64, 1e-6), (16 * math.pi, 2 / 32, 1e-6),
+                                      (5.0, 0.5, 1e-4), (1e-3, 0.01, 1e-12), (300.0, 0.5, 1e-10)])
+def test_host_rep_grid_equals_oracle(ka, a, eps):
+    """Translation-only grid rule (R-14) of the library == the oracle's (independent code)."""
+    from oracle.plan import rep_grid
+    assert hf.rep_grid(ka, a, eps) == rep_grid(ka, a, eps)
+
+
 def test_plan_rejects_bad_args():
     with pytest.raises(hf.HFMMError):
         hf.level_quadrature(-1.0, 1.0, 1e-6, 0.8)
