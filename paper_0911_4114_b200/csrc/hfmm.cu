@@ -24,7 +24,7 @@ namespace {
 
 const double kPi = 3.14159265358979323846;
 const double kURound = 1.1102230246251565e-16;  // 2^-53
-const int64_t kTile = 256;                       // targets per P2P / L2T tile (2 per thread)
+const int64_t kTile = 256;                       // targets per L2T tile (2 per thread)
 
 struct LevelDev {
   int l = 0;
@@ -117,7 +117,7 @@ struct hfmm_plan {
   int64_t *dir_items = nullptr;
   int64_t dir_nitems = 0;
   double *ux = nullptr, *uy = nullptr, *uz = nullptr;
-  double uscale = 0;               // kappa TAB / (2 pi)
+  double uscale = 0;               // kappa TAB_STEPS / (2 pi)
   int64_t p2p_sym_pairs = 0;
   double dummy_t[3] = {0, 0, 0}, dummy_s[3] = {0, 0, 0};
   double2 *tmp = nullptr;
@@ -595,7 +595,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       ux[i] = t.xs[i] * p->uscale, uy[i] = t.ys[i] * p->uscale, uz[i] = t.zs[i] * p->uscale;
     p->ux = dupload(ux), p->uy = dupload(uy), p->uz = dupload(uz);
     // Owned target ranges: owned near-level boxes (far field), or the rank's point range of the
-    // root (no far field).  Every target tile (<= kTile points of one box) gets
+    // root (no far field).  Every target tile (<= P2P_TILE points of one box) gets
     //   DIAG (tile, tile);  SYM (tile, later tile of the same box);
     //   SYM (tile, owned neighbour box beta > alpha);  ORD (tile, neighbour range owned elsewhere).
     std::vector<int64_t> it[3];
@@ -607,10 +607,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     auto own_box = [&](int64_t A0, int64_t A1, const std::vector<std::pair<int64_t, int64_t>> &others_owned,
                        const std::vector<std::pair<int64_t, int64_t>> &others_foreign) {
       // targets [A0, A1) of one owned box; others_* = neighbour ranges (sym: only beta > alpha)
-      for (int64_t t0 = A0; t0 < A1; t0 += kTile) {
-        const int64_t t1 = std::min(t0 + kTile, A1);
+      for (int64_t t0 = A0; t0 < A1; t0 += P2P_TILE) {
+        const int64_t t1 = std::min(t0 + P2P_TILE, A1);
         add(P2P_DIAG, t0, t1, t0, t1);
-        for (int64_t u0 = t1; u0 < A1; u0 += kTile) add(P2P_SYM, t0, t1, u0, std::min(u0 + kTile, A1));
+        for (int64_t u0 = t1; u0 < A1; u0 += P2P_TILE) add(P2P_SYM, t0, t1, u0, std::min(u0 + P2P_TILE, A1));
         for (auto &r : others_owned) add(P2P_SYM, t0, t1, r.first, r.second);
         for (auto &r : others_foreign) add(P2P_ORD, t0, t1, r.first, r.second);
       }
@@ -662,7 +662,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     // hfmm_direct: every target tile against all points (self pair masked)
     {
       std::vector<int64_t> d;
-      for (int64_t t0 = 0; t0 < t.n; t0 += kTile) d.insert(d.end(), {t0, std::min(t0 + kTile, t.n), 0, t.n});
+      for (int64_t t0 = 0; t0 < t.n; t0 += P2P_TILE) d.insert(d.end(), {t0, std::min(t0 + P2P_TILE, t.n), 0, t.n});
       p->dir_items = dupload(d);
       p->dir_nitems = (int64_t)d.size() / 4;
     }

@@ -69,7 +69,8 @@ __device__ __forceinline__ double rsqrt_fast(double r2) {
 //   symmetric disjoint ranges: each unordered pair evaluated once, G q_j added to y_i (rows, in
 //             registers) and G q_i to y_j (columns: systolic warp reduction, below)
 // ---------------------------------------------------------------------------------------------
-constexpr int P2P_TPB = 128;
+constexpr int P2P_TPB = P2P_THREADS;
+constexpr int PT = P2P_T;  // targets per thread (tile = PT * P2P_TPB)
 
 __device__ __forceinline__ double2 green_u(double tx, double ty, double tz, double xs, double ys, double zs,
                                            const double2 *tab) {
@@ -90,11 +91,14 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU
   fill_exp_table(tab);
   const int64_t *it = items + 4 * (int64_t)blockIdx.x;
   const int64_t t1 = it[1], s0 = it[2], s1 = it[3];
-  const int64_t i0 = it[0] + threadIdx.x, i1 = i0 + P2P_TPB;
-  // inactive lanes evaluate far-away dummy targets (results discarded)
-  const double x0 = i0 < t1 ? pts.ux[i0] : 1e30, y0 = i0 < t1 ? pts.uy[i0] : 0.0, z0 = i0 < t1 ? pts.uz[i0] : 0.0;
-  const double x1 = i1 < t1 ? pts.ux[i1] : 1e30, y1 = i1 < t1 ? pts.uy[i1] : 0.0, z1 = i1 < t1 ? pts.uz[i1] : 0.0;
-  double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
+  double tx[PT], ty[PT], tz[PT], ar[PT], ai[PT];
+#pragma unroll
+  for (int p = 0; p < PT; ++p) {
+    const int64_t i = it[0] + threadIdx.x + p * P2P_TPB;
+    // inactive lanes evaluate far-away dummy targets (results discarded)
+    tx[p] = i < t1 ? pts.ux[i] : 1e30, ty[p] = i < t1 ? pts.uy[i] : 0.0, tz[p] = i < t1 ? pts.uz[i] : 0.0;
+    ar[p] = ai[p] = 0.0;
+  }
   for (int64_t c0 = s0; c0 < s1; c0 += P2P_TPB) {
     const int cnt = (int)min((int64_t)P2P_TPB, s1 - c0);
     __syncthreads();
@@ -110,37 +114,32 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU
     for (int u = 0; u < cnt; ++u) {
       const double xs = sx[u], ys = sy[u], zs = sz[u];
       const double2 q = sq[u];
-      {
-        const double dx = x0 - xs, dy = y0 - ys, dz = z0 - zs;
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        const double dx = tx[p] - xs, dy = ty[p] - ys, dz = tz[p] - zs;
         const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
         double ri = rsqrt_fast(r2);
         if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;  // self pair excluded
         const double2 e = cexpi_u(r2 * ri, tab);
         const double gr = e.x * ri, gi = e.y * ri;
-        a0r = fma(gr, q.x, fma(-gi, q.y, a0r));
-        a0i = fma(gr, q.y, fma(gi, q.x, a0i));
-      }
-      {
-        const double dx = x1 - xs, dy = y1 - ys, dz = z1 - zs;
-        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-        double ri = rsqrt_fast(r2);
-        if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;
-        const double2 e = cexpi_u(r2 * ri, tab);
-        const double gr = e.x * ri, gi = e.y * ri;
-        a1r = fma(gr, q.x, fma(-gi, q.y, a1r));
-        a1i = fma(gr, q.y, fma(gi, q.x, a1i));
+        ar[p] = fma(gr, q.x, fma(-gi, q.y, ar[p]));
+        ai[p] = fma(gr, q.y, fma(gi, q.x, ai[p]));
       }
     }
   }
   // y_near is zeroed before the P2P launches; every item adds into its target rows
-  if (i0 < t1) atomicAdd(&y_near[i0].x, scale * a0r), atomicAdd(&y_near[i0].y, scale * a0i);
-  if (i1 < t1) atomicAdd(&y_near[i1].x, scale * a1r), atomicAdd(&y_near[i1].y, scale * a1i);
+#pragma unroll
+  for (int p = 0; p < PT; ++p) {
+    const int64_t i = it[0] + threadIdx.x + p * P2P_TPB;
+    if (i < t1) atomicAdd(&y_near[i].x, scale * ar[p]), atomicAdd(&y_near[i].y, scale * ai[p]);
+  }
 }
 
 // Symmetric item: column sums use a systolic warp reduction -- in a block of 32 sources, lane t
 // processes source (t + u) mod 32 at step u and passes the running column accumulator to lane
 // t - 1, so after 32 steps lane t holds the warp sum of source t (2 shuffles per step instead of
 // a 5-level butterfly per source); the 4 warps combine in shared memory, one atomic per source.
+// Each source loaded from shared memory serves PT targets of the lane.
 __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU pts,
                                                                         const int64_t *__restrict__ items,
                                                                         double scale, double3 dummy_t,
@@ -154,13 +153,17 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t *it = items + 4 * (int64_t)blockIdx.x;
   const int64_t t1 = it[1], s0 = it[2], s1 = it[3];
-  const int64_t i0 = it[0] + threadIdx.x, i1 = i0 + P2P_TPB;
-  const bool v0 = i0 < t1, v1 = i1 < t1;
-  // inactive targets: far dummy position, zero charge (their column contributions vanish)
-  const double x0 = v0 ? pts.ux[i0] : dummy_t.x, y0 = v0 ? pts.uy[i0] : dummy_t.y, z0 = v0 ? pts.uz[i0] : dummy_t.z;
-  const double x1 = v1 ? pts.ux[i1] : dummy_t.x, y1 = v1 ? pts.uy[i1] : dummy_t.y, z1 = v1 ? pts.uz[i1] : dummy_t.z;
-  const double2 q0 = v0 ? pts.q[i0] : make_double2(0.0, 0.0), q1 = v1 ? pts.q[i1] : make_double2(0.0, 0.0);
-  double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
+  double tx[PT], ty[PT], tz[PT], ar[PT], ai[PT];
+  double2 tq[PT];
+#pragma unroll
+  for (int p = 0; p < PT; ++p) {
+    const int64_t i = it[0] + threadIdx.x + p * P2P_TPB;
+    const bool v = i < t1;
+    // inactive targets: far dummy position, zero charge (their column contributions vanish)
+    tx[p] = v ? pts.ux[i] : dummy_t.x, ty[p] = v ? pts.uy[i] : dummy_t.y, tz[p] = v ? pts.uz[i] : dummy_t.z;
+    tq[p] = v ? pts.q[i] : make_double2(0.0, 0.0);
+    ar[p] = ai[p] = 0.0;
+  }
   for (int64_t c0 = s0; c0 < s1; c0 += P2P_TPB) {
     const int cnt = (int)min((int64_t)P2P_TPB, s1 - c0);
     __syncthreads();
@@ -183,16 +186,14 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
         const int s = base + ((lane + u) & 31);
         const double xs = sx[s], ys = sy[s], zs = sz[s];
         const double2 qs = sq[s];
-        const double2 g0 = green_u(x0, y0, z0, xs, ys, zs, tab);
-        const double2 g1 = green_u(x1, y1, z1, xs, ys, zs, tab);
-        a0r = fma(g0.x, qs.x, fma(-g0.y, qs.y, a0r));
-        a0i = fma(g0.x, qs.y, fma(g0.y, qs.x, a0i));
-        a1r = fma(g1.x, qs.x, fma(-g1.y, qs.y, a1r));
-        a1i = fma(g1.x, qs.y, fma(g1.y, qs.x, a1i));
-        cr = fma(g0.x, q0.x, fma(-g0.y, q0.y, cr));
-        ci = fma(g0.x, q0.y, fma(g0.y, q0.x, ci));
-        cr = fma(g1.x, q1.x, fma(-g1.y, q1.y, cr));
-        ci = fma(g1.x, q1.y, fma(g1.y, q1.x, ci));
+#pragma unroll
+        for (int p = 0; p < PT; ++p) {
+          const double2 g = green_u(tx[p], ty[p], tz[p], xs, ys, zs, tab);
+          ar[p] = fma(g.x, qs.x, fma(-g.y, qs.y, ar[p]));
+          ai[p] = fma(g.x, qs.y, fma(g.y, qs.x, ai[p]));
+          cr = fma(g.x, tq[p].x, fma(-g.y, tq[p].y, cr));
+          ci = fma(g.x, tq[p].y, fma(g.y, tq[p].x, ci));
+        }
         cr = __shfl_sync(0xffffffffu, cr, (lane + 1) & 31);   // accumulator follows its source
         ci = __shfl_sync(0xffffffffu, ci, (lane + 1) & 31);
       }
@@ -207,8 +208,11 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
       atomicAdd(&y_near[c0 + threadIdx.x].y, scale * sum.y);
     }
   }
-  if (v0) atomicAdd(&y_near[i0].x, scale * a0r), atomicAdd(&y_near[i0].y, scale * a0i);
-  if (v1) atomicAdd(&y_near[i1].x, scale * a1r), atomicAdd(&y_near[i1].y, scale * a1i);
+#pragma unroll
+  for (int p = 0; p < PT; ++p) {
+    const int64_t i = it[0] + threadIdx.x + p * P2P_TPB;
+    if (i < t1) atomicAdd(&y_near[i].x, scale * ar[p]), atomicAdd(&y_near[i].y, scale * ai[p]);
+  }
 }
 
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
