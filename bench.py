@@ -395,7 +395,7 @@ def main():
         except Exception:
             traffic = None
     L_f = info["L_f"]
-    launches = 3 + (0 if L_f is None else (1 + 2 * (L_f - 2) + (L_f - 1) + 2 * (L_f - 2) + 1))
+    launches = info["launches"]                  # counted by libhfmm for one matvec (hfmm_info.launches)
     line = {
         "metric": "FMM matvecs/s", "value": 1e3 / ms, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",

@@ -108,6 +108,7 @@ typedef struct {
   int rank, nranks;
   int64_t owned_points;    /* points whose y this rank computes                              */
   int source_level;        /* D_s: level of S2M / L2T (R-14), -1 if no far field             */
+  int launches;            /* libhfmm kernel launches per matvec (this rank)                 */
 } hfmm_info;
 
 /* Create a plan on CUDA device `device` (-1: the current device).  *out receives the plan. */

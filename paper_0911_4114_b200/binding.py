@@ -50,7 +50,7 @@ class Info(C.Structure):
                 ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("p2p_sym_pairs", C.c_int64),
                 ("s2m_evals", C.c_int64),
                 ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64),
-                ("source_level", C.c_int)]
+                ("source_level", C.c_int), ("launches", C.c_int)]
 
 
 class HFMMError(RuntimeError):
@@ -241,7 +241,7 @@ class HFMM:
                     eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
                     p2p_sym_pairs=inf.p2p_sym_pairs,
                     s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points,
-                    source_level=(None if inf.source_level < 0 else inf.source_level))
+                    source_level=(None if inf.source_level < 0 else inf.source_level), launches=inf.launches)
 
     def stage_times(self):
         out = (C.c_double * 8)()

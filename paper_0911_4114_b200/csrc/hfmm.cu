@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -40,9 +41,10 @@ struct LevelDev {
   std::vector<int64_t> rlo, rhi; // every rank's owned range (for the all-gather)
   double *cx = nullptr, *cy = nullptr, *cz = nullptr;
   double *ks = nullptr;          // kappa s [3][K]
-  double2 *T = nullptr;          // [316][K]
+  double2 *T = nullptr;          // [34][K]: the canonical transfer vectors x >= y >= 0, z >= 0
+  int32_t *perm = nullptr;       // [16][K]: grid permutation of each reflection / swap op (NEXT 3)
   double2 *M = nullptr, *I = nullptr, *L = nullptr;  // [nbox][K]
-  int32_t *il_row = nullptr, *il_src = nullptr, *il_oid = nullptr;
+  int32_t *il_row = nullptr, *il_src = nullptr, *il_sym = nullptr;  // il_sym = canonical id << 4 | op
   int64_t il_nnz = 0;
   int32_t *parent = nullptr;     // into level l-1
   int8_t *oct = nullptr;         // octant of the box inside its parent
@@ -151,7 +153,7 @@ static thread_local std::string g_create_err;
 static void free_levels(hfmm_plan *p) {
   for (auto &L : p->lv) {
     for (void *ptr : {(void *)L.cx, (void *)L.cy, (void *)L.cz, (void *)L.ks, (void *)L.T, (void *)L.M,
-                      (void *)L.I, (void *)L.L, (void *)L.il_row, (void *)L.il_src, (void *)L.il_oid,
+                      (void *)L.I, (void *)L.L, (void *)L.il_row, (void *)L.il_src, (void *)L.il_sym, (void *)L.perm,
                       (void *)L.parent, (void *)L.oct, (void *)L.cbeg, (void *)L.shift})
       if (ptr) cudaFree(ptr);
   }
@@ -268,14 +270,18 @@ extern "C" int hfmm_build_tree(hfmm_plan *p, int64_t n, const double *xyz, int d
 
 // ---- precompute helpers ---------------------------------------------------------------------
 static int level_tables(hfmm_plan *p, LevelDev &L, double2 **T_out, double *F_out) {
-  // Alg. 1 for the 316 offsets on the GPU; c_n per distinct |r0| from the host.
+  // Alg. 1 for the 34 canonical offsets on the GPU; c_n per distinct |r0| from the host.
+  std::vector<int> cids, sym_of;
+  canonical_offsets(cids, sym_of);
+  const int NC = (int)cids.size();
   std::vector<double2> coef;
-  std::vector<int32_t> coef_of(316);
-  std::vector<double> r0hat(316 * 3);
+  std::vector<int32_t> coef_of(NC);
+  std::vector<double> r0hat(NC * 3);
   std::map<int, int> by_norm2;
-  for (int id = 0; id < 316; ++id) {
+  for (int ci = 0; ci < NC; ++ci) {
+    const int id = ci;  // row of the canonical table set
     int o[3];
-    offset_vec(id, o);
+    offset_vec(cids[ci], o);
     int n2 = o[0] * o[0] + o[1] * o[1] + o[2] * o[2];
     auto it = by_norm2.find(n2);
     if (it == by_norm2.end()) {
@@ -301,27 +307,27 @@ static int level_tables(hfmm_plan *p, LevelDev &L, double2 **T_out, double *F_ou
   double2 *dcoef = dupload(coef);
   int32_t *dcof = dupload(coef_of);
   double *dr0 = dupload(r0hat);
-  double2 *T = dalloc<double2>((size_t)316 * L.K);
+  double2 *T = dalloc<double2>((size_t)NC * L.K);
   if (!dcoef || !dcof || !dr0 || !T) {
     p->err = "precompute: allocation failed (transfer tables)";
     return HFMM_E_NOMEM;
   }
   if (L.nph >= 2 * L.ell + 2) {
-    launch_alg1_tables(dcoef, dcof, dr0, L.ell, L.nth, L.nph, L.nph / 2, T, p->stream);
+    launch_alg1_tables(dcoef, dcof, dr0, NC, L.ell, L.nth, L.nph, L.nph / 2, T, p->stream);
   } else {
     const int nphf = 2 * L.ell + 2;
-    double2 *full = dalloc<double2>((size_t)316 * L.nth * nphf);
+    double2 *full = dalloc<double2>((size_t)NC * L.nth * nphf);
     if (!full) {
       p->err = "precompute: allocation failed (phi-fine tables)";
       return HFMM_E_NOMEM;
     }
-    launch_alg1_tables(dcoef, dcof, dr0, L.ell, L.nth, nphf, nphf, full, p->stream);
-    launch_phi_anterp(full, L.nth, nphf, L.nph, T, p->stream);
+    launch_alg1_tables(dcoef, dcof, dr0, NC, L.ell, L.nth, nphf, nphf, full, p->stream);
+    launch_phi_anterp(full, NC, L.nth, nphf, L.nph, T, p->stream);
     CK(cudaStreamSynchronize(p->stream));
     cudaFree(full);
   }
   double *dmax = dalloc<double>(1);
-  launch_absmax(T, (int64_t)316 * L.K, dmax, p->stream);
+  launch_absmax(T, (int64_t)NC * L.K, dmax, p->stream);  // = max over all 316 (reflections)
   double mx = 0;
   CK(cudaMemcpyAsync(&mx, dmax, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
@@ -533,6 +539,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     }
     // interaction lists for every box of an active level
     std::vector<int32_t> row(1, 0), src, oid;
+    std::vector<int> cids, sym_of;
+    canonical_offsets(cids, sym_of);
     for (int64_t b = 0; b < (L.active ? B.nbox() : 0); ++b) {
       const int px = B.ix[b] >> 1, py = B.iy[b] >> 1, pz = B.iz[b] >> 1;
       for (int dx = -3; dx <= 3; ++dx)
@@ -545,12 +553,17 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
             int32_t k = B.find(x, y, z);
             if (k < 0) continue;
             src.push_back(k);
-            oid.push_back(offset_id(dx, dy, dz));
+            oid.push_back(sym_of[offset_id(dx, dy, dz)]);
           }
       row.push_back((int32_t)src.size());
     }
     L.il_nnz = (int64_t)src.size();
-    L.il_row = dupload(row), L.il_src = dupload(src), L.il_oid = dupload(oid);
+    L.il_row = dupload(row), L.il_src = dupload(src), L.il_sym = dupload(oid);
+    if (L.active) {
+      std::vector<int32_t> pm;
+      symmetry_perms(L.nth, L.nph, pm);
+      L.perm = dupload(pm);
+    }
     // tree links
     std::vector<int32_t> par(B.parent.begin(), B.parent.end());
     std::vector<int8_t> oc(B.nbox());
@@ -709,6 +722,16 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   }
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
   in.source_level = p->D_s;
+  {  // kernel launches of one matvec (run_matvec): permute, P2P kinds, far chain, combine
+    int nl = 2;
+    for (int k = 0; k < 3; ++k) nl += p->p2p_nitems[k] > 0 ? 1 : 0;
+    if (p->L_f >= 2) {
+      for (int l = p->D_s; l > 2; --l) nl += 2;   // M2M: rows + cols pass per level
+      for (int l = 2; l < p->D_s; ++l) nl += 2;   // L2L: cols + rows pass per level
+      nl += 2 + (p->L_f - 1);                      // S2M, L2T, M2L per active level
+    }
+    in.launches = nl;
+  }
   in.owned_points = p->own_pt1 - p->own_pt0;
   p->have_plan = true;
   if (p->L_f < 0) {
@@ -783,7 +806,7 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
     if (prof) cudaEventRecord(p->sev[2], s);
     for (int l = 2; l <= Lf; ++l) {  // M2L
       LevelDev &L = p->lv[l];
-      launch_m2l((int32_t)L.own0, (int32_t)L.own1, L.K, L.il_row, L.il_src, L.il_oid, L.T, L.M, L.I, s);
+      launch_m2l_sym((int32_t)L.own0, (int32_t)L.own1, L.K, L.il_row, L.il_src, L.il_sym, L.perm, L.T, L.M, L.I, s);
     }
     if (prof) cudaEventRecord(p->sev[3], s);
     for (int l = 2; l < Ds; ++l) {  // L2L; L_2 = I_2; I = 0 below L_f (R-14)
@@ -919,7 +942,25 @@ extern "C" int hfmm_debug_copy(const hfmm_plan *p, int what, int level, void *ho
       return HFMM_E_ARG;
     const LevelDev &L = p->lv[level];
     if (what == 3) {
-      src = L.T, bytes = (int64_t)316 * L.K * 16;
+      // the 316 tables T_o[k] = T_c(o)[perm_op(o)[k]], expanded from the 34 canonical ones
+      bytes = (int64_t)316 * L.K * 16;
+      if (needed) *needed = bytes;
+      if (!host_out) return HFMM_OK;
+      if (nbytes < bytes) return HFMM_E_ARG;
+      if (!L.T || !L.perm) return HFMM_E_STATE;
+      std::vector<int> cids, sym_of;
+      canonical_offsets(cids, sym_of);
+      std::vector<double2> T34((size_t)cids.size() * L.K);
+      std::vector<int32_t> pm((size_t)16 * L.K);
+      if (cudaMemcpy(T34.data(), L.T, T34.size() * 16, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(pm.data(), L.perm, pm.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return HFMM_E_CUDA;
+      double2 *dst = (double2 *)host_out;
+      for (int id = 0; id < 316; ++id) {
+        const int c = sym_of[id] >> 4, op = sym_of[id] & 15;
+        for (int64_t k = 0; k < L.K; ++k) dst[(size_t)id * L.K + k] = T34[(size_t)c * L.K + pm[(size_t)op * L.K + k]];
+      }
+      return HFMM_OK;
     } else {
       const double2 *b = what == 0 ? L.M : what == 1 ? L.I : (level == 2 ? L.I : L.L);
       src = b, bytes = L.nbox * L.K * 16;

@@ -63,6 +63,11 @@ void partition_level2(const Tree &t, int L_f, int64_t K, int R, std::vector<int6
 // offsets: id in [0,316) <-> (ox, oy, oz) in [-3,3]^3 \ [-1,1]^3, lexicographic x, y, z
 int offset_id(int ox, int oy, int oz);
 void offset_vec(int id, int o[3]);
+// NEXT 3: the 34 canonical offsets (x >= y >= 0, z >= 0; cids = their offset ids) and,
+// per offset, canonical index << 4 | op with op = x-flip | y-flip << 1 | z-flip << 2 | swap << 3
+void canonical_offsets(std::vector<int> &cids, std::vector<int> &sym_of);
+// perm[op][k]: stored grid index of the canonical table that holds T_o at stored point k
+void symmetry_perms(int nth, int nph, std::vector<int32_t> &perm);
 
 // ---------------- device kernels (kernels_*.cu) ---------------------------------------------
 struct ResampleDims {
@@ -138,6 +143,22 @@ void launch_m2l(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const
                 const int32_t *oid, const double2 *T, const double2 *M, double2 *I,
                 cudaStream_t s);
 
+// Sibling-group M2L (kernels_m2l.cu): plan once per level / operator, apply per matvec.
+struct M2LGroupPlan;
+// targets = boxes [0, nbox) with host CSR row/src/oid (oid = offset id 0..315); groups
+// [gbeg[i], gbeg[i+1]) of <= 8 boxes (nullptr: consecutive blocks of 8)
+M2LGroupPlan *m2l_group_plan_create(int64_t nbox, int64_t K, const int32_t *row, const int32_t *src,
+                                    const int32_t *oid, const std::vector<int64_t> *gbeg);
+void m2l_group_plan_destroy(M2LGroupPlan *pl);
+// T: [316][K] (perm == nullptr) or the 34 canonical tables [34][K] with perm [16][K]
+void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *perm, const double2 *M, double2 *I,
+                     cudaStream_t s);
+
+// M2L with the 34 canonical tables: T[sym_e >> 4][perm[sym_e & 15][k]]
+void launch_m2l_sym(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
+                    const int32_t *sym, const int32_t *perm, const double2 *T /*[34][K]*/, const double2 *M,
+                    double2 *I, cudaStream_t s);
+
 // Fourier resampling building blocks, warp-per-sequence shared-memory FFTs.
 // Row pass of an upward resample: for each box b and row n <= nth/2, full row of length nph
 // (stored rows n and (nth-n)%nth) resampled to nph2 -> tmp[b][n][0..nph2).
@@ -162,10 +183,10 @@ void launch_rows_down(const double2 *tmp, int64_t nbox, int nth2, int nph, int n
 
 // Alg. 1 transfer tables on the GPU (precompute).
 void launch_alg1_tables(const double2 *coef /*[nr][ell+1]*/, const int32_t *coef_of_offset,
-                        const double *r0hat /*[316][3]*/, int ell, int nth, int nphf, int qcount,
-                        double2 *out /*[316][nth][qcount]*/, cudaStream_t s);
-void launch_phi_anterp(const double2 *full /*[316][nth][nphf]*/, int nth, int nphf, int nph,
-                       double2 *out /*[316][nth][nph/2]*/, cudaStream_t s);
+                        const double *r0hat /*[noff][3]*/, int noff, int ell, int nth, int nphf, int qcount,
+                        double2 *out /*[noff][nth][qcount]*/, cudaStream_t s);
+void launch_phi_anterp(const double2 *full /*[noff][nth][nphf]*/, int noff, int nth, int nphf, int nph,
+                       double2 *out /*[noff][nth][nph/2]*/, cudaStream_t s);
 void launch_absmax(const double2 *v, int64_t n, double *out /*device, 1 value*/, cudaStream_t s);
 
 }  // namespace hfmm

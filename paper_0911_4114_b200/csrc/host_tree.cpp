@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <map>
 #include <string>
+#include <tuple>
 
 #include "hfmm_impl.h"
 #include "../../include/hfmm.h"
@@ -206,6 +208,56 @@ void partition_level2(const Tree &t, int L_f, int64_t K, int R, std::vector<int6
   }
   for (; k < R; ++k) cut[k] = B2.nbox();
 }
+
+// 34 canonical transfer vectors (Fig. SemiOctant): x >= y >= 0, z >= 0, in the
+// lexicographic order of the 316.  Offset o = F P c with c canonical, P the x<->y swap (when
+// |o_y| > |o_x|) and F the sign flips of o's negative components, so
+//   T_o(s) = T_c((F P)^T s) = T_c(P F s)
+// and on the quadrature (N_theta even, N_phi = 0 mod 4) every reflection maps grid points to grid
+// points: z-flip theta -> pi - theta (n -> N_theta/2 - n), x-flip phi -> pi - phi (m -> N_phi/2 - m),
+// y-flip phi -> -phi, swap phi -> pi/2 - phi (m -> N_phi/4 - m), folded back into the stored half
+// with eqn:NumSphereSym.  op = fx | fy << 1 | fz << 2 | swap << 3.
+void canonical_offsets(std::vector<int> &cids, std::vector<int> &sym_of /*[316]: cid << 4 | op*/) {
+  cids.clear();
+  std::map<std::tuple<int, int, int>, int> cidx;
+  for (int id = 0; id < 316; ++id) {
+    int o[3];
+    offset_vec(id, o);
+    if (o[0] >= o[1] && o[1] >= 0 && o[2] >= 0) {
+      cidx[std::make_tuple(o[0], o[1], o[2])] = (int)cids.size();
+      cids.push_back(id);
+    }
+  }
+  sym_of.assign(316, 0);
+  for (int id = 0; id < 316; ++id) {
+    int o[3];
+    offset_vec(id, o);
+    const int ax = std::abs(o[0]), ay = std::abs(o[1]), az = std::abs(o[2]);
+    const int sw = ay > ax ? 1 : 0;
+    const int c = cidx.at(std::make_tuple(std::max(ax, ay), std::min(ax, ay), az));
+    const int op = (o[0] < 0 ? 1 : 0) | (o[1] < 0 ? 2 : 0) | (o[2] < 0 ? 4 : 0) | (sw << 3);
+    sym_of[id] = (c << 4) | op;
+  }
+}
+
+// perm[op][k]: stored index of the canonical table holding T_o at stored point k
+void symmetry_perms(int nth, int nph, std::vector<int32_t> &perm) {
+  const int h = nph / 2;
+  const int64_t K = (int64_t)nth * h;
+  perm.assign((size_t)16 * K, 0);
+  for (int op = 0; op < 16; ++op)
+    for (int n = 0; n < nth; ++n)
+      for (int m = 0; m < h; ++m) {
+        int nn = n, mm = m;  // full-torus indices, 0 <= mm < nph
+        if (op & 1) mm = (nph / 2 - mm + nph) % nph;      // x -> -x: phi -> pi - phi
+        if (op & 2) mm = (nph - mm) % nph;                // y -> -y: phi -> -phi
+        if (op & 4) nn = (nth / 2 - nn + nth) % nth;      // z -> -z: theta -> pi - theta
+        if (op & 8) mm = ((nph / 4 - mm) % nph + nph) % nph;  // x <-> y: phi -> pi/2 - phi
+        if (mm >= h) nn = (nth - nn) % nth, mm -= h;      // eqn:NumSphereSym
+        perm[(size_t)op * K + (int64_t)n * h + m] = (int32_t)((int64_t)nn * h + mm);
+      }
+}
+
 
 }  // namespace hfmm
 

@@ -48,6 +48,48 @@ void launch_m2l(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const
   m2l_kernel<<<grid, M2L_TPB, 0, s>>>(box0, K, row, src, oid, T, M, I);
 }
 
+// M2L with the 34 canonical tables (NEXT 3): the table of interaction e is
+// T[c_e][perm[op_e][k]], c_e / op_e packed in sym[e] = c << 4 | op (reflection / swap op).  The
+// permuted reads are reversed runs of a row (reflections) and stay coalesced.
+__global__ void __launch_bounds__(M2L_TPB) m2l_sym_kernel(int32_t box0, int64_t K, const int32_t *__restrict__ row,
+                                                          const int32_t *__restrict__ src,
+                                                          const int32_t *__restrict__ sym,
+                                                          const int32_t *__restrict__ perm,
+                                                          const double2 *__restrict__ T,
+                                                          const double2 *__restrict__ M,
+                                                          double2 *__restrict__ I) {
+  const int32_t a = box0 + blockIdx.x;
+  const int64_t k = (int64_t)blockIdx.y * M2L_TPB + threadIdx.x;
+  if (k >= K) return;
+  double2 acc = make_double2(0.0, 0.0);
+  const int32_t e0 = row[a], e1 = row[a + 1];
+  int32_t e = e0;
+  for (; e + 1 < e1; e += 2) {  // two partners in flight
+    const int32_t c0 = sym[e], c1 = sym[e + 1];
+    const int32_t p0 = __ldg(&perm[(int64_t)(c0 & 15) * K + k]), p1 = __ldg(&perm[(int64_t)(c1 & 15) * K + k]);
+    const double2 t0 = __ldg(&T[(int64_t)(c0 >> 4) * K + p0]);
+    const double2 m0 = __ldg(&M[(int64_t)src[e] * K + k]);
+    const double2 t1 = __ldg(&T[(int64_t)(c1 >> 4) * K + p1]);
+    const double2 m1 = __ldg(&M[(int64_t)src[e + 1] * K + k]);
+    acc = cfma(t0, m0, acc);
+    acc = cfma(t1, m1, acc);
+  }
+  if (e < e1) {
+    const int32_t c0 = sym[e];
+    const int32_t p0 = __ldg(&perm[(int64_t)(c0 & 15) * K + k]);
+    acc = cfma(__ldg(&T[(int64_t)(c0 >> 4) * K + p0]), __ldg(&M[(int64_t)src[e] * K + k]), acc);
+  }
+  I[(int64_t)a * K + k] = acc;
+}
+
+void launch_m2l_sym(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
+                    const int32_t *sym, const int32_t *perm, const double2 *T, const double2 *M, double2 *I,
+                    cudaStream_t s) {
+  if (box1 <= box0 || K <= 0) return;
+  dim3 grid((unsigned)(box1 - box0), (unsigned)((K + M2L_TPB - 1) / M2L_TPB));
+  m2l_sym_kernel<<<grid, M2L_TPB, 0, s>>>(box0, K, row, src, sym, perm, T, M, I);
+}
+
 // ------------------------------------ Alg. 1 -----------------------------------------------
 // One CTA per (phi column q, offset o).  shared: c_n, samples, spectrum, truncated spectrum,
 // twiddles of length P = 2 ell + 1 and N_theta.
@@ -141,12 +183,12 @@ __global__ void __launch_bounds__(ALG1_TPB) alg1_kernel(const double2 *__restric
   }
 }
 
-void launch_alg1_tables(const double2 *coef, const int32_t *coef_of_offset, const double *r0hat,
+void launch_alg1_tables(const double2 *coef, const int32_t *coef_of_offset, const double *r0hat, int noff,
                         int ell, int nth, int nphf, int qcount, double2 *out, cudaStream_t s) {
   const int P = 2 * ell + 1;
   size_t smem = sizeof(double2) * ((size_t)(ell + 1) + 3 * (size_t)P + (size_t)(nth - 1) + (size_t)nth);
   cudaFuncSetAttribute((const void *)alg1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)qcount, 316u);
+  dim3 grid((unsigned)qcount, (unsigned)noff);
   alg1_kernel<<<grid, ALG1_TPB, smem, s>>>(coef, coef_of_offset, r0hat, ell, nth, nphf, qcount, out);
 }
 
@@ -181,9 +223,9 @@ __global__ void phi_anterp_kernel(const double2 *__restrict__ full, int nth, int
   }
 }
 
-void launch_phi_anterp(const double2 *full, int nth, int nphf, int nph, double2 *out, cudaStream_t s) {
+void launch_phi_anterp(const double2 *full, int noff, int nth, int nphf, int nph, double2 *out, cudaStream_t s) {
   size_t smem = sizeof(double2) * (size_t)nph;
-  phi_anterp_kernel<<<(unsigned)(316 * nth), 128, smem, s>>>(full, nth, nphf, nph, out);
+  phi_anterp_kernel<<<(unsigned)(noff * nth), 128, smem, s>>>(full, nth, nphf, nph, out);
 }
 
 __global__ void absmax_kernel(const double2 *__restrict__ v, int64_t n, unsigned long long *out) {

@@ -141,3 +141,36 @@ def test_toy_integral_filtered_quadrature():
     e2 = abs(trapezoid(2001) - exact)
     slope = math.log(e1 / e2) / math.log(2001 / 1001)
     assert 1.7 < slope < 2.3                      # 1/K^2 (Fig. SINconv caption)
+
+
+def test_reflection_symmetry_34_tables():
+    """P:412-415 / Fig. SemiOctant: with N_theta even and N_phi = 0 mod 4, every one of the 316
+    bandlimited tables is a grid permutation of one of the 34 canonical ones (x >= y >= 0, z >= 0):
+    T_{F P c}(theta, phi) = T_c(P F (theta, phi)) with F the sign flips and P the x<->y swap.
+    Written here from the geometry (reflections of s-hat), independently of the library."""
+    import math
+    from oracle.transfer import bmtf_table, offsets316, offsets_canonical
+    ell, kappa, a, nth, nph = 12, 9.0, 1.0, 28, 32
+    h = nph // 2
+    canon = {tuple(int(v) for v in c): bmtf_table(ell, kappa, c.astype(float) * a, nth, nph)
+             for c in offsets_canonical()}
+    assert len(canon) == 34
+    n, m = np.meshgrid(np.arange(nth), np.arange(h), indexing="ij")
+    rng = np.random.default_rng(0)
+    for o in offsets316()[rng.choice(316, 40, replace=False)]:
+        ox, oy, oz = (int(v) for v in o)
+        c = (max(abs(ox), abs(oy)), min(abs(ox), abs(oy)), abs(oz))
+        nn, mm = n.copy(), m.copy()
+        if ox < 0:
+            mm = (nph // 2 - mm) % nph            # phi -> pi - phi
+        if oy < 0:
+            mm = (-mm) % nph                      # phi -> -phi
+        if oz < 0:
+            nn = (nth // 2 - nn) % nth            # theta -> pi - theta
+        if abs(oy) > abs(ox):
+            mm = (nph // 4 - mm) % nph            # phi -> pi/2 - phi
+        up = mm >= h                              # eqn:NumSphereSym back into the stored half
+        nn = np.where(up, (nth - nn) % nth, nn)
+        mm = np.where(up, mm - h, mm)
+        direct = bmtf_table(ell, kappa, o.astype(float) * a, nth, nph)
+        assert np.allclose(canon[c][nn, mm], direct, rtol=0, atol=1e-13 * np.max(np.abs(direct))), tuple(o)
