@@ -212,10 +212,18 @@ int hfmm_l2l_op(int nparent, int n_theta, int n_phi, int n_theta2, int n_phi2,
                 const double *parent, const double *shift, const double *incoming,
                 double *child_out, void *work, void *stream);
 
-/* Diagonal M2L over a CSR interaction list: out[a][k] = sum_e T[oid[e]][k] * M[src[e]][k] for
- * e in [row[a], row[a+1]).  row: int32 [nbox+1], src: int32, oid: int32 (0..315). */
+/* Diagonal M2L over a CSR interaction list: out[a][k] = sum_e T[oid[e]][k] * M[src[e]][k]
+ * for e in [row[a], row[a+1]).  row: int32 [nbox+1], src: int32, oid: int32 (0..315); T [316][K],
+ * M / out [nbox][K] complex128.  hfmm_m2l_op: DEVICE CSR, one-shot (copies the CSR to the host and
+ * builds the sibling-group plan every call; synchronises `stream`).  For repeated application:
+ * hfmm_m2l_op_plan (HOST CSR; consecutive boxes 8 at a time form a group -- siblings when boxes
+ * are in Morton order; returns HFMM_E_ARG for an out-of-range src / oid), hfmm_m2l_op_apply
+ * (device T / M / out, enqueued on `stream`), hfmm_m2l_op_free. */
 int hfmm_m2l_op(int nbox, int64_t K, const int *row, const int *src, const int *oid,
                 const double *T, const double *M, double *out, void *stream);
+int hfmm_m2l_op_plan(int nbox, int64_t K, const int *row, const int *src, const int *oid, void **plan);
+int hfmm_m2l_op_apply(const void *plan, const double *T, const double *M, double *out, void *stream);
+void hfmm_m2l_op_free(void *plan);
 
 #ifdef __cplusplus
 }

@@ -34,6 +34,7 @@ EXPORTED = [
     "hfmm_direct", "hfmm_get_info", "hfmm_stage_times", "hfmm_debug_copy", "hfmm_last_error",
     "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
     "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
+    "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free",
 ]
 
 
@@ -93,6 +94,9 @@ def load() -> C.CDLL:
         "hfmm_m2l_op": (ci, [ci, i64, vp, vp, vp, vp, vp, vp, vp]),
         "hfmm_partition": (ci, [i64, vp, ci, vp, dbl, ci, i64, ci, vp, vp, vp]),
         "hfmm_rep_grid": (ci, [dbl, dbl, dbl, C.POINTER(ci), C.POINTER(ci)]),
+        "hfmm_m2l_op_plan": (ci, [ci, i64, vp, vp, vp, C.POINTER(vp)]),
+        "hfmm_m2l_op_apply": (ci, [vp, vp, vp, vp, vp]),
+        "hfmm_m2l_op_free": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -312,3 +316,34 @@ def m2l_op(row, src, oid, T, M, out, stream=None):
     if rc < 0:
         raise HFMMError(rc, "hfmm_m2l_op")
     return out
+
+
+class M2LOp:
+    """Sibling-group M2L plan built once from a HOST CSR (numpy int32 row / src / oid), applied to
+    device tensors (T [316][K], M and out [nbox][K], complex128) -- include/hfmm.h hfmm_m2l_op_plan."""
+
+    def __init__(self, row, src, oid, K: int):
+        self.lib = load()
+        row, src, oid = (np.ascontiguousarray(a, dtype=np.int32) for a in (row, src, oid))
+        h = C.c_void_p()
+        rc = self.lib.hfmm_m2l_op_plan(len(row) - 1, K, _ptr(row), _ptr(src), _ptr(oid), C.byref(h))
+        if rc < 0:
+            raise HFMMError(rc, "hfmm_m2l_op_plan")
+        self.h = h
+
+    def apply(self, T, M, out, stream=None):
+        rc = self.lib.hfmm_m2l_op_apply(self.h, T.data_ptr(), M.data_ptr(), out.data_ptr(), _stream(stream))
+        if rc < 0:
+            raise HFMMError(rc, "hfmm_m2l_op_apply")
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.hfmm_m2l_op_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -45,6 +45,7 @@ struct LevelDev {
   int32_t *perm = nullptr;       // [16][K]: grid permutation of each reflection / swap op (NEXT 3)
   double2 *M = nullptr, *I = nullptr, *L = nullptr;  // [nbox][K]
   int32_t *il_row = nullptr, *il_src = nullptr, *il_sym = nullptr;  // il_sym = canonical id << 4 | op
+  M2LGroupPlan *m2lg = nullptr;  // sibling-group M2L plan over the owned boxes
   int64_t il_nnz = 0;
   int32_t *parent = nullptr;     // into level l-1
   int8_t *oct = nullptr;         // octant of the box inside its parent
@@ -152,6 +153,8 @@ static thread_local std::string g_create_err;
 
 static void free_levels(hfmm_plan *p) {
   for (auto &L : p->lv) {
+    m2l_group_plan_destroy(L.m2lg);
+    L.m2lg = nullptr;
     for (void *ptr : {(void *)L.cx, (void *)L.cy, (void *)L.cz, (void *)L.ks, (void *)L.T, (void *)L.M,
                       (void *)L.I, (void *)L.L, (void *)L.il_row, (void *)L.il_src, (void *)L.il_sym, (void *)L.perm,
                       (void *)L.parent, (void *)L.oct, (void *)L.cbeg, (void *)L.shift})
@@ -538,7 +541,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       return HFMM_E_NOMEM;
     }
     // interaction lists for every box of an active level
-    std::vector<int32_t> row(1, 0), src, oid;
+    std::vector<int32_t> row(1, 0), src, oid, oid316;
     std::vector<int> cids, sym_of;
     canonical_offsets(cids, sym_of);
     for (int64_t b = 0; b < (L.active ? B.nbox() : 0); ++b) {
@@ -553,7 +556,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
             int32_t k = B.find(x, y, z);
             if (k < 0) continue;
             src.push_back(k);
-            oid.push_back(sym_of[offset_id(dx, dy, dz)]);
+            oid316.push_back(offset_id(dx, dy, dz));
+            oid.push_back(sym_of[oid316.back()]);
           }
       row.push_back((int32_t)src.size());
     }
@@ -563,6 +567,12 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       std::vector<int32_t> pm;
       symmetry_perms(L.nth, L.nph, pm);
       L.perm = dupload(pm);
+      // sibling groups over the owned boxes: consecutive boxes (Morton order) with one parent
+      std::vector<int64_t> gb;
+      for (int64_t b = L.own0; b < L.own1; ++b)
+        if (gb.empty() || B.parent[b] != B.parent[b - 1] || b - gb.back() == 8) gb.push_back(b);
+      gb.push_back(L.own1);
+      if (L.own1 > L.own0) L.m2lg = m2l_group_plan_create(B.nbox(), L.K, row.data(), src.data(), oid316.data(), &gb);
     }
     // tree links
     std::vector<int32_t> par(B.parent.begin(), B.parent.end());
@@ -806,7 +816,7 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
     if (prof) cudaEventRecord(p->sev[2], s);
     for (int l = 2; l <= Lf; ++l) {  // M2L
       LevelDev &L = p->lv[l];
-      launch_m2l_sym((int32_t)L.own0, (int32_t)L.own1, L.K, L.il_row, L.il_src, L.il_sym, L.perm, L.T, L.M, L.I, s);
+      m2l_group_apply(L.m2lg, L.T, L.perm, L.M, L.I, s);
     }
     if (prof) cudaEventRecord(p->sev[3], s);
     for (int l = 2; l < Ds; ++l) {  // L2L; L_2 = I_2; I = 0 below L_f (R-14)
@@ -1131,10 +1141,38 @@ extern "C" int hfmm_l2l_op(int nparent, int nth, int nph, int nth2, int nph2, co
   return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
 }
 
+extern "C" int hfmm_m2l_op_plan(int nbox, int64_t K, const int *row, const int *src, const int *oid, void **plan) {
+  if (nbox < 0 || K <= 0 || !row || !src || !oid || !plan) return HFMM_E_ARG;
+  for (int64_t e = 0; e < row[nbox]; ++e)
+    if (oid[e] < 0 || oid[e] >= 316 || src[e] < 0 || src[e] >= nbox) return HFMM_E_ARG;
+  *plan = m2l_group_plan_create(nbox, K, row, src, oid, nullptr);
+  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
+}
+
+extern "C" int hfmm_m2l_op_apply(const void *plan, const double *T, const double *M, double *out, void *stream) {
+  if (!plan || !T || !M || !out) return HFMM_E_ARG;
+  m2l_group_apply((const M2LGroupPlan *)plan, (const double2 *)T, nullptr, (const double2 *)M, (double2 *)out,
+                  (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
+}
+
+extern "C" void hfmm_m2l_op_free(void *plan) { m2l_group_plan_destroy((M2LGroupPlan *)plan); }
+
 extern "C" int hfmm_m2l_op(int nbox, int64_t K, const int *row, const int *src, const int *oid, const double *T,
                            const double *M, double *out, void *stream) {
   if (nbox < 0 || K <= 0 || !row || !src || !oid || !T || !M || !out) return HFMM_E_ARG;
-  launch_m2l(0, nbox, K, row, src, oid, (const double2 *)T, (const double2 *)M, (double2 *)out,
-             (cudaStream_t)stream);
-  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
+  // device CSR -> host, one-shot plan (hfmm_m2l_op_plan / _apply for repeated use)
+  std::vector<int32_t> hr(nbox + 1);
+  if (cudaMemcpy(hr.data(), row, hr.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return HFMM_E_CUDA;
+  std::vector<int32_t> hs(hr[nbox]), ho(hr[nbox]);
+  if (cudaMemcpy(hs.data(), src, hs.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(ho.data(), oid, ho.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return HFMM_E_CUDA;
+  void *pl = nullptr;
+  int rc = hfmm_m2l_op_plan(nbox, K, hr.data(), hs.data(), ho.data(), &pl);
+  if (rc) return rc;
+  rc = hfmm_m2l_op_apply(pl, T, M, out, stream);
+  cudaStreamSynchronize((cudaStream_t)stream);
+  hfmm_m2l_op_free(pl);
+  return rc;
 }

@@ -27,7 +27,13 @@
 namespace hfmm {
 
 constexpr int M2LG_KC = 32;       // directions per chunk (lanes)
-constexpr int M2LG_WARPS = 8;     // groups in flight per CTA
+#ifndef HFMM_M2L_WARPS
+#define HFMM_M2L_WARPS 16
+#endif
+#ifndef HFMM_M2L_PF
+#define HFMM_M2L_PF 4
+#endif
+constexpr int M2LG_WARPS = HFMM_M2L_WARPS;  // groups in flight per CTA (one CTA per SM: 162 KB table chunk)
 constexpr int M2LG_NOFF = 316;
 
 __constant__ int32_t c_sym_of[M2LG_NOFF];  // offset id -> canonical id << 4 | op (34-table mode)
@@ -73,14 +79,25 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_group_kernel(
 #pragma unroll
       for (int a = 0; a < 8; ++a) acc[a] = make_double2(0.0, 0.0);
       const int32_t e0 = gsrc_row[g], e1 = gsrc_row[g + 1];
-      for (int32_t e = e0; e < e1; ++e) {
-        const double2 m = kval ? __ldg(&M[(int64_t)src_box[e] * K + k]) : make_double2(0.0, 0.0);
-        const int4 packed = __ldg(reinterpret_cast<const int4 *>(tid8) + e);  // 8 x int16, warp-uniform
-        const int16_t *t8 = reinterpret_cast<const int16_t *>(&packed);
+      // sources in batches of PF: all loads of a batch in flight before its MACs
+      constexpr int PF = HFMM_M2L_PF;
+      for (int32_t e = e0; e < e1; e += PF) {
+        double2 m[PF];
+        int4 pk[PF];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          const int t = t8[a];
-          if (t >= 0) acc[a] = g_cfma(Ts[t * M2LG_KC + lane], m, acc[a]);
+        for (int j = 0; j < PF; ++j) {
+          const bool v = e + j < e1;
+          m[j] = (v && kval) ? __ldg(&M[(int64_t)src_box[e + j] * K + k]) : make_double2(0.0, 0.0);
+          pk[j] = v ? __ldg(reinterpret_cast<const int4 *>(tid8) + e + j) : make_int4(-1, -1, -1, -1);
+        }
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+          const int16_t *t8 = reinterpret_cast<const int16_t *>(&pk[j]);
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            const int t = t8[a];
+            if (t >= 0) acc[a] = g_cfma(Ts[t * M2LG_KC + lane], m[j], acc[a]);
+          }
         }
       }
 #pragma unroll
@@ -179,9 +196,9 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nchunks = (pl->K + M2LG_KC - 1) / M2LG_KC;
-  // group ranges per chunk: enough units to spread one chunk over the SMs, >= 8 groups per warp-set
-  int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((pl->ngroups + 2 * M2LG_WARPS - 1) / (2 * M2LG_WARPS),
-                                                          (nsm + nchunks - 1) / nchunks * 4));
+  // group ranges per chunk: one chunk spread over all SMs at a time (chunk-major units), so the
+  // chunk's slice of M stays L2-resident while every CTA works on it; >= 8 groups per unit
+  int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((pl->ngroups + M2LG_WARPS - 1) / M2LG_WARPS, nsm));
   const int64_t gpu = (pl->ngroups + ranges - 1) / ranges;
   ranges = (pl->ngroups + gpu - 1) / gpu;
   const int64_t nunits = nchunks * ranges;

@@ -120,6 +120,11 @@ def test_c2_m2l(hf, lattice, B):
     I = torch.empty_like(M)
     r, s_, o_ = (torch.from_numpy(a).cuda() for a in (row, src, oid))
     hf.m2l_op(r, s_, o_, T, M, I)
+    # the plan-once entry point (what bench.py times) gives the same result
+    I2 = torch.empty_like(M)
+    hf.M2LOp(row, src, oid, K).apply(T, M, I2)
+    torch.cuda.synchronize()
+    assert torch.equal(I, I2)
     lev = Level(0, 1.0, [tuple(c) for c in g], _Periodic(g, MICROBENCH["lattice"]), [], np.zeros((nbox, 3)))
     tid = {tuple(int(v) for v in o): k for k, o in enumerate(offs)}
     Th = T.cpu().numpy()
