@@ -1,13 +1,11 @@
 // Fourier interpolation / anterpolation on the sphere (product code, sm_100a).
 //   P:373-378  interpolation = zero-pad the Fourier coefficients, anterpolation = truncate
-//   P:512      kept band |k| <= min(N, N')/2 - 1 (Nyquist dropped; R-6)
+//   P:512      kept band |k| <= (min(N, N') - 1) / 2 (Nyquist dropped; R-6)
 //   P:724-749  5-step 2-D procedure between quadratures, with eqn:NumSphereSym
 //              used to build theta-periodic columns / full phi-rows from half storage.
 // Each 1-D resample N -> N' is: forward FFT (length N), spectral pad/truncate with 1/N,
-// inverse FFT (length N') computed as conj(FFT(conj(.))).  FFTs are mixed-radix Stockham
-// (radices 4, 2, 3, 5, 7; autosort, ping-pong buffers) run by one warp per sequence in
-// shared memory, with exact twiddles e^{-2 pi i t/N} from a per-length table in global
-// memory (read through L1).
+// inverse FFT (length N') computed as the conjugate of a forward FFT of the conjugate (the
+// conjugations fold into the pad and the store).
 //
 // The two-pass layout (rows pass, columns pass, intermediate in global memory / L2):
 //   upward   (M2M): rows n <= N_theta/2 resampled N_phi -> N'_phi (step 1), then
@@ -17,6 +15,14 @@
 //   downward (L2L): columns of conj(shift) * L_parent (steps 1-2 are the identity for
 //            anterpolation) resampled N_theta -> N'_theta (step 3), then rows n <= N'_theta/2
 //            rebuilt (step 4) and resampled N_phi -> N'_phi (step 5), + I_child.
+//
+// Each pass is a tiled, batched FFT kernel: a CTA stages a tile of vectors (RB whole rows, or a
+// CB-column strip of one box) in shared memory with coalesced global loads, runs mixed-radix
+// Stockham passes (radices 16, 8, 4, 2, 3, 5, 7; radix-16/8 butterflies in registers) with one
+// butterfly per thread and the batch index on the fastest thread index -- shared accesses then
+// stride over vectors of odd pitch (conflict-free) and the twiddles of a warp are uniform -- and
+// writes the tile back with coalesced stores.  Tiles are sized to ~70 KB of shared memory so
+// three CTAs share an SM.
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cmath>
@@ -26,27 +32,6 @@
 #include "hfmm_impl.h"
 
 namespace hfmm {
-
-struct FFTLen {
-  int N;
-  int nr;
-  int radix[12];
-  const double2 *tw;  // e^{-2 pi i t/N}, t < N
-};
-
-static FFTLen make_len(const TwiddleSet &ts, int N) {
-  FFTLen L;
-  L.N = N;
-  L.nr = 0;
-  int m = N;
-  for (int r : {4, 2, 3, 5, 7})
-    while (m % r == 0) {
-      L.radix[L.nr++] = r;
-      m /= r;
-    }
-  L.tw = (N < 1024 && ts.offset[N] >= 0) ? ts.d + ts.offset[N] : nullptr;
-  return L;
-}
 
 void TwiddleSet::build(const std::vector<int> &lengths) {
   for (int i = 0; i < 1024; ++i) offset[i] = -1;
@@ -72,103 +57,244 @@ void TwiddleSet::free_all() {
   d = nullptr;
 }
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+
+// radix codes 0..6 = {16, 8, 4, 2, 3, 5, 7}, 3 bits per pass (a packed word: no local-memory array)
+struct RLen {
+  int N;
+  int nr;
+  unsigned codes;
+  const double2 *tw;  // e^{-2 pi i t / N}, t < N (global, L1-resident)
+};
+
+static RLen rlen(const TwiddleSet &ts, int N) {
+  RLen L{};
+  L.N = N;
+  int m = N, e = 0;
+  while (m % 2 == 0) m /= 2, ++e;
+  auto push = [&](int code) { L.codes |= (unsigned)code << (3 * L.nr++); };
+  // powers of two as radix-16 passes plus at most one 8 / 4 (no radix-2 pass unless N has a single 2)
+  if (e == 1) push(3);
+  else {
+    int e16 = e / 4, rest = e % 4;
+    if (rest == 1 && e16 > 0) --e16, push(1), push(2);  // 2^5 = 8 * 4
+    for (int i = 0; i < e16; ++i) push(0);
+    if (rest == 2) push(2);
+    if (rest == 3) push(1);
+  }
+  const int odd[3] = {3, 5, 7};
+  for (int c = 0; c < 3; ++c)
+    while (m % odd[c] == 0) push(4 + c), m /= odd[c];
+  L.tw = ts.d + ts.offset[N];
+  return L;
+}
+
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_conj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 c_mi(double2 a) { return make_double2(a.y, -a.x); }  // -i a
 
-// forward small DFTs, out[t] = sum_s v[s] e^{-2 pi i s t / R}
-__device__ __forceinline__ void bfly2(double2 *v) {
-  double2 a = v[0], b = v[1];
-  v[0] = cadd(a, b);
-  v[1] = csub(a, b);
+// ---- forward small DFTs in registers: out[t] = sum_s v[s] e^{-2 pi i s t / R} -------------------
+__device__ __forceinline__ void dft4(double2 &a0, double2 &a1, double2 &a2, double2 &a3) {
+  const double2 s0 = c_add(a0, a2), d0 = c_sub(a0, a2);
+  const double2 s1 = c_add(a1, a3), d1 = c_mi(c_sub(a1, a3));
+  a0 = c_add(s0, s1);
+  a2 = c_sub(s0, s1);
+  a1 = c_add(d0, d1);
+  a3 = c_sub(d0, d1);
 }
-__device__ __forceinline__ void bfly4(double2 *v) {
-  double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
-  double2 b0 = cadd(v[1], v[3]), b1 = csub(v[1], v[3]);
-  // multiply b1 by -i
-  double2 b1m = make_double2(b1.y, -b1.x);
-  v[0] = cadd(a0, b0);
-  v[2] = csub(a0, b0);
-  v[1] = cadd(a1, b1m);
-  v[3] = csub(a1, b1m);
-}
-__device__ __forceinline__ void bfly3(double2 *v) {
-  const double c = -0.5, s = -0.86602540378443864676372317075294;  // e^{-2 pi i/3}
-  double2 t1 = cadd(v[1], v[2]), t2 = csub(v[1], v[2]);
-  double2 m1 = make_double2(fma(c, t1.x, v[0].x), fma(c, t1.y, v[0].y));
-  double2 m2 = make_double2(-s * t2.y, s * t2.x);  // i s t2
-  v[0] = cadd(v[0], t1);
-  v[1] = cadd(m1, m2);
-  v[2] = csub(m1, m2);
-}
-// e^{-2 pi i e / R} for R = 5, 7 (compile-time constants after unrolling)
+
 template <int R>
-__device__ __forceinline__ void bfly_generic(double2 *v) {
-  const double c5[5] = {1.0, 0.30901699437494742410, -0.80901699437494742410, -0.80901699437494742410,
-                        0.30901699437494742410};
-  const double s5[5] = {0.0, -0.95105651629515357212, -0.58778525229247312917, 0.58778525229247312917,
-                        0.95105651629515357212};
-  const double c7[7] = {1.0, 0.62348980185873353053, -0.22252093395631440429, -0.90096886790241912624,
-                        -0.90096886790241912624, -0.22252093395631440429, 0.62348980185873353053};
-  const double s7[7] = {0.0, -0.78183148246802980871, -0.97492791218182360702, -0.43388373911755812048,
-                        0.43388373911755812048, 0.97492791218182360702, 0.78183148246802980871};
+__device__ __forceinline__ void dft(double2 *v);
+
+template <>
+__device__ __forceinline__ void dft<2>(double2 *v) {
+  const double2 a = v[0], b = v[1];
+  v[0] = c_add(a, b);
+  v[1] = c_sub(a, b);
+}
+template <>
+__device__ __forceinline__ void dft<4>(double2 *v) {
+  dft4(v[0], v[1], v[2], v[3]);
+}
+template <>
+__device__ __forceinline__ void dft<3>(double2 *v) {
+  const double c = -0.5, s = -0.86602540378443864676372317075294;  // e^{-2 pi i/3}
+  const double2 t1 = c_add(v[1], v[2]), t2 = c_sub(v[1], v[2]);
+  const double2 m1 = make_double2(fma(c, t1.x, v[0].x), fma(c, t1.y, v[0].y));
+  const double2 m2 = make_double2(-s * t2.y, s * t2.x);
+  v[0] = c_add(v[0], t1);
+  v[1] = c_add(m1, m2);
+  v[2] = c_sub(m1, m2);
+}
+template <int R>
+__device__ __forceinline__ void dft_odd(double2 *v) {  // R = 5, 7: symmetric pairs
+  constexpr int H = R / 2;
+  double c[H], s[H];
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    c[k - 1] = (R == 5) ? (k == 1 ? 0.30901699437494742410 : -0.80901699437494742410)
+                        : (k == 1 ? 0.62348980185873353053 : k == 2 ? -0.22252093395631440429 : -0.90096886790241912624);
+    s[k - 1] = (R == 5) ? (k == 1 ? -0.95105651629515357212 : -0.58778525229247312917)
+                        : (k == 1 ? -0.78183148246802980871 : k == 2 ? -0.97492791218182360702 : -0.43388373911755812048);
+  }
+  double2 a[H], b[H];
+#pragma unroll
+  for (int k = 1; k <= H; ++k) a[k - 1] = c_add(v[k], v[R - k]), b[k - 1] = c_sub(v[k], v[R - k]);
   double2 o[R];
+  double2 s0 = v[0];
 #pragma unroll
-  for (int t = 0; t < R; ++t) {
-    double2 acc = v[0];
+  for (int k = 0; k < H; ++k) s0 = c_add(s0, a[k]);
+  o[0] = s0;
 #pragma unroll
-    for (int s = 1; s < R; ++s) {
-      const int e = (s * t) % R;
-      const double cs = (R == 5) ? c5[e] : c7[e];
-      const double sn = (R == 5) ? s5[e] : s7[e];
-      acc = make_double2(fma(v[s].x, cs, fma(-v[s].y, sn, acc.x)), fma(v[s].x, sn, fma(v[s].y, cs, acc.y)));
+  for (int t = 1; t <= H; ++t) {
+    double2 re = v[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 1; k <= H; ++k) {
+      const int e = (k * t) % R;
+      const int ee = e <= H ? e : R - e;
+      const double cs = c[ee - 1];
+      const double sn = e <= H ? s[ee - 1] : -s[ee - 1];
+      re = make_double2(fma(cs, a[k - 1].x, re.x), fma(cs, a[k - 1].y, re.y));
+      im = make_double2(fma(sn, b[k - 1].x, im.x), fma(sn, b[k - 1].y, im.y));
     }
-    o[t] = acc;
+    // X_t = re + i im, X_{R-t} = re - i im
+    o[t] = make_double2(re.x - im.y, re.y + im.x);
+    o[R - t] = make_double2(re.x + im.y, re.y - im.x);
   }
 #pragma unroll
   for (int t = 0; t < R; ++t) v[t] = o[t];
 }
-
-template <int R>
-__device__ __forceinline__ void stockham_stage(const double2 *__restrict__ src, double2 *__restrict__ dst,
-                                               int N, int Ns, const double2 *__restrict__ tw, int lane) {
-  const int stride = N / R;
-  const int tstep = N / (Ns * R);
-  for (int j = lane; j < stride; j += 32) {
-    const int k = j % Ns;
-    double2 v[R];
+template <>
+__device__ __forceinline__ void dft<5>(double2 *v) {
+  dft_odd<5>(v);
+}
+template <>
+__device__ __forceinline__ void dft<7>(double2 *v) {
+  dft_odd<7>(v);
+}
+template <>
+__device__ __forceinline__ void dft<8>(double2 *v) {
+  const double h = 0.70710678118654752440;
+  dft4(v[0], v[2], v[4], v[6]);
+  dft4(v[1], v[3], v[5], v[7]);
+  // odd part twiddles w8^k, k = 0..3
+  const double2 o1 = make_double2(h * (v[3].x + v[3].y), h * (v[3].y - v[3].x));     // (1 - i)/sqrt2
+  const double2 o2 = c_mi(v[5]);                                                     // -i
+  const double2 o3 = make_double2(h * (v[7].y - v[7].x), -h * (v[7].x + v[7].y));    // (-1 - i)/sqrt2
+  const double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6], o0 = v[1];
+  v[0] = c_add(e0, o0);
+  v[4] = c_sub(e0, o0);
+  v[1] = c_add(e1, o1);
+  v[5] = c_sub(e1, o1);
+  v[2] = c_add(e2, o2);
+  v[6] = c_sub(e2, o2);
+  v[3] = c_add(e3, o3);
+  v[7] = c_sub(e3, o3);
+}
+template <>
+__device__ __forceinline__ void dft<16>(double2 *v) {
+  // 16 = 4 x 4: DFT4 over q (stride 4), twiddle w16^{q k}, DFT4 over k
+  dft4(v[0], v[4], v[8], v[12]);
+  dft4(v[1], v[5], v[9], v[13]);
+  dft4(v[2], v[6], v[10], v[14]);
+  dft4(v[3], v[7], v[11], v[15]);
+  // A_q[k] sits at v[q + 4 k]; multiply by w16^{q k}
+  const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+  const double2 w1 = make_double2(c1, -s1), w2 = make_double2(h, -h), w3 = make_double2(s1, -c1);
+  const double2 w6 = make_double2(-h, -h), w9 = make_double2(-c1, s1);
+  v[5] = c_mul(v[5], w1);
+  v[9] = c_mul(v[9], w2);
+  v[13] = c_mul(v[13], w3);
+  v[6] = c_mul(v[6], w2);
+  v[10] = c_mi(v[10]);
+  v[14] = c_mul(v[14], w6);
+  v[7] = c_mul(v[7], w3);
+  v[11] = c_mul(v[11], w6);
+  v[15] = c_mul(v[15], w9);
+  // X[k + 4 p] = sum_q A_q[k] w4^{q p}
+  dft4(v[0], v[1], v[2], v[3]);
+  dft4(v[4], v[5], v[6], v[7]);
+  dft4(v[8], v[9], v[10], v[11]);
+  dft4(v[12], v[13], v[14], v[15]);
+  double2 o[16];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      v[r] = src[j + r * stride];
-      if (r) v[r] = cmul(v[r], __ldg(&tw[k * r * tstep]));
-    }
-    if (R == 2) bfly2(v);
-    else if (R == 4) bfly4(v);
-    else if (R == 3) bfly3(v);
-    else bfly_generic<R>(v);
-    const int idxD = (j / Ns) * Ns * R + k;
+  for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[idxD + r * Ns] = v[r];
-  }
-  __syncwarp();
+    for (int p = 0; p < 4; ++p) o[k + 4 * p] = v[4 * k + p];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) v[t] = o[t];
 }
 
-// forward FFT of a[0..N) (warp-cooperative); returns the buffer holding the result (a or b)
-__device__ double2 *warp_fft(double2 *a, double2 *b, const FFTLen &L, int lane) {
+// ---- integer division by a runtime divisor without the ~25-instruction IDIV sequence: float
+//      reciprocal estimate + one correction (exact for 0 <= x < 2^22) -------------------------------
+struct FDiv {
+  int d;
+  float inv;
+  __device__ __forceinline__ FDiv(int d_) : d(d_), inv(1.0f / (float)d_) {}
+  __device__ __forceinline__ int div(int x, int &rem) const {
+    int q = __float2int_rz(__int2float_rz(x) * inv);
+    int r = x - q * d;
+    if (r < 0) r += d, --q;
+    else if (r >= d) r -= d, ++q;
+    rem = r;
+    return q;
+  }
+};
+
+// ---- batched vectors: vector v = (group g = v / vper, member u = v % vper) at
+//      base(v) = g * gstride + u * vstride, element e at base + e * estride ----------------------
+struct VecSet {
+  int nvec, vper, gstride, vstride, estride;
+};
+__device__ __forceinline__ int vbase(const VecSet &vs, const FDiv &fper, int v) {
+  int u;
+  const int g = fper.div(v, u);
+  return g * vs.gstride + u * vs.vstride;
+}
+
+template <int R>
+__device__ __forceinline__ void stockham_pass(const double2 *__restrict__ src, double2 *__restrict__ dst,
+                                              const VecSet &vs, int N, int Ns, const double2 *__restrict__ tw) {
+  const int nb = N / R, tstep = N / (Ns * R), total = vs.nvec * nb, es = vs.estride;
+  const FDiv fv(vs.nvec), fper(vs.vper), fns(Ns);
+  for (int w = threadIdx.x; w < total; w += blockDim.x) {
+    int v, k;
+    const int j = fv.div(w, v);
+    fns.div(j, k);
+    const int b = vbase(vs, fper, v);
+    double2 x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = src[b + (j + r * nb) * es];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) x[r] = c_mul(x[r], __ldg(&tw[k * r * tstep]));
+    }
+    dft<R>(x);
+    const int o = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[b + (o + r * Ns) * es] = x[r];
+  }
+}
+
+// forward FFT of every vector (length L.N) in buffer a, ping-pong with b; returns the result buffer
+__device__ __forceinline__ double2 *fft_batch(double2 *a, double2 *b, const VecSet &vs, const RLen &L) {
   double2 *src = a, *dst = b;
   int Ns = 1;
   for (int s = 0; s < L.nr; ++s) {
-    const int R = L.radix[s];
-    switch (R) {
-      case 4: stockham_stage<4>(src, dst, L.N, Ns, L.tw, lane); break;
-      case 2: stockham_stage<2>(src, dst, L.N, Ns, L.tw, lane); break;
-      case 3: stockham_stage<3>(src, dst, L.N, Ns, L.tw, lane); break;
-      case 5: stockham_stage<5>(src, dst, L.N, Ns, L.tw, lane); break;
-      default: stockham_stage<7>(src, dst, L.N, Ns, L.tw, lane); break;
+    int R;
+    switch ((L.codes >> (3 * s)) & 7u) {
+      case 0: stockham_pass<16>(src, dst, vs, L.N, Ns, L.tw); R = 16; break;
+      case 1: stockham_pass<8>(src, dst, vs, L.N, Ns, L.tw); R = 8; break;
+      case 2: stockham_pass<4>(src, dst, vs, L.N, Ns, L.tw); R = 4; break;
+      case 3: stockham_pass<2>(src, dst, vs, L.N, Ns, L.tw); R = 2; break;
+      case 4: stockham_pass<3>(src, dst, vs, L.N, Ns, L.tw); R = 3; break;
+      case 5: stockham_pass<5>(src, dst, vs, L.N, Ns, L.tw); R = 5; break;
+      default: stockham_pass<7>(src, dst, vs, L.N, Ns, L.tw); R = 7; break;
     }
+    __syncthreads();
     double2 *t = src;
     src = dst;
     dst = t;
@@ -177,198 +303,232 @@ __device__ double2 *warp_fft(double2 *a, double2 *b, const FFTLen &L, int lane) 
   return src;
 }
 
-// 1-D Fourier resample of A[0..N) to length N'; returns Z with y[t] = conj(Z[t]).
-__device__ double2 *warp_resample(double2 *A, double2 *B, const FFTLen &Lin, const FFTLen &Lout, int lane) {
-  double2 *X = warp_fft(A, B, Lin, lane);
-  double2 *Y = (X == A) ? B : A;
-  const int N = Lin.N, Np = Lout.N;
-  const int K = (min(N, Np) - 1) / 2;
+// spectrum X (length N) -> conj(Y / N) on length N2, band |f| <= (min(N, N2) - 1) / 2 (R-6)
+__device__ __forceinline__ void pad_batch(const double2 *__restrict__ X, double2 *__restrict__ Y, const VecSet &vs, int N, int N2) {
+  const int K = (min(N, N2) - 1) / 2, total = vs.nvec * N2, es = vs.estride;
   const double sc = 1.0 / (double)N;
-  for (int t = lane; t < Np; t += 32) {
-    const int f = (t <= Np / 2) ? t : t - Np;
-    double2 v = make_double2(0.0, 0.0);
+  const FDiv fv(vs.nvec), fper(vs.vper);
+  for (int w = threadIdx.x; w < total; w += blockDim.x) {
+    int v;
+    const int t = fv.div(w, v);
+    const int f = (t <= N2 / 2) ? t : t - N2;
+    const int b = vbase(vs, fper, v);
+    double2 val = make_double2(0.0, 0.0);
     if (f <= K && f >= -K) {
-      const double2 x = X[f >= 0 ? f : f + N];
-      v = make_double2(x.x * sc, -x.y * sc);  // conj for the inverse transform
+      const double2 x = X[b + (f >= 0 ? f : f + N) * es];
+      val = make_double2(x.x * sc, -x.y * sc);
     }
-    Y[t] = v;
+    Y[b + t * es] = val;
   }
-  __syncwarp();
-  return warp_fft(Y, X, Lout, lane);
+  __syncthreads();
 }
 
-constexpr int FFT_WARPS = 4;
 
-// ------------------------------- upward: rows pass -----------------------------------------
-__global__ void __launch_bounds__(32 * FFT_WARPS) rows_up_kernel(const double2 *__restrict__ in, int64_t nbox,
-                                                                 int nth, int nph, FFTLen Lin, FFTLen Lout,
-                                                                 double2 *__restrict__ tmp) {
+constexpr int RS_TPB = 128;
+
+// 16-byte global -> shared copies issued asynchronously (cp.async, L2 only): a thread's whole
+// share of a tile is in flight at once instead of one load-store round trip at a time.
+__device__ __forceinline__ void cp_async16(double2 *smem, const double2 *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+static const size_t kTileSmem = 72 * 1024;  // per CTA: three CTAs per SM
+
+// ---- rows pass --------------------------------------------------------------------------------
+// Row r = (box b, n) for n < nrow = nth/2 + 1 (grid rows n <= N_theta/2).  Input: half storage
+// [nth][h] of box b; full row e < nph = (row n)[e] for e < h, (row (nth - n) % nth)[e - h] beyond
+// (eqn:NumSphereSym).  UP: output full rows of length nph2 to out[b][n][.]; DOWN: output back to
+// half storage out[b][n][t < h2] and out[b][nth - n][t - h2] (+ add).
+template <bool UP>
+__global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict__ in, int64_t nbox, int nth,
+                                                      int nph, int nph2, int RB, int pitch, RLen L1, RLen L2,
+                                                      const double2 *__restrict__ add, double2 *__restrict__ out) {
   extern __shared__ double2 sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int maxn = max(Lin.N, Lout.N);
-  double2 *A = sm + (size_t)warp * 2 * maxn, *B = A + maxn;
-  const int rows = nth / 2 + 1;
-  const int64_t seq = (int64_t)blockIdx.x * FFT_WARPS + warp;
-  if (seq >= nbox * rows) return;
-  const int64_t b = seq / rows;
-  const int n = (int)(seq % rows);
-  const int h = nph / 2;
-  const double2 *r0 = in + ((int64_t)b * nth + n) * h;
-  const double2 *r1 = in + ((int64_t)b * nth + (nth - n) % nth) * h;
-  for (int m = lane; m < nph; m += 32) A[m] = (m < h) ? r0[m] : r1[m - h];
-  __syncwarp();
-  double2 *Z = warp_resample(A, B, Lin, Lout, lane);
-  double2 *o = tmp + ((int64_t)b * rows + n) * Lout.N;
-  for (int t = lane; t < Lout.N; t += 32) o[t] = conjd(Z[t]);
+  double2 *A = sm, *Bf = sm + (size_t)RB * pitch;
+  const int nrow = nth / 2 + 1, h = nph / 2, h2 = nph2 / 2;
+  const int64_t total = nbox * nrow;
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int nr = (int)min((int64_t)RB, total - r0);
+  // load (e fastest: coalesced half-rows)
+  const FDiv fn(nph);
+  for (int w = threadIdx.x; w < nr * nph; w += blockDim.x) {
+    int e;
+    const int v = fn.div(w, e);
+    const int64_t r = r0 + v;
+    const int64_t b = r / nrow;
+    const int n = (int)(r - b * nrow);
+    const int row = (e < h || n == 0) ? n : nth - n;
+    cp_async16(&A[v * pitch + e], &in[(b * nth + row) * h + (e < h ? e : e - h)]);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const VecSet vs{nr, nr, 0, pitch, 1};
+  double2 *X = fft_batch(A, Bf, vs, L1);
+  double2 *Y = (X == A) ? Bf : A;
+  pad_batch(X, Y, vs, nph, nph2);
+  double2 *Z = fft_batch(Y, X, vs, L2);  // conj of the resampled rows
+  const FDiv fn2(nph2);
+  for (int w = threadIdx.x; w < nr * nph2; w += blockDim.x) {
+    int t;
+    const int v = fn2.div(w, t);
+    const int64_t r = r0 + v;
+    const int64_t b = r / nrow;
+    const int n = (int)(r - b * nrow);
+    double2 val = c_conj(Z[v * pitch + t]);
+    if (UP) {
+      out[(b * nrow + n) * nph2 + t] = val;
+    } else {
+      int orow, oc;
+      if (t < h2) {
+        orow = n, oc = t;
+      } else {
+        if (n == 0 || 2 * n == nth) continue;   // both halves are the same points
+        orow = nth - n, oc = t - h2;
+      }
+      const int64_t o = (b * nth + orow) * h2 + oc;
+      if (add) val = c_add(val, add[o]);
+      out[o] = val;
+    }
+  }
 }
 
-// ------------------------------- upward: columns pass (+ shift, accumulate) -----------------
-__global__ void __launch_bounds__(32 * FFT_WARPS) cols_up_kernel(const double2 *__restrict__ tmp, int nth, int nph2,
-                                                                 const int32_t *__restrict__ cbeg, int64_t cbase,
-                                                                 const int8_t *__restrict__ oct, int64_t nparent,
-                                                                 const double2 *__restrict__ shift,
-                                                                 FFTLen Lin, FFTLen Lout,
-                                                                 double2 *__restrict__ out) {
+// ---- columns pass -----------------------------------------------------------------------------
+// CTA = (item, strip of CB columns).  UP (M2M): item = parent p, columns m < h2 of the rows-pass
+// output of each child c in [cbeg[p], cbeg[p+1]) (full rows of length nph2, rows n <= nth/2; the
+// theta-periodic column is (row n)[m] for n <= nth/2 and (row nth - n)[m + h2] beyond), resampled
+// nth -> nth2, times shift[oct[c]][t][m], summed over the children into out[p][t][m].
+// DOWN (L2L): item = child c, columns m < h of conj(shift[oct[c]]) * in[par[c]] ([nth][h]),
+// resampled nth -> nth2 into out[c][t][m] ([nth2][h]).
+template <bool UP>
+__global__ void __launch_bounds__(RS_TPB) cols_kernel(const double2 *__restrict__ in, int64_t nitem, int nth,
+                                                      int ncols, int rowlen, int nth2, int CB, int cp,
+                                                      const int32_t *__restrict__ cbeg, int64_t cbase,
+                                                      const int32_t *__restrict__ par,
+                                                      const int8_t *__restrict__ oct,
+                                                      const double2 *__restrict__ shift, RLen L1, RLen L2,
+                                                      double2 *__restrict__ out) {
   extern __shared__ double2 sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int maxn = max(Lin.N, Lout.N);
-  double2 *A = sm + (size_t)warp * 3 * maxn, *B = A + maxn, *C = B + maxn;
-  const int h2 = nph2 / 2;
-  const int64_t seq = (int64_t)blockIdx.x * FFT_WARPS + warp;
-  if (seq >= nparent * h2) return;
-  const int64_t p = seq / h2;
-  const int m = (int)(seq % h2);
-  const int rows = nth / 2 + 1;
-  const int nth2 = Lout.N;
-  for (int t = lane; t < nth2; t += 32) C[t] = make_double2(0.0, 0.0);
-  const int64_t c0 = cbeg ? cbeg[p] : p, c1 = cbeg ? cbeg[p + 1] : p + 1;
+  const int maxn = max(nth, nth2);
+  double2 *A = sm, *Bf = sm + (size_t)maxn * cp;
+  const int nstrip = (ncols + CB - 1) / CB;
+  const int64_t item = blockIdx.x / nstrip;
+  const int m0 = (int)(blockIdx.x % nstrip) * CB;
+  const int nc = min(CB, ncols - m0);
+  const int64_t c0 = UP ? (cbeg ? cbeg[item] : item) : item;
+  const int64_t c1 = UP ? (cbeg ? cbeg[item + 1] : item + 1) : item + 1;
+  const FDiv fc(nc);
+  const VecSet vs{nc, nc, 0, 1, cp};
   for (int64_t c = c0; c < c1; ++c) {
-    const double2 *tc = tmp + (int64_t)(c - cbase) * rows * nph2;
-    for (int n = lane; n < nth; n += 32)
-      A[n] = (2 * n <= nth) ? tc[(int64_t)n * nph2 + m] : tc[(int64_t)(nth - n) * nph2 + m + h2];
-    __syncwarp();
-    double2 *Z = warp_resample(A, B, Lin, Lout, lane);
-    const double2 *sh = shift ? shift + (int64_t)(oct ? oct[c] : 0) * nth2 * h2 : nullptr;
-    for (int t = lane; t < nth2; t += 32) {
-      double2 v = conjd(Z[t]);
-      if (sh) v = cmul(v, sh[(int64_t)t * h2 + m]);
-      C[t] = cadd(C[t], v);
+    if (c > c0) __syncthreads();  // previous child's tile consumed
+    for (int w = threadIdx.x; w < nth * nc; w += blockDim.x) {
+      int mm;
+      const int n = fc.div(w, mm);
+      const int m = m0 + mm;
+      if (UP) {
+        const double2 *t = in + (c - cbase) * (int64_t)(nth / 2 + 1) * rowlen;
+        cp_async16(&A[n * cp + mm],
+                   (2 * n <= nth) ? &t[(int64_t)n * rowlen + m] : &t[(int64_t)(nth - n) * rowlen + m + ncols]);
+      } else {
+        const int64_t p = par ? par[c] : c;
+        cp_async16(&A[n * cp + mm], &in[(p * nth + n) * (int64_t)ncols + m]);
+      }
     }
-    __syncwarp();
-  }
-  double2 *o = out + (int64_t)p * nth2 * h2;
-  for (int t = lane; t < nth2; t += 32) o[(int64_t)t * h2 + m] = C[t];
-}
-
-// ------------------------------- downward: columns pass ------------------------------------
-__global__ void __launch_bounds__(32 * FFT_WARPS) cols_down_kernel(const double2 *__restrict__ in, int nph,
-                                                                   const int32_t *__restrict__ par,
-                                                                   const int8_t *__restrict__ oct, int64_t nchild,
-                                                                   const double2 *__restrict__ shift,
-                                                                   FFTLen Lin, FFTLen Lout,
-                                                                   double2 *__restrict__ tmp) {
-  extern __shared__ double2 sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int maxn = max(Lin.N, Lout.N);
-  double2 *A = sm + (size_t)warp * 2 * maxn, *B = A + maxn;
-  const int h = nph / 2;
-  const int64_t seq = (int64_t)blockIdx.x * FFT_WARPS + warp;
-  if (seq >= nchild * h) return;
-  const int64_t c = seq / h;
-  const int m = (int)(seq % h);
-  const int64_t p = par ? par[c] : c;
-  const int nth = Lin.N, nth2 = Lout.N;
-  const double2 *src = in + (int64_t)p * nth * h;
-  const double2 *sh = shift ? shift + (int64_t)(oct ? oct[c] : 0) * nth * h : nullptr;
-  for (int n = lane; n < nth; n += 32) {
-    double2 v = src[(int64_t)n * h + m];
-    if (sh) v = cmul(v, conjd(sh[(int64_t)n * h + m]));  // e^{i kappa s.(c_parent - c_child)}
-    A[n] = v;
-  }
-  __syncwarp();
-  double2 *Z = warp_resample(A, B, Lin, Lout, lane);
-  double2 *o = tmp + (int64_t)c * nth2 * h;
-  for (int t = lane; t < nth2; t += 32) o[(int64_t)t * h + m] = conjd(Z[t]);
-}
-
-// ------------------------------- downward: rows pass (+ add) -------------------------------
-__global__ void __launch_bounds__(32 * FFT_WARPS) rows_down_kernel(const double2 *__restrict__ tmp, int64_t nbox,
-                                                                   int nth2, int nph, FFTLen Lin, FFTLen Lout,
-                                                                   const double2 *__restrict__ add,
-                                                                   double2 *__restrict__ out) {
-  extern __shared__ double2 sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int maxn = max(Lin.N, Lout.N);
-  double2 *A = sm + (size_t)warp * 2 * maxn, *B = A + maxn;
-  const int rows = nth2 / 2 + 1;
-  const int64_t seq = (int64_t)blockIdx.x * FFT_WARPS + warp;
-  if (seq >= nbox * rows) return;
-  const int64_t c = seq / rows;
-  const int n = (int)(seq % rows);
-  const int h = nph / 2, h2 = Lout.N / 2;
-  const double2 *r0 = tmp + ((int64_t)c * nth2 + n) * h;
-  const double2 *r1 = tmp + ((int64_t)c * nth2 + (nth2 - n) % nth2) * h;
-  for (int m = lane; m < nph; m += 32) A[m] = (m < h) ? r0[m] : r1[m - h];
-  __syncwarp();
-  double2 *Z = warp_resample(A, B, Lin, Lout, lane);
-  const int64_t o0 = ((int64_t)c * nth2 + n) * h2;
-  for (int t = lane; t < h2; t += 32) {
-    double2 v = conjd(Z[t]);
-    if (add) v = cadd(v, add[o0 + t]);
-    out[o0 + t] = v;
-  }
-  if (n > 0 && 2 * n < nth2) {
-    const int64_t o1 = ((int64_t)c * nth2 + (nth2 - n)) * h2;
-    for (int t = lane; t < h2; t += 32) {
-      double2 v = conjd(Z[t + h2]);
-      if (add) v = cadd(v, add[o1 + t]);
-      out[o1 + t] = v;
+    cp_async_wait_all();
+    __syncthreads();
+    if (!UP && shift) {  // e^{i kappa s.(c_parent - c_child)} on the parent grid
+      const int64_t so = (int64_t)(oct ? oct[c] : 0) * nth * ncols;
+      for (int w = threadIdx.x; w < nth * nc; w += blockDim.x) {
+        int mm;
+        const int n = fc.div(w, mm);
+        A[n * cp + mm] = c_mul(A[n * cp + mm], c_conj(__ldg(&shift[so + (int64_t)n * ncols + m0 + mm])));
+      }
+      __syncthreads();
+    }
+    double2 *X = fft_batch(A, Bf, vs, L1);
+    double2 *Y = (X == A) ? Bf : A;
+    pad_batch(X, Y, vs, nth, nth2);
+    double2 *Z = fft_batch(Y, X, vs, L2);
+    for (int w = threadIdx.x; w < nth2 * nc; w += blockDim.x) {
+      int mm;
+      const int t = fc.div(w, mm);
+      const int m = m0 + mm;
+      double2 v = c_conj(Z[t * cp + mm]);
+      if (UP) {
+        const int64_t o = (item * nth2 + t) * (int64_t)ncols + m;
+        if (shift) v = c_mul(v, shift[((int64_t)(oct ? oct[c] : 0) * nth2 + t) * ncols + m]);
+        out[o] = (c == c0) ? v : c_add(out[o], v);   // same thread owns o for every child
+      } else {
+        out[(c * nth2 + t) * (int64_t)ncols + m] = v;
+      }
     }
   }
 }
-
-static unsigned nblocks(int64_t seqs) { return (unsigned)((seqs + FFT_WARPS - 1) / FFT_WARPS); }
 
 static void set_smem(const void *fn, size_t bytes) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+static int rows_per_cta(int pitch) {
+  int RB = 1;
+  while (RB < 128 && (size_t)(2 * 2 * RB) * pitch * sizeof(double2) <= kTileSmem) RB *= 2;
+  return RB;
+}
+static int cols_per_cta(int maxn, int ncols) {
+  int CB = 1;
+  while (CB < 32 && CB < ncols && (size_t)2 * maxn * ((2 * CB) | 1) * sizeof(double2) <= kTileSmem) CB *= 2;
+  return CB;
+}
+
+template <bool UP>
+static void launch_rows(const double2 *in, int64_t nbox, int nth, int nph, int nph2, const double2 *add,
+                        double2 *out, const TwiddleSet &tw, cudaStream_t s) {
+  const int64_t total = nbox * (nth / 2 + 1);
+  if (total <= 0) return;
+  const int pitch = std::max(nph, nph2) | 1;
+  const int RB = rows_per_cta(pitch);
+  const size_t smem = (size_t)2 * RB * pitch * sizeof(double2);
+  set_smem((const void *)rows_kernel<UP>, smem);
+  rows_kernel<UP><<<(unsigned)((total + RB - 1) / RB), RS_TPB, smem, s>>>(in, nbox, nth, nph, nph2, RB, pitch,
+                                                                        rlen(tw, nph), rlen(tw, nph2), add, out);
+}
+
+template <bool UP>
+static void launch_cols(const double2 *in, int64_t nitem, int nth, int ncols, int rowlen, int nth2,
+                        const int32_t *cbeg, int64_t cbase, const int32_t *par, const int8_t *oct,
+                        const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
+  if (nitem <= 0 || ncols <= 0) return;
+  const int maxn = std::max(nth, nth2);
+  const int CB = cols_per_cta(maxn, ncols);
+  const int cp = CB | 1;
+  const size_t smem = (size_t)2 * maxn * cp * sizeof(double2);
+  set_smem((const void *)cols_kernel<UP>, smem);
+  const int64_t nstrip = (ncols + CB - 1) / CB;
+  cols_kernel<UP><<<(unsigned)(nitem * nstrip), RS_TPB, smem, s>>>(in, nitem, nth, ncols, rowlen, nth2, CB, cp, cbeg,
+                                                                  cbase, par, oct, shift, rlen(tw, nth),
+                                                                  rlen(tw, nth2), out);
+}
+
 void launch_rows_up(const double2 *in, int64_t nbox, int nth, int nph, int nph2, double2 *tmp,
                     const TwiddleSet &tw, cudaStream_t s) {
-  FFTLen Li = make_len(tw, nph), Lo = make_len(tw, nph2);
-  size_t smem = (size_t)FFT_WARPS * 2 * std::max(nph, nph2) * sizeof(double2);
-  set_smem((const void *)rows_up_kernel, smem);
-  int64_t seqs = nbox * (nth / 2 + 1);
-  if (seqs) rows_up_kernel<<<nblocks(seqs), 32 * FFT_WARPS, smem, s>>>(in, nbox, nth, nph, Li, Lo, tmp);
+  launch_rows<true>(in, nbox, nth, nph, nph2, nullptr, tmp, tw, s);
 }
 
 void launch_cols_up(const double2 *tmp, int nth, int nph2, int nth2, const int32_t *cbeg,
                     int64_t cbase, const int8_t *oct, int64_t nparent, const double2 *shift, double2 *out,
                     const TwiddleSet &tw, cudaStream_t s) {
-  FFTLen Li = make_len(tw, nth), Lo = make_len(tw, nth2);
-  size_t smem = (size_t)FFT_WARPS * 3 * std::max(nth, nth2) * sizeof(double2);
-  set_smem((const void *)cols_up_kernel, smem);
-  int64_t seqs = nparent * (nph2 / 2);
-  if (seqs) cols_up_kernel<<<nblocks(seqs), 32 * FFT_WARPS, smem, s>>>(tmp, nth, nph2, cbeg, cbase, oct, nparent, shift, Li, Lo, out);
+  launch_cols<true>(tmp, nparent, nth, nph2 / 2, nph2, nth2, cbeg, cbase, nullptr, oct, shift, out, tw, s);
 }
 
 void launch_cols_down(const double2 *in, int nth, int nph, int nth2, const int32_t *par,
                       const int8_t *oct, int64_t nchild, const double2 *shift, double2 *tmp,
                       const TwiddleSet &tw, cudaStream_t s) {
-  FFTLen Li = make_len(tw, nth), Lo = make_len(tw, nth2);
-  size_t smem = (size_t)FFT_WARPS * 2 * std::max(nth, nth2) * sizeof(double2);
-  set_smem((const void *)cols_down_kernel, smem);
-  int64_t seqs = nchild * (nph / 2);
-  if (seqs) cols_down_kernel<<<nblocks(seqs), 32 * FFT_WARPS, smem, s>>>(in, nph, par, oct, nchild, shift, Li, Lo, tmp);
+  launch_cols<false>(in, nchild, nth, nph / 2, nph / 2, nth2, nullptr, 0, par, oct, shift, tmp, tw, s);
 }
 
 void launch_rows_down(const double2 *tmp, int64_t nbox, int nth2, int nph, int nph2,
                       const double2 *add, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
-  FFTLen Li = make_len(tw, nph), Lo = make_len(tw, nph2);
-  size_t smem = (size_t)FFT_WARPS * 2 * std::max(nph, nph2) * sizeof(double2);
-  set_smem((const void *)rows_down_kernel, smem);
-  int64_t seqs = nbox * (nth2 / 2 + 1);
-  if (seqs) rows_down_kernel<<<nblocks(seqs), 32 * FFT_WARPS, smem, s>>>(tmp, nbox, nth2, nph, Li, Lo, add, out);
+  launch_rows<false>(tmp, nbox, nth2, nph, nph2, add, out, tw, s);
 }
 
 }  // namespace hfmm
