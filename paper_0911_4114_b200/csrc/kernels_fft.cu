@@ -333,7 +333,10 @@ __device__ __forceinline__ void cp_async16(double2 *smem, const double2 *gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
-static const size_t kTileSmem = 72 * 1024;  // per CTA: three CTAs per SM
+#ifndef HFMM_RS_SMEM_KB
+#define HFMM_RS_SMEM_KB 72
+#endif
+static const size_t kTileSmem = HFMM_RS_SMEM_KB * 1024;  // per CTA (72 KB: three CTAs per SM)
 
 // ---- rows pass --------------------------------------------------------------------------------
 // Row r = (box b, n) for n < nrow = nth/2 + 1 (grid rows n <= N_theta/2).  Input: half storage
