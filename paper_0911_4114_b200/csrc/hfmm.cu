@@ -44,7 +44,6 @@ struct LevelDev {
   double2 *T = nullptr;          // [34][K]: the canonical transfer vectors x >= y >= 0, z >= 0
   int32_t *perm = nullptr;       // [16][K]: grid permutation of each reflection / swap op (NEXT 3)
   double2 *M = nullptr, *I = nullptr, *L = nullptr;  // [nbox][K]
-  int32_t *il_row = nullptr, *il_src = nullptr, *il_sym = nullptr;  // il_sym = canonical id << 4 | op
   M2LGroupPlan *m2lg = nullptr;  // sibling-group M2L plan over the owned boxes
   int64_t il_nnz = 0;
   int32_t *parent = nullptr;     // into level l-1
@@ -156,7 +155,7 @@ static void free_levels(hfmm_plan *p) {
     m2l_group_plan_destroy(L.m2lg);
     L.m2lg = nullptr;
     for (void *ptr : {(void *)L.cx, (void *)L.cy, (void *)L.cz, (void *)L.ks, (void *)L.T, (void *)L.M,
-                      (void *)L.I, (void *)L.L, (void *)L.il_row, (void *)L.il_src, (void *)L.il_sym, (void *)L.perm,
+                      (void *)L.I, (void *)L.L, (void *)L.perm,
                       (void *)L.parent, (void *)L.oct, (void *)L.cbeg, (void *)L.shift})
       if (ptr) cudaFree(ptr);
   }
@@ -541,9 +540,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       return HFMM_E_NOMEM;
     }
     // interaction lists for every box of an active level
-    std::vector<int32_t> row(1, 0), src, oid, oid316;
-    std::vector<int> cids, sym_of;
-    canonical_offsets(cids, sym_of);
+    std::vector<int32_t> row(1, 0), src, oid316;
     for (int64_t b = 0; b < (L.active ? B.nbox() : 0); ++b) {
       const int px = B.ix[b] >> 1, py = B.iy[b] >> 1, pz = B.iz[b] >> 1;
       for (int dx = -3; dx <= 3; ++dx)
@@ -557,12 +554,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
             if (k < 0) continue;
             src.push_back(k);
             oid316.push_back(offset_id(dx, dy, dz));
-            oid.push_back(sym_of[oid316.back()]);
           }
       row.push_back((int32_t)src.size());
     }
     L.il_nnz = (int64_t)src.size();
-    L.il_row = dupload(row), L.il_src = dupload(src), L.il_sym = dupload(oid);
     if (L.active) {
       std::vector<int32_t> pm;
       symmetry_perms(L.nth, L.nph, pm);

@@ -138,11 +138,6 @@ void launch_l2t_small(PointsDev pts, const int64_t *first, const double *cx, con
                       int32_t box0, int32_t box1, const double *ks, int64_t K, const double2 *L, double w,
                       double2 *y_far, cudaStream_t s);
 
-// M2L: I[a][k] = sum_e T[oid_e][k] M[src_e][k]
-void launch_m2l(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
-                const int32_t *oid, const double2 *T, const double2 *M, double2 *I,
-                cudaStream_t s);
-
 // Sibling-group M2L (kernels_m2l.cu): plan once per level / operator, apply per matvec.
 struct M2LGroupPlan;
 // targets = boxes [0, nbox) with host CSR row/src/oid (oid = offset id 0..315); groups
@@ -153,11 +148,6 @@ void m2l_group_plan_destroy(M2LGroupPlan *pl);
 // T: [316][K] (perm == nullptr) or the 34 canonical tables [34][K] with perm [16][K]
 void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *perm, const double2 *M, double2 *I,
                      cudaStream_t s);
-
-// M2L with the 34 canonical tables: T[sym_e >> 4][perm[sym_e & 15][k]]
-void launch_m2l_sym(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
-                    const int32_t *sym, const int32_t *perm, const double2 *T /*[34][K]*/, const double2 *M,
-                    double2 *I, cudaStream_t s);
 
 // Fourier resampling building blocks, warp-per-sequence shared-memory FFTs.
 // Row pass of an upward resample: for each box b and row n <= nth/2, full row of length nph

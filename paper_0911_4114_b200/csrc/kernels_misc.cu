@@ -1,5 +1,4 @@
-// M2L transfer pass and the GPU side of the precompute (product code, sm_100a).
-//   M2L   I^l_a(s) = sum_{b in I(B_a)} M^l_b(s) T_{l, c_b - c_a}(s)
+// GPU side of the precompute (product code, sm_100a); the M2L pass is in kernels_m2l.cu.
 //   Alg.1 bandlimited modified transfer function T^{s,L}, one CTA per (offset, phi column)
 //         (P:508-530); phi-truncation to T^{s,LL} when N_phi < 2 ell + 2
 #include <cuda_runtime.h>
@@ -11,83 +10,6 @@ namespace hfmm {
 
 __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // a*b + c
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
-}
-
-// ------------------------------------ M2L --------------------------------------------------
-// grid: (k tiles, target boxes); thread per direction k; interaction list read by broadcast.
-constexpr int M2L_TPB = 256;
-
-__global__ void __launch_bounds__(M2L_TPB) m2l_kernel(int32_t box0, int64_t K, const int32_t *__restrict__ row,
-                                                      const int32_t *__restrict__ src,
-                                                      const int32_t *__restrict__ oid,
-                                                      const double2 *__restrict__ T,
-                                                      const double2 *__restrict__ M,
-                                                      double2 *__restrict__ I) {
-  const int32_t a = box0 + blockIdx.x;   // boxes on x (gridDim.y is limited to 65535)
-  const int64_t k = (int64_t)blockIdx.y * M2L_TPB + threadIdx.x;
-  if (k >= K) return;
-  double2 acc = make_double2(0.0, 0.0);
-  const int32_t e0 = row[a], e1 = row[a + 1];
-  int32_t e = e0;
-  for (; e + 1 < e1; e += 2) {  // two partners in flight
-    const double2 t0 = __ldg(&T[(int64_t)oid[e] * K + k]);
-    const double2 m0 = __ldg(&M[(int64_t)src[e] * K + k]);
-    const double2 t1 = __ldg(&T[(int64_t)oid[e + 1] * K + k]);
-    const double2 m1 = __ldg(&M[(int64_t)src[e + 1] * K + k]);
-    acc = cfma(t0, m0, acc);
-    acc = cfma(t1, m1, acc);
-  }
-  if (e < e1) acc = cfma(__ldg(&T[(int64_t)oid[e] * K + k]), __ldg(&M[(int64_t)src[e] * K + k]), acc);
-  I[(int64_t)a * K + k] = acc;
-}
-
-void launch_m2l(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
-                const int32_t *oid, const double2 *T, const double2 *M, double2 *I, cudaStream_t s) {
-  if (box1 <= box0 || K <= 0) return;
-  dim3 grid((unsigned)(box1 - box0), (unsigned)((K + M2L_TPB - 1) / M2L_TPB));
-  m2l_kernel<<<grid, M2L_TPB, 0, s>>>(box0, K, row, src, oid, T, M, I);
-}
-
-// M2L with the 34 canonical tables (NEXT 3): the table of interaction e is
-// T[c_e][perm[op_e][k]], c_e / op_e packed in sym[e] = c << 4 | op (reflection / swap op).  The
-// permuted reads are reversed runs of a row (reflections) and stay coalesced.
-__global__ void __launch_bounds__(M2L_TPB) m2l_sym_kernel(int32_t box0, int64_t K, const int32_t *__restrict__ row,
-                                                          const int32_t *__restrict__ src,
-                                                          const int32_t *__restrict__ sym,
-                                                          const int32_t *__restrict__ perm,
-                                                          const double2 *__restrict__ T,
-                                                          const double2 *__restrict__ M,
-                                                          double2 *__restrict__ I) {
-  const int32_t a = box0 + blockIdx.x;
-  const int64_t k = (int64_t)blockIdx.y * M2L_TPB + threadIdx.x;
-  if (k >= K) return;
-  double2 acc = make_double2(0.0, 0.0);
-  const int32_t e0 = row[a], e1 = row[a + 1];
-  int32_t e = e0;
-  for (; e + 1 < e1; e += 2) {  // two partners in flight
-    const int32_t c0 = sym[e], c1 = sym[e + 1];
-    const int32_t p0 = __ldg(&perm[(int64_t)(c0 & 15) * K + k]), p1 = __ldg(&perm[(int64_t)(c1 & 15) * K + k]);
-    const double2 t0 = __ldg(&T[(int64_t)(c0 >> 4) * K + p0]);
-    const double2 m0 = __ldg(&M[(int64_t)src[e] * K + k]);
-    const double2 t1 = __ldg(&T[(int64_t)(c1 >> 4) * K + p1]);
-    const double2 m1 = __ldg(&M[(int64_t)src[e + 1] * K + k]);
-    acc = cfma(t0, m0, acc);
-    acc = cfma(t1, m1, acc);
-  }
-  if (e < e1) {
-    const int32_t c0 = sym[e];
-    const int32_t p0 = __ldg(&perm[(int64_t)(c0 & 15) * K + k]);
-    acc = cfma(__ldg(&T[(int64_t)(c0 >> 4) * K + p0]), __ldg(&M[(int64_t)src[e] * K + k]), acc);
-  }
-  I[(int64_t)a * K + k] = acc;
-}
-
-void launch_m2l_sym(int32_t box0, int32_t box1, int64_t K, const int32_t *row, const int32_t *src,
-                    const int32_t *sym, const int32_t *perm, const double2 *T, const double2 *M, double2 *I,
-                    cudaStream_t s) {
-  if (box1 <= box0 || K <= 0) return;
-  dim3 grid((unsigned)(box1 - box0), (unsigned)((K + M2L_TPB - 1) / M2L_TPB));
-  m2l_sym_kernel<<<grid, M2L_TPB, 0, s>>>(box0, K, row, src, sym, perm, T, M, I);
 }
 
 // ------------------------------------ Alg. 1 -----------------------------------------------
