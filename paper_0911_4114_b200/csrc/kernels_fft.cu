@@ -31,6 +31,7 @@
 
 #include "hfmm_impl.h"
 
+
 namespace hfmm {
 
 void TwiddleSet::build(const std::vector<int> &lengths) {
@@ -66,7 +67,7 @@ struct RLen {
   const double2 *tw;  // e^{-2 pi i t / N}, t < N (global, L1-resident)
 };
 
-static RLen rlen(const TwiddleSet &ts, int N) {
+static RLen rlen(const TwiddleSet &ts, int N, int maxr) {
   RLen L{};
   L.N = N;
   int m = N, e = 0;
@@ -74,7 +75,12 @@ static RLen rlen(const TwiddleSet &ts, int N) {
   auto push = [&](int code) { L.codes |= (unsigned)code << (3 * L.nr++); };
   // powers of two as radix-16 passes plus at most one 8 / 4 (no radix-2 pass unless N has a single 2)
   if (e == 1) push(3);
-  else {
+  else if (maxr < 16) {  // radix-8 passes (fewer registers per thread)
+    int e8 = e / 3, rest = e % 3;
+    if (rest == 1 && e8 > 0) --e8, push(2), push(2);  // 2^4 = 4 * 4
+    for (int i = 0; i < e8; ++i) push(1);
+    if (rest == 2) push(2);
+  } else {
     int e16 = e / 4, rest = e % 4;
     if (rest == 1 && e16 > 0) --e16, push(1), push(2);  // 2^5 = 8 * 4
     for (int i = 0; i < e16; ++i) push(0);
@@ -280,13 +286,17 @@ __device__ __forceinline__ void stockham_pass(const double2 *__restrict__ src, d
 }
 
 // forward FFT of every vector (length L.N) in buffer a, ping-pong with b; returns the result buffer
+template <int MAXR>
 __device__ __forceinline__ double2 *fft_batch(double2 *a, double2 *b, const VecSet &vs, const RLen &L) {
   double2 *src = a, *dst = b;
   int Ns = 1;
   for (int s = 0; s < L.nr; ++s) {
     int R;
     switch ((L.codes >> (3 * s)) & 7u) {
-      case 0: stockham_pass<16>(src, dst, vs, L.N, Ns, L.tw); R = 16; break;
+      case 0:
+        if (MAXR >= 16) stockham_pass<MAXR >= 16 ? 16 : 8>(src, dst, vs, L.N, Ns, L.tw);
+        R = 16;
+        break;
       case 1: stockham_pass<8>(src, dst, vs, L.N, Ns, L.tw); R = 8; break;
       case 2: stockham_pass<4>(src, dst, vs, L.N, Ns, L.tw); R = 4; break;
       case 3: stockham_pass<2>(src, dst, vs, L.N, Ns, L.tw); R = 2; break;
@@ -333,17 +343,12 @@ __device__ __forceinline__ void cp_async16(double2 *smem, const double2 *gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
-#ifndef HFMM_RS_SMEM_KB
-#define HFMM_RS_SMEM_KB 72
-#endif
-static const size_t kTileSmem = HFMM_RS_SMEM_KB * 1024;  // per CTA (72 KB: three CTAs per SM)
-
 // ---- rows pass --------------------------------------------------------------------------------
 // Row r = (box b, n) for n < nrow = nth/2 + 1 (grid rows n <= N_theta/2).  Input: half storage
 // [nth][h] of box b; full row e < nph = (row n)[e] for e < h, (row (nth - n) % nth)[e - h] beyond
 // (eqn:NumSphereSym).  UP: output full rows of length nph2 to out[b][n][.]; DOWN: output back to
 // half storage out[b][n][t < h2] and out[b][nth - n][t - h2] (+ add).
-template <bool UP>
+template <bool UP, int MAXR>
 __global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict__ in, int64_t nbox, int nth,
                                                       int nph, int nph2, int RB, int pitch, RLen L1, RLen L2,
                                                       const double2 *__restrict__ add, double2 *__restrict__ out) {
@@ -367,10 +372,10 @@ __global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict_
   cp_async_wait_all();
   __syncthreads();
   const VecSet vs{nr, nr, 0, pitch, 1};
-  double2 *X = fft_batch(A, Bf, vs, L1);
+  double2 *X = fft_batch<MAXR>(A, Bf, vs, L1);
   double2 *Y = (X == A) ? Bf : A;
   pad_batch(X, Y, vs, nph, nph2);
-  double2 *Z = fft_batch(Y, X, vs, L2);  // conj of the resampled rows
+  double2 *Z = fft_batch<MAXR>(Y, X, vs, L2);  // conj of the resampled rows
   const FDiv fn2(nph2);
   for (int w = threadIdx.x; w < nr * nph2; w += blockDim.x) {
     int t;
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict_
 // nth -> nth2, times shift[oct[c]][t][m], summed over the children into out[p][t][m].
 // DOWN (L2L): item = child c, columns m < h of conj(shift[oct[c]]) * in[par[c]] ([nth][h]),
 // resampled nth -> nth2 into out[c][t][m] ([nth2][h]).
-template <bool UP>
+template <bool UP, int MAXR>
 __global__ void __launch_bounds__(RS_TPB) cols_kernel(const double2 *__restrict__ in, int64_t nitem, int nth,
                                                       int ncols, int rowlen, int nth2, int CB, int cp,
                                                       const int32_t *__restrict__ cbeg, int64_t cbase,
@@ -448,10 +453,10 @@ __global__ void __launch_bounds__(RS_TPB) cols_kernel(const double2 *__restrict_
       }
       __syncthreads();
     }
-    double2 *X = fft_batch(A, Bf, vs, L1);
+    double2 *X = fft_batch<MAXR>(A, Bf, vs, L1);
     double2 *Y = (X == A) ? Bf : A;
     pad_batch(X, Y, vs, nth, nth2);
-    double2 *Z = fft_batch(Y, X, vs, L2);
+    double2 *Z = fft_batch<MAXR>(Y, X, vs, L2);
     for (int w = threadIdx.x; w < nth2 * nc; w += blockDim.x) {
       int mm;
       const int t = fc.div(w, mm);
@@ -468,32 +473,63 @@ __global__ void __launch_bounds__(RS_TPB) cols_kernel(const double2 *__restrict_
   }
 }
 
+// Tile plan per size (A/B on the C2 sizes): grids of <= 128 points use radix <= 8 butterflies
+// (~75 registers) in 48 KB tiles; larger grids radix-16 butterflies (~140 registers) in 72 KB tiles.
+struct TilePlan {
+  int maxr;
+  size_t smem_budget;
+};
+static TilePlan tile_plan(int maxn) { return maxn > 128 ? TilePlan{16, 72 * 1024} : TilePlan{8, 48 * 1024}; }
+
 static void set_smem(const void *fn, size_t bytes) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-static int rows_per_cta(int pitch) {
+static int rows_per_cta(int pitch, size_t budget) {
   int RB = 1;
-  while (RB < 128 && (size_t)(2 * 2 * RB) * pitch * sizeof(double2) <= kTileSmem) RB *= 2;
+  while (RB < 128 && (size_t)(2 * 2 * RB) * pitch * sizeof(double2) <= budget) RB *= 2;
   return RB;
 }
-static int cols_per_cta(int maxn, int ncols) {
+static int cols_per_cta(int maxn, int ncols, size_t budget) {
   int CB = 1;
-  while (CB < 32 && CB < ncols && (size_t)2 * maxn * ((2 * CB) | 1) * sizeof(double2) <= kTileSmem) CB *= 2;
+  while (CB < 32 && CB < ncols && (size_t)2 * maxn * ((2 * CB) | 1) * sizeof(double2) <= budget) CB *= 2;
   return CB;
+}
+
+template <bool UP, int MAXR>
+static void launch_rows_t(const double2 *in, int64_t nbox, int nth, int nph, int nph2, const double2 *add,
+                          double2 *out, size_t budget, const TwiddleSet &tw, cudaStream_t s) {
+  const int64_t total = nbox * (nth / 2 + 1);
+  const int pitch = std::max(nph, nph2) | 1;
+  const int RB = rows_per_cta(pitch, budget);
+  const size_t smem = (size_t)2 * RB * pitch * sizeof(double2);
+  set_smem((const void *)rows_kernel<UP, MAXR>, smem);
+  rows_kernel<UP, MAXR><<<(unsigned)((total + RB - 1) / RB), RS_TPB, smem, s>>>(
+      in, nbox, nth, nph, nph2, RB, pitch, rlen(tw, nph, MAXR), rlen(tw, nph2, MAXR), add, out);
 }
 
 template <bool UP>
 static void launch_rows(const double2 *in, int64_t nbox, int nth, int nph, int nph2, const double2 *add,
                         double2 *out, const TwiddleSet &tw, cudaStream_t s) {
-  const int64_t total = nbox * (nth / 2 + 1);
-  if (total <= 0) return;
-  const int pitch = std::max(nph, nph2) | 1;
-  const int RB = rows_per_cta(pitch);
-  const size_t smem = (size_t)2 * RB * pitch * sizeof(double2);
-  set_smem((const void *)rows_kernel<UP>, smem);
-  rows_kernel<UP><<<(unsigned)((total + RB - 1) / RB), RS_TPB, smem, s>>>(in, nbox, nth, nph, nph2, RB, pitch,
-                                                                        rlen(tw, nph), rlen(tw, nph2), add, out);
+  if (nbox * (nth / 2 + 1) <= 0) return;
+  const TilePlan tp = tile_plan(std::max(nph, nph2));
+  if (tp.maxr >= 16) launch_rows_t<UP, 16>(in, nbox, nth, nph, nph2, add, out, tp.smem_budget, tw, s);
+  else launch_rows_t<UP, 8>(in, nbox, nth, nph, nph2, add, out, tp.smem_budget, tw, s);
+}
+
+template <bool UP, int MAXR>
+static void launch_cols_t(const double2 *in, int64_t nitem, int nth, int ncols, int rowlen, int nth2,
+                          const int32_t *cbeg, int64_t cbase, const int32_t *par, const int8_t *oct,
+                          const double2 *shift, double2 *out, size_t budget, const TwiddleSet &tw, cudaStream_t s) {
+  const int maxn = std::max(nth, nth2);
+  const int CB = cols_per_cta(maxn, ncols, budget);
+  const int cp = CB | 1;
+  const size_t smem = (size_t)2 * maxn * cp * sizeof(double2);
+  set_smem((const void *)cols_kernel<UP, MAXR>, smem);
+  const int64_t nstrip = (ncols + CB - 1) / CB;
+  cols_kernel<UP, MAXR><<<(unsigned)(nitem * nstrip), RS_TPB, smem, s>>>(
+      in, nitem, nth, ncols, rowlen, nth2, CB, cp, cbeg, cbase, par, oct, shift, rlen(tw, nth, MAXR),
+      rlen(tw, nth2, MAXR), out);
 }
 
 template <bool UP>
@@ -501,15 +537,11 @@ static void launch_cols(const double2 *in, int64_t nitem, int nth, int ncols, in
                         const int32_t *cbeg, int64_t cbase, const int32_t *par, const int8_t *oct,
                         const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
   if (nitem <= 0 || ncols <= 0) return;
-  const int maxn = std::max(nth, nth2);
-  const int CB = cols_per_cta(maxn, ncols);
-  const int cp = CB | 1;
-  const size_t smem = (size_t)2 * maxn * cp * sizeof(double2);
-  set_smem((const void *)cols_kernel<UP>, smem);
-  const int64_t nstrip = (ncols + CB - 1) / CB;
-  cols_kernel<UP><<<(unsigned)(nitem * nstrip), RS_TPB, smem, s>>>(in, nitem, nth, ncols, rowlen, nth2, CB, cp, cbeg,
-                                                                  cbase, par, oct, shift, rlen(tw, nth),
-                                                                  rlen(tw, nth2), out);
+  const TilePlan tp = tile_plan(std::max(nth, nth2));
+  if (tp.maxr >= 16)
+    launch_cols_t<UP, 16>(in, nitem, nth, ncols, rowlen, nth2, cbeg, cbase, par, oct, shift, out, tp.smem_budget, tw, s);
+  else
+    launch_cols_t<UP, 8>(in, nitem, nth, ncols, rowlen, nth2, cbeg, cbase, par, oct, shift, out, tp.smem_budget, tw, s);
 }
 
 void launch_rows_up(const double2 *in, int64_t nbox, int nth, int nph, int nph2, double2 *tmp,
