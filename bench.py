@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ops", default="8,16,32,64",
                     help="C2 operator microbench bandwidths B (comma list; '' to skip)")
+    ap.add_argument("--extra", default="C3,C5",
+                    help="other BASELINE matvec configs timed after the main one (comma list; '' to skip)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -271,6 +273,43 @@ def bench_operators(bandwidths, reps: int = 5, fp64_peak_tflops: float = 37.2):
     return out
 
 
+def bench_matvec_config(cfg, warmup: int, steps: int):
+    """One more BASELINE matvec config on this GPU (context for the main line): ms per matvec with
+    q resident, L2 flushed between steps, CUDA events on the launching stream."""
+    import torch
+    import paper_0911_4114_b200 as hf
+    from workloads import points_and_charges
+    x, q = points_and_charges(cfg)
+    g = hf.HFMM(0)
+    g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha)
+    info = g.info()
+    qd = torch.from_numpy(q).cuda()
+    yd = torch.empty_like(qd)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        g.matvec(qd, out=yd)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        g.matvec(qd, out=yd)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.mean(ms)
+    out = {"n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps, "geometry": cfg.kind,
+           "L_f": info["L_f"], "source_level": info["source_level"], "ms_per_matvec": t, "matvec_per_s": 1e3 / t,
+           "mpoints_per_s": cfg.n / t / 1e3, "p2p_pairs": info["p2p_pairs"], "steps": steps}
+    g.close()
+    del qd, yd, flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the CPU oracle, each step a bounded sample, on rank 0 only."""
     if rank != 0:
@@ -425,10 +464,14 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s, desc, cores = oracle_sample(cfg, x, q)
         line["cpu_baseline"] = {"value": 1.0 / s, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": desc}
-    if world == 1 and args.ops:
+    if world == 1 and (args.ops or args.extra):
         g.close()
         del qd, yd, flush, qh, yh
         torch.cuda.empty_cache()
+    if world == 1 and args.extra:
+        line["other_configs"] = {name: bench_matvec_config(CONFIGS[name], args.warmup, max(3, args.steps // 2))
+                                 for name in args.extra.split(",") if name and name != cfg.name}
+    if world == 1 and args.ops:
         line["operators"] = bench_operators([int(b) for b in args.ops.split(",")], fp64_peak_tflops=peak_tflops)
     if rank == 0:
         print(json.dumps(line), flush=True)
