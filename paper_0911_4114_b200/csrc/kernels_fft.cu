@@ -313,26 +313,82 @@ __device__ __forceinline__ double2 *fft_batch(double2 *a, double2 *b, const VecS
   return src;
 }
 
-// spectrum X (length N) -> conj(Y / N) on length N2, band |f| <= (min(N, N2) - 1) / 2 (R-6)
-__device__ __forceinline__ void pad_batch(const double2 *__restrict__ X, double2 *__restrict__ Y, const VecSet &vs, int N, int N2) {
-  const int K = (min(N, N2) - 1) / 2, total = vs.nvec * N2, es = vs.estride;
+// First pass (Ns = 1) of the inverse transform reading the padded spectrum on the fly: input
+// element i < N2 of a vector is conj(X[f] / N) for f = i (i <= N2/2) or i - N2, |f| <= K, else 0
+// (R-6) -- the pad never touches shared memory.
+template <int R>
+__device__ __forceinline__ void stockham_pass_padin(const double2 *__restrict__ X, double2 *__restrict__ dst,
+                                                    const VecSet &vs, int N, int N2) {
+  const int nb = N2 / R, total = vs.nvec * nb, es = vs.estride;
+  const int K = (min(N, N2) - 1) / 2;
   const double sc = 1.0 / (double)N;
   const FDiv fv(vs.nvec), fper(vs.vper);
   for (int w = threadIdx.x; w < total; w += blockDim.x) {
     int v;
-    const int t = fv.div(w, v);
-    const int f = (t <= N2 / 2) ? t : t - N2;
+    const int j = fv.div(w, v);
     const int b = vbase(vs, fper, v);
-    double2 val = make_double2(0.0, 0.0);
-    if (f <= K && f >= -K) {
-      const double2 x = X[b + (f >= 0 ? f : f + N) * es];
-      val = make_double2(x.x * sc, -x.y * sc);
+    double2 x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = j + r * nb;
+      const int f = (i <= N2 / 2) ? i : i - N2;
+      double2 val = make_double2(0.0, 0.0);
+      if (f <= K && f >= -K) {
+        const double2 y = X[b + (f >= 0 ? f : f + N) * es];
+        val = make_double2(y.x * sc, -y.y * sc);
+      }
+      x[r] = val;
     }
-    Y[b + t * es] = val;
+    dft<R>(x);
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[b + (j * R + r) * es] = x[r];
   }
-  __syncthreads();
 }
 
+// inverse resample half: forward FFT (length L.N = N2) of the padded conj spectrum of X (length
+// N, in buffer a or b); returns the buffer with the result (conj of the resampled values)
+template <int MAXR>
+__device__ __forceinline__ double2 *fft_batch_padin(double2 *X, double2 *a, double2 *b, const VecSet &vs,
+                                                    const RLen &L, int N) {
+  double2 *dst = (X == a) ? b : a;
+  int R0;
+  switch (L.codes & 7u) {
+    case 0:
+      if (MAXR >= 16) stockham_pass_padin<MAXR >= 16 ? 16 : 8>(X, dst, vs, N, L.N);
+      R0 = 16;
+      break;
+    case 1: stockham_pass_padin<8>(X, dst, vs, N, L.N); R0 = 8; break;
+    case 2: stockham_pass_padin<4>(X, dst, vs, N, L.N); R0 = 4; break;
+    case 3: stockham_pass_padin<2>(X, dst, vs, N, L.N); R0 = 2; break;
+    case 4: stockham_pass_padin<3>(X, dst, vs, N, L.N); R0 = 3; break;
+    case 5: stockham_pass_padin<5>(X, dst, vs, N, L.N); R0 = 5; break;
+    default: stockham_pass_padin<7>(X, dst, vs, N, L.N); R0 = 7; break;
+  }
+  __syncthreads();
+  double2 *src = dst, *nxt = X;
+  int Ns = R0;
+  for (int s = 1; s < L.nr; ++s) {
+    int R;
+    switch ((L.codes >> (3 * s)) & 7u) {
+      case 0:
+        if (MAXR >= 16) stockham_pass<MAXR >= 16 ? 16 : 8>(src, nxt, vs, L.N, Ns, L.tw);
+        R = 16;
+        break;
+      case 1: stockham_pass<8>(src, nxt, vs, L.N, Ns, L.tw); R = 8; break;
+      case 2: stockham_pass<4>(src, nxt, vs, L.N, Ns, L.tw); R = 4; break;
+      case 3: stockham_pass<2>(src, nxt, vs, L.N, Ns, L.tw); R = 2; break;
+      case 4: stockham_pass<3>(src, nxt, vs, L.N, Ns, L.tw); R = 3; break;
+      case 5: stockham_pass<5>(src, nxt, vs, L.N, Ns, L.tw); R = 5; break;
+      default: stockham_pass<7>(src, nxt, vs, L.N, Ns, L.tw); R = 7; break;
+    }
+    __syncthreads();
+    double2 *t = src;
+    src = nxt;
+    nxt = t;
+    Ns *= R;
+  }
+  return src;
+}
 
 constexpr int RS_TPB = 128;
 
@@ -373,9 +429,7 @@ __global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict_
   __syncthreads();
   const VecSet vs{nr, nr, 0, pitch, 1};
   double2 *X = fft_batch<MAXR>(A, Bf, vs, L1);
-  double2 *Y = (X == A) ? Bf : A;
-  pad_batch(X, Y, vs, nph, nph2);
-  double2 *Z = fft_batch<MAXR>(Y, X, vs, L2);  // conj of the resampled rows
+  double2 *Z = fft_batch_padin<MAXR>(X, A, Bf, vs, L2, nph);  // conj of the resampled rows
   const FDiv fn2(nph2);
   for (int w = threadIdx.x; w < nr * nph2; w += blockDim.x) {
     int t;
@@ -454,9 +508,7 @@ __global__ void __launch_bounds__(RS_TPB) cols_kernel(const double2 *__restrict_
       __syncthreads();
     }
     double2 *X = fft_batch<MAXR>(A, Bf, vs, L1);
-    double2 *Y = (X == A) ? Bf : A;
-    pad_batch(X, Y, vs, nth, nth2);
-    double2 *Z = fft_batch<MAXR>(Y, X, vs, L2);
+    double2 *Z = fft_batch_padin<MAXR>(X, A, Bf, vs, L2, nth);
     for (int w = threadIdx.x; w < nth2 * nc; w += blockDim.x) {
       int mm;
       const int t = fc.div(w, mm);
