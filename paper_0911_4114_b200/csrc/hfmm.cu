@@ -19,6 +19,10 @@
 #include "hfmm_impl.h"
 #include "../../include/hfmm.h"
 
+#ifndef HFMM_STREAM_PRIORITY
+#define HFMM_STREAM_PRIORITY 1
+#endif
+
 using namespace hfmm;
 
 namespace {
@@ -86,8 +90,8 @@ TwiddleSet &global_twiddles(int device) {
 
 struct hfmm_plan {
   int device = 0;
-  cudaStream_t stream = nullptr, stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t stream = nullptr, stream2 = nullptr, stream_hi = nullptr;  // near field low, far chain high priority
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join_hi = nullptr;
   std::string err;
   bool have_tree = false, have_plan = false;
   Tree tree;
@@ -201,9 +205,22 @@ extern "C" int hfmm_create(hfmm_plan **out, int device) {
   p->device = device;
   cudaSetDevice(device);
   CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+  {
+    // The far-field chain (latency-bound resampling, M2L, S2M/L2T) runs at high priority so its
+    // CTAs take SM slots as soon as CTAs of the FP64-bound near field (low priority) retire.
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+#if HFMM_STREAM_PRIORITY
+    CK(cudaStreamCreateWithPriority(&p->stream2, cudaStreamNonBlocking, lo));
+    CK(cudaStreamCreateWithPriority(&p->stream_hi, cudaStreamNonBlocking, hi));
+#else
+    CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->stream_hi, cudaStreamNonBlocking));
+#endif
+  }
   CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&p->ev_join_hi, cudaEventDisableTiming));
   for (auto &e : p->sev) CK(cudaEventCreate(&e));
   const char *prof = std::getenv("HFMM_PROFILE_STAGES");
   p->profile = prof && prof[0] && prof[0] != '0';
@@ -766,16 +783,18 @@ static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
   return HFMM_OK;
 }
 
-static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
+static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user) {
   const Tree &t = p->tree;
   const int64_t n = t.n;
   const bool prof = p->profile;
-  if (prof) cudaEventRecord(p->sev[0], s);
-  launch_permute_q(q_dev, p->perm, p->q_sorted, n, s);
+  if (prof) cudaEventRecord(p->sev[0], s_user);
+  launch_permute_q(q_dev, p->perm, p->q_sorted, n, s_user);
   PointsDev pts{p->px, p->py, p->pz, p->q_sorted};
-  // near field on the second stream, concurrent with the far-field chain
-  CK(cudaEventRecord(p->ev_fork, s));
+  // near field (low priority) and far-field chain (high priority) forked from the caller's stream
+  CK(cudaEventRecord(p->ev_fork, s_user));
   CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
+  CK(cudaStreamWaitEvent(p->stream_hi, p->ev_fork, 0));
+  cudaStream_t s = p->stream_hi;
   if (prof) cudaEventRecord(p->sev[7], p->stream2);
   CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), p->stream2));
   {
@@ -837,9 +856,11 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s) {
   } else if (prof) {
     for (int k = 1; k <= 5; ++k) cudaEventRecord(p->sev[k], s);
   }
-  CK(cudaStreamWaitEvent(s, p->ev_join, 0));
-  launch_combine(p->y_near, p->L_f >= 2 ? p->y_far : nullptr, p->perm, p->y_out, n, p->own_pt0, p->own_pt1, s);
-  if (prof) cudaEventRecord(p->sev[6], s);
+  CK(cudaEventRecord(p->ev_join_hi, s));
+  CK(cudaStreamWaitEvent(s_user, p->ev_join, 0));
+  CK(cudaStreamWaitEvent(s_user, p->ev_join_hi, 0));
+  launch_combine(p->y_near, p->L_f >= 2 ? p->y_far : nullptr, p->perm, p->y_out, n, p->own_pt0, p->own_pt1, s_user);
+  if (prof) cudaEventRecord(p->sev[6], s_user);
   CK(cudaGetLastError());
   return HFMM_OK;
 }
@@ -1014,6 +1035,8 @@ extern "C" void hfmm_destroy(hfmm_plan *p) {
     if (e) cudaEventDestroy(e);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
+  if (p->ev_join_hi) cudaEventDestroy(p->ev_join_hi);
+  if (p->stream_hi) cudaStreamDestroy(p->stream_hi);
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->stream2) cudaStreamDestroy(p->stream2);
   delete p;

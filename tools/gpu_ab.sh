@@ -1,6 +1,6 @@
 # A/B timing of kernel variants (HFMM_LIB) on the C4 bench; parity of each variant first
 mkdir -p gpurun_out
-for v in t3m4 t4m3 t2m5; do
+for v in "" noprio; do
   lib=""; [ -n "$v" ] && lib="$PWD/paper_0911_4114_b200/libhfmm_$v.so"
   HFMM_LIB=$lib timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "small or deep or c1" 2>&1 | tail -2 > gpurun_out/ab_test_$v.log
   HFMM_LIB=$lib timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --ops "" > gpurun_out/ab_bench_$v.log 2>&1
