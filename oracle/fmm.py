@@ -24,8 +24,8 @@ from typing import Dict, Optional
 import numpy as np
 
 from .plan import Plan
-from .resample import resample_half_batch
-from .transfer import shat, bmtf_table
+from .resample import resample_half_batch, resample_ragged
+from .transfer import shat, bmtf_table, bmtf_table_rows
 from .tree import build_level, neighbours, interaction_list, parent
 
 
@@ -46,18 +46,39 @@ class OracleFMM:
 
     # ---- quadrature of level l (half storage) -----------------------
     def grid(self, l: int):
+        """Stored directions, row by row: theta_n = 2 pi n / N_theta, phi = 2 pi m / N_phi(theta_n),
+        m < N_phi(theta_n)/2 (rectangular: k = n * (N_phi/2) + m; ragged rows R-15)."""
         lp = self.plan.levels[l]
-        th = 2 * math.pi * np.arange(lp.n_theta) / lp.n_theta
-        ph = 2 * math.pi * np.arange(lp.n_phi // 2) / lp.n_phi
-        TH, PH = np.meshgrid(th, ph, indexing="ij")
-        return shat(TH, PH).reshape(-1, 3)                       # [K, 3], k = n * (N_phi/2) + m
+        th, ph = self.grid_angles(l)
+        return shat(th, ph)                                      # [K, 3]
+
+    def grid_angles(self, l: int):
+        lp = self.plan.levels[l]
+        rows = lp.row_nphi()
+        th = np.concatenate([np.full(r // 2, 2 * math.pi * n / lp.n_theta) for n, r in enumerate(rows)])
+        ph = np.concatenate([2 * math.pi * np.arange(r // 2) / r for r in rows])
+        return th, ph
+
+    def ragged(self, l: int) -> bool:
+        return self.plan.levels[l].rows is not None
+
+    def resample(self, F: np.ndarray, l_from: int, l_to: int) -> np.ndarray:
+        """5-step resample of one stored field between the quadratures of two levels."""
+        a, b = self.plan.levels[l_from], self.plan.levels[l_to]
+        if a.rows is None and b.rows is None:
+            return resample_half_batch(F.reshape(1, a.n_theta, a.n_phi // 2), a.n_phi, b.n_theta,
+                                       b.n_phi).reshape(-1)
+        return resample_ragged(F, a.row_nphi(), b.n_theta, b.row_nphi())
 
     def table(self, l: int, o) -> np.ndarray:
         key = (l, tuple(int(v) for v in o))
         if key not in self._tables:
             lp = self.plan.levels[l]
             r0 = np.asarray(o, dtype=np.float64) * lp.a
-            self._tables[key] = bmtf_table(lp.ell, self.kappa, r0, lp.n_theta, lp.n_phi).reshape(-1)
+            if lp.rows is not None:
+                self._tables[key] = bmtf_table_rows(lp.ell, self.kappa, r0, lp.n_theta, lp.rows)
+            else:
+                self._tables[key] = bmtf_table(lp.ell, self.kappa, r0, lp.n_theta, lp.n_phi).reshape(-1)
         return self._tables[key]
 
     # ---- passes ---------------------------------------------------------------
@@ -75,12 +96,10 @@ class OracleFMM:
     def m2m(self, Ml: Dict[int, np.ndarray], l: int) -> Dict[int, np.ndarray]:
         """Level l -> l-1: interpolate, multiply by e^{i kappa s.(c_b - c_a)}, accumulate."""
         ch, pa = self.levels[l], self.levels[l - 1]
-        lc, lpp = self.plan.levels[l], self.plan.levels[l - 1]
         Sp = self.grid(l - 1)
         out = {}
         for b, M in Ml.items():
-            Mi = resample_half_batch(M.reshape(1, lc.n_theta, lc.n_phi // 2), lc.n_phi,
-                                     lpp.n_theta, lpp.n_phi).reshape(-1)
+            Mi = self.resample(M, l, l - 1)
             p = pa.index[parent(ch.boxes[b])]
             shift = np.exp(1j * self.kappa * (Sp @ (ch.centers[b] - pa.centers[p])))
             out[p] = out.get(p, 0) + shift * Mi
@@ -100,28 +119,27 @@ class OracleFMM:
     def l2l(self, Ll: Dict[int, np.ndarray], I_next: Dict[int, np.ndarray], l: int):
         """Level l -> l+1: multiply by e^{i kappa s.(c_parent - c_child)}, anterpolate, add I."""
         pa, ch = self.levels[l], self.levels[l + 1]
-        lpp, lc = self.plan.levels[l], self.plan.levels[l + 1]
         Sp = self.grid(l)
         out = {}
         for c, I in I_next.items():
             p = pa.index[parent(ch.boxes[c])]
             shift = np.exp(1j * self.kappa * (Sp @ (pa.centers[p] - ch.centers[c])))
-            prod = (shift * Ll[p]).reshape(1, lpp.n_theta, lpp.n_phi // 2)
-            out[c] = resample_half_batch(prod, lpp.n_phi, lc.n_theta, lc.n_phi).reshape(-1) + I
+            out[c] = self.resample(shift * Ll[p], l, l + 1) + I
         return out
 
     def l2t(self, Lf: Dict[int, np.ndarray], targets: np.ndarray) -> np.ndarray:
         lev = self.levels[self.S]
         lp = self.plan.levels[self.S]
         S = self.grid(self.S)
-        w = 8 * math.pi ** 2 / (lp.n_theta * lp.n_phi)
+        # doubled-grid weight 4 pi^2 / (N_theta N_phi(theta_n)) (P:287, P:813) x 2 for half storage
+        w = np.concatenate([np.full(r // 2, 8 * math.pi ** 2 / (lp.n_theta * r)) for r in lp.row_nphi()])
         y = np.zeros(len(targets), dtype=np.complex128)
         box_of = self._box_of_points(targets, self.S)
         for a in np.unique(box_of):
             sel = np.nonzero(box_of == a)[0]
             d = lev.centers[a] - self.x[targets[sel]]                            # c_a - x_i
             E = np.exp(1j * self.kappa * (d @ S.T))                              # [n, K]
-            y[sel] = w * (E @ Lf[a])
+            y[sel] = E @ (w * Lf[a])
         return y
 
     def p2p(self, q: np.ndarray, targets: np.ndarray) -> np.ndarray:

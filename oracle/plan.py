@@ -34,6 +34,13 @@ Readings of silent/ambiguous points are listed in DESIGN.md ("Readings"):
       2 sum_{n >= N/2} |J_n(kappa rho_l)| <= eps / 100.  R-5 (monotone grids) holds on the
       whole chain 2..D_s.  Policy for D_s (choose_source_level): the deepest level <= depth whose
       occupied boxes hold >= 8 points on average (L_f if none); D_s = L_f is the paper's setup.
+  R-15 ragged quadrature (Alg. 3's per-row result): with ragged=True
+      every active level stores N_phi(theta_n) points on row n, N_phi(theta_n) = the smallest
+      7-smooth multiple of 4 at which row n passes Alg. 3's test (eqn:EpsIPhi, threshold
+      eps_l / 4 pi^2) at the level's final N_theta (after R-5); rows n > N_theta/2 mirror
+      N_theta - n.  Never above the rectangular N_phi.  F_l, L_f and R-5 use the rectangular grid;
+      translation-only levels stay rectangular.  The 5-step resample maps between any
+      two quadratures; the stored half keeps N_phi(theta_n)/2 points per row.
 """
 from __future__ import annotations
 
@@ -188,10 +195,17 @@ class LevelPlan:
     active: bool = False
     alpha: float = 0.8
     rep: bool = False        # translation-only level below L_f (R-14): no ell, no M2L
+    rows: Optional[List[int]] = None   # R-15: N_phi(theta_n) for n < N_theta (None: rectangular)
 
     @property
     def K(self) -> int:
+        if self.rows is not None:
+            return sum(self.rows) // 2
         return self.n_theta * self.n_phi // 2
+
+    def row_nphi(self) -> List[int]:
+        """N_phi of every stored row n < N_theta (constant for a rectangular grid)."""
+        return list(self.rows) if self.rows is not None else [self.n_phi] * self.n_theta
 
 
 @dataclass
@@ -205,6 +219,8 @@ class Plan:
     levels: dict            # level -> LevelPlan
     L_f: Optional[int]      # None: no admissible level -> P2P over all pairs
     source_level: Optional[int] = None   # S2M / L2T level D_s (R-14); None iff L_f is None
+    ragged: bool = False                 # R-15: ragged rows on the active levels
+    eps_absolute: bool = False
 
 
 def level_params(kappa: float, a: float, eps: float, alpha: float, eps_absolute: bool = False):
@@ -246,6 +262,22 @@ def rep_grid(kappa: float, a: float, eps: float):
     return nth, nph
 
 
+def ragged_rows(lp: "LevelPlan", kappa: float, eps: float, eps_absolute: bool = False) -> List[int]:
+    """R-15: per-row N_phi(theta_n) of an active level at its final N_theta (Alg. 3)."""
+    a = lp.a
+    eps_l = eps if eps_absolute else eps / a
+    r, r0 = lp.alpha * a * math.sqrt(3.0), 2.0 * a
+    thr = eps_l / (4 * math.pi ** 2)
+    cands = [N for N in range(4, lp.n_phi + 1, 4) if is_7smooth(N)]
+    B = nphi_row_bounds(lp.ell, kappa, r, r0, lp.n_theta, cands)       # rows n <= N_theta / 2
+    half = []
+    for i in range(B.shape[0]):
+        ok = np.nonzero(B[i] < thr)[0]
+        half.append(cands[ok[0]] if len(ok) else lp.n_phi)
+    nth = lp.n_theta
+    return [half[n] if n <= nth // 2 else half[nth - n] for n in range(nth)]
+
+
 def choose_source_level(x: np.ndarray, lo, a0: float, depth: int, L_f: Optional[int],
                         min_mean: float = MIN_MEAN_POINTS) -> Optional[int]:
     """R-14 policy: deepest l in [L_f, depth] whose occupied boxes hold >= min_mean points on average."""
@@ -274,7 +306,7 @@ def alpha_candidates(alpha: float, fixed: bool):
 def make_plan(kappa: float, eps: float, a0: float, depth: int, alpha: float = 0.8,
               tau: Optional[float] = None, force_all: bool = False,
               eps_absolute: bool = False, alpha_fixed: bool = False,
-              source_level: Optional[int] = None) -> Plan:
+              source_level: Optional[int] = None, ragged: bool = False) -> Plan:
     """Plan for levels 2..depth (P:140-722 + admissibility R-9, design radius R-13, monotone R-5).
 
     Shallowest level first: for each candidate design radius alpha (R-13, largest first) take
@@ -283,6 +315,7 @@ def make_plan(kappa: float, eps: float, a0: float, depth: int, alpha: float = 0.
     levels are reported with the caller's alpha and no F."""
     if tau is None or tau <= 0:
         tau = default_tau(eps)
+    ragged_grids = bool(ragged)        # (the loop below rebinds `ragged` to Alg. 3's row lists)
     levels = {}
     L_f = None
     cands = alpha_candidates(alpha, alpha_fixed or force_all)
@@ -305,7 +338,7 @@ def make_plan(kappa: float, eps: float, a0: float, depth: int, alpha: float = 0.
             L_f = l
         else:
             stop = l
-    plan = Plan(kappa, eps, alpha, tau, a0, depth, levels, L_f, L_f)
+    plan = Plan(kappa, eps, alpha, tau, a0, depth, levels, L_f, L_f, ragged_grids, eps_absolute)
     if L_f is not None:
         set_source_level(plan, L_f if source_level is None else source_level)
     return plan
@@ -328,4 +361,6 @@ def set_source_level(plan: Plan, source_level: int) -> Plan:
             if not up.rep:
                 up.F = level_F(kappa, up.a, up.ell, nth, nph)
     plan.source_level = D_s
+    for l in range(2, L_f + 1):          # R-15 at the final N_theta of every active level
+        levels[l].rows = ragged_rows(levels[l], kappa, eps, plan.eps_absolute) if plan.ragged else None
     return plan

@@ -23,6 +23,7 @@ Every resample here is an explicit dense matrix built from the definition.
 from __future__ import annotations
 
 import math
+from functools import lru_cache
 from typing import List, Sequence
 
 import numpy as np
@@ -34,8 +35,9 @@ def band(N: int, Np: int) -> np.ndarray:
     return np.arange(-K, K + 1)
 
 
+@lru_cache(maxsize=256)
 def resample_matrix(N: int, Np: int) -> np.ndarray:
-    """Dense R[p, j] = sum_{k in band} (1/N) e^{-2 pi i j k / N} e^{2 pi i k p / N'}."""
+    """Dense R[p, j] = sum_{k in band} (1/N) e^{-2 pi i j k / N} e^{2 pi i k p / N'} (cached; read-only)."""
     k = band(N, Np)
     fwd = np.exp(-2j * math.pi * np.outer(k, np.arange(N)) / N) / N          # [k, j]
     inv = np.exp(2j * math.pi * np.outer(np.arange(Np), k) / Np)             # [p, k]
@@ -113,6 +115,36 @@ def resample_rows(rows: Sequence[np.ndarray], nth: int, nth_p: int,
     if trace is not None:
         trace.append(("A_phi", [len(r) for r in out]))
     return out
+
+
+def ragged_to_rows(F: np.ndarray, rows_n) -> List[np.ndarray]:
+    """Ragged stored half (rows n < N_theta of N_phi(theta_n)/2 values, concatenated) -> full
+    phi-rows for n = 0..N_theta/2 (eqn:NumSphereSym; N_phi(theta_{N_theta-n}) = N_phi(theta_n))."""
+    nth = len(rows_n)
+    off = np.concatenate([[0], np.cumsum(np.asarray(rows_n) // 2)])
+    half = [F[off[n]: off[n + 1]] for n in range(nth)]
+    return [np.concatenate([half[n], half[(nth - n) % nth]]) for n in range(nth // 2 + 1)]
+
+
+def rows_to_ragged(rows: Sequence[np.ndarray], nth: int) -> np.ndarray:
+    """Inverse of ragged_to_rows: full rows n <= N_theta/2 -> ragged stored half."""
+    out = []
+    for n in range(nth):
+        if n <= nth // 2:
+            r = rows[n]
+            out.append(r[: len(r) // 2])
+        else:
+            r = rows[nth - n]
+            out.append(r[len(r) // 2:])
+    return np.concatenate(out)
+
+
+def resample_ragged(F: np.ndarray, rows_n, nth_p: int, rows_p) -> np.ndarray:
+    """5-step resample between two (possibly ragged) stored halves."""
+    nth = len(rows_n)
+    rows = ragged_to_rows(F, rows_n)
+    out = resample_rows(rows, nth, nth_p, [int(rows_p[n]) for n in range(nth_p // 2 + 1)])
+    return rows_to_ragged(out, nth_p)
 
 
 def resample_half(F: np.ndarray, nph: int, nth_p: int, nph_p: int) -> np.ndarray:

@@ -104,6 +104,27 @@ def bmtf_table(ell: int, kappa: float, r0vec, n_theta: int, n_phi: int) -> np.nd
     return eval_coeffs(C[:, keep], n, m_all[keep], theta, phi)
 
 
+def bmtf_table_rows(ell: int, kappa: float, r0vec, n_theta: int, rows) -> np.ndarray:
+    """T^{s,LL} on a ragged stored half (R-15): row n keeps |m| <= N_phi(theta_n)/2 - 1
+    and is sampled at phi = 2 pi q / N_phi(theta_n), q < N_phi(theta_n)/2; rows concatenated.
+    (Rows of equal N_phi are evaluated together; the values are per row.)"""
+    C = bmtf_coeffs(ell, kappa, r0vec, n_theta)
+    nmax = n_theta // 2 - 1
+    nf = np.arange(-nmax, nmax + 1)
+    m_all = np.arange(-ell, ell + 1)
+    rows = [int(r) for r in rows]
+    out = [None] * n_theta
+    for nph in sorted(set(rows)):
+        ns = [n for n in range(n_theta) if rows[n] == nph]
+        keep = np.abs(m_all) <= min(ell, nph // 2 - 1)
+        theta = 2 * math.pi * np.asarray(ns) / n_theta
+        phi = 2 * math.pi * np.arange(nph // 2) / nph
+        vals = eval_coeffs(C[:, keep], nf, m_all[keep], theta, phi)          # [len(ns), nph/2]
+        for i, n in enumerate(ns):
+            out[n] = vals[i]
+    return np.concatenate(out)
+
+
 def bmtf_realspace_column(ell: int, kappa: float, r0vec, n_theta: int, phi: float) -> np.ndarray:
     """Real-space route of P:532 / Fig. SarvasDiag for one phi column.
 
