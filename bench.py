@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ops", default="8,16,32,64",
                     help="C2 operator microbench bandwidths B (comma list; '' to skip)")
+    ap.add_argument("--ragged", type=int, default=0,
+                    help="1: ragged quadrature on the active levels (HFMM_RAGGED, DESIGN.md R-15)")
     ap.add_argument("--extra", default="C3,C5",
                     help="other BASELINE matvec configs timed after the main one (comma list; '' to skip)")
     ap.add_argument("--json-out", default=None)
@@ -369,7 +371,8 @@ def main():
     g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
     t_tree = time.perf_counter() - t0
     t0 = time.perf_counter()
-    g.precompute(cfg.kappa, cfg.eps, cfg.alpha)
+    pflags = hf.HFMM_RAGGED if args.ragged else 0
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha, flags=pflags)
     t_pre = time.perf_counter() - t0
     info = g.info()
     stream = torch.cuda.current_stream()

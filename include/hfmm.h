@@ -64,6 +64,8 @@ extern "C" {
                                       {1, 0.9, 0.8} (>= the caller's) that keeps F_l <= tau   */
 #define HFMM_SOURCE_AT_LF 0x8u     /* S2M / L2T at L_f (the paper's setup, no translation-only
                                       levels); default: source level D_s by the policy below */
+#define HFMM_RAGGED 0x20u          /* ragged quadrature on the active levels (R-15, Alg. 3 per row;
+                                      SURVEY 8f NEXT 2); default: rectangular N_phi (R-4)    */
 #define HFMM_SOURCE_AT_DEPTH 0x10u /* S2M / L2T at the configured depth D.  Default policy
                                       (R-14): the deepest level <= D whose occupied
                                       boxes hold >= 8 points on average; levels L_f < l <= D_s
@@ -93,6 +95,7 @@ typedef struct {
   int64_t boxes;    /* occupied boxes at this level                                        */
   int64_t m2l_pairs;/* interaction-list entries at this level (all ranks)                  */
   int rep;          /* 1: translation-only level L_f < l <= D_s (R-14; ell = 0, F = NaN)   */
+  int ragged;       /* 1: ragged rows N_phi(theta_n) (R-15, HFMM_RAGGED); K = stored points   */
 } hfmm_level_info;
 
 typedef struct {
@@ -170,6 +173,14 @@ const char *hfmm_last_error(const hfmm_plan *p);
 
 /* Free everything owned by the plan, including the NCCL communicator. */
 void hfmm_destroy(hfmm_plan *p);
+
+/* Host-only (no GPU needed): ragged rows of an active level (R-15; Alg. 3 per row,
+ * P:669-684): rows[n], n < n_theta, = the smallest 7-smooth multiple of 4 at which row n passes
+ * Alg. 3's test for (kappa, box size a, absolute level target eps_level, design radius alpha,
+ * ell) at this n_theta, capped at n_phi_cap; rows n > n_theta/2 mirror n_theta - n.  Returns 0,
+ * HFMM_E_ARG or HFMM_E_SEARCH. */
+int hfmm_ragged_rows(double kappa, double a, double eps_level, double alpha, int ell, int n_theta,
+                     int n_phi_cap, int *rows);
 
 /* Host-only (no GPU needed): grid (N_theta, N_phi) of a translation-only level of box size a
  * (R-14; eqn:PlaneWaveSpec): smallest even 7-smooth N_theta >= 4 and

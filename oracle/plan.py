@@ -38,7 +38,8 @@ Readings of silent/ambiguous points are listed in DESIGN.md ("Readings"):
       every active level stores N_phi(theta_n) points on row n, N_phi(theta_n) = the smallest
       7-smooth multiple of 4 at which row n passes Alg. 3's test (eqn:EpsIPhi, threshold
       eps_l / 4 pi^2) at the level's final N_theta (after R-5); rows n > N_theta/2 mirror
-      N_theta - n.  Never above the rectangular N_phi.  F_l, L_f and R-5 use the rectangular grid;
+      N_theta - n, rows n and N_theta/2 - n take the larger of the two (exact theta -> pi - theta
+      symmetry for the 34-table permutations).  Never above the rectangular N_phi.  F_l, L_f and R-5 use the rectangular grid;
       translation-only levels stay rectangular.  The 5-step resample maps between any
       two quadratures; the stored half keeps N_phi(theta_n)/2 points per row.
 """
@@ -275,6 +276,9 @@ def ragged_rows(lp: "LevelPlan", kappa: float, eps: float, eps_absolute: bool = 
         ok = np.nonzero(B[i] < thr)[0]
         half.append(cands[ok[0]] if len(ok) else lp.n_phi)
     nth = lp.n_theta
+    # exact reflection symmetry theta -> pi - theta (rows n and N_theta/2 - n), required by the
+    # 34-table permutations; the two bounds agree up to rounding, take the larger row
+    half = [max(half[n], half[nth // 2 - n]) for n in range(nth // 2 + 1)]
     return [half[n] if n <= nth // 2 else half[nth - n] for n in range(nth)]
 
 

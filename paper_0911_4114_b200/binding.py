@@ -24,6 +24,7 @@ HFMM_FORCE_ALL_LEVELS = 0x2
 HFMM_ALPHA_FIXED = 0x4
 HFMM_SOURCE_AT_LF = 0x8
 HFMM_SOURCE_AT_DEPTH = 0x10
+HFMM_RAGGED = 0x20
 HFMM_HOST = 0
 HFMM_DEVICE = 1
 HFMM_Y_LOCAL = 2
@@ -34,7 +35,7 @@ EXPORTED = [
     "hfmm_direct", "hfmm_get_info", "hfmm_stage_times", "hfmm_debug_copy", "hfmm_last_error",
     "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
     "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
-    "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free",
+    "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free", "hfmm_ragged_rows",
 ]
 
 
@@ -42,7 +43,7 @@ class LevelInfo(C.Structure):
     _fields_ = [("level", C.c_int), ("a", C.c_double), ("ell", C.c_int), ("n_theta", C.c_int),
                 ("n_phi", C.c_int), ("alpha", C.c_double), ("K", C.c_int64), ("F", C.c_double),
                 ("active", C.c_int),
-                ("boxes", C.c_int64), ("m2l_pairs", C.c_int64), ("rep", C.c_int)]
+                ("boxes", C.c_int64), ("m2l_pairs", C.c_int64), ("rep", C.c_int), ("ragged", C.c_int)]
 
 
 class Info(C.Structure):
@@ -97,6 +98,7 @@ def load() -> C.CDLL:
         "hfmm_m2l_op_plan": (ci, [ci, i64, vp, vp, vp, C.POINTER(vp)]),
         "hfmm_m2l_op_apply": (ci, [vp, vp, vp, vp, vp]),
         "hfmm_m2l_op_free": (None, [vp]),
+        "hfmm_ragged_rows": (ci, [dbl, dbl, dbl, dbl, ci, ci, ci, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -135,6 +137,15 @@ def rep_grid(kappa: float, a: float, eps: float):
     if rc < 0:
         raise HFMMError(rc, "hfmm_rep_grid")
     return nth.value, nph.value
+
+
+def ragged_rows(kappa: float, a: float, eps_level: float, alpha: float, ell: int, n_theta: int, n_phi_cap: int):
+    """Host-only: per-row N_phi(theta_n) of an active level (include/hfmm.h hfmm_ragged_rows)."""
+    out = np.zeros(n_theta, dtype=np.int32)
+    rc = load().hfmm_ragged_rows(kappa, a, eps_level, alpha, ell, n_theta, n_phi_cap, out.ctypes.data)
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_ragged_rows")
+    return [int(v) for v in out]
 
 
 def partition(xyz, depth, lo, size, L_f, K, nranks):
@@ -240,7 +251,7 @@ class HFMM:
             levels.append(dict(level=lv.level, a=lv.a, ell=lv.ell, n_theta=lv.n_theta, n_phi=lv.n_phi,
                                alpha=lv.alpha, K=lv.K,
                                F=lv.F, active=bool(lv.active), boxes=lv.boxes, m2l_pairs=lv.m2l_pairs,
-                               rep=bool(lv.rep)))
+                               rep=bool(lv.rep), ragged=bool(lv.ragged)))
         return dict(n=inf.n, depth=inf.depth, L_f=(None if inf.L_f < 0 else inf.L_f), kappa=inf.kappa,
                     eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
                     p2p_sym_pairs=inf.p2p_sym_pairs,

@@ -40,6 +40,13 @@ struct LevelDev {
   double F = NAN;
   bool active = false;
   bool rep = false;              // translation-only level L_f < l <= D_s (R-14)
+  bool ragged = false;           // R-15: rows of N_phi(theta_n) points (active levels, HFMM_RAGGED)
+  std::vector<int32_t> rows_h;   // N_phi(theta_n), n < nth (ragged)
+  std::vector<int64_t> off_h;    // row offsets into the stored half, n <= nth (ragged)
+  int32_t *rows_d = nullptr;
+  int64_t *off_d = nullptr;
+  int64_t K_rect = 0;            // nth * nph / 2 of the rectangular grid (nph = max row)
+  double *wk = nullptr;          // per-point L2T weights 8 pi^2 / (nth N_phi(theta_n)) (ragged source level)
   int64_t nbox = 0;
   int64_t own0 = 0, own1 = 0;  // owned box range (Morton order)
   std::vector<int64_t> rlo, rhi; // every rank's owned range (for the all-gather)
@@ -128,6 +135,7 @@ struct hfmm_plan {
   double dummy_t[3] = {0, 0, 0}, dummy_s[3] = {0, 0, 0};
   double2 *tmp = nullptr;
   size_t tmp_elems = 0;
+  double2 *scr1 = nullptr, *scr2 = nullptr;  // rectangular copies around ragged levels (R-15)
   hfmm_info info{};
   double stage_ms[8] = {0};
   bool profile = false;
@@ -159,17 +167,18 @@ static void free_levels(hfmm_plan *p) {
     m2l_group_plan_destroy(L.m2lg);
     L.m2lg = nullptr;
     for (void *ptr : {(void *)L.cx, (void *)L.cy, (void *)L.cz, (void *)L.ks, (void *)L.T, (void *)L.M,
-                      (void *)L.I, (void *)L.L, (void *)L.perm,
+                      (void *)L.I, (void *)L.L, (void *)L.perm, (void *)L.rows_d, (void *)L.off_d, (void *)L.wk,
                       (void *)L.parent, (void *)L.oct, (void *)L.cbeg, (void *)L.shift})
       if (ptr) cudaFree(ptr);
   }
   p->lv.clear();
-  for (void *ptr : {(void *)p->first_near, (void *)p->first_src, (void *)p->tile_leaf, (void *)p->tile_begin, (void *)p->tmp,
+  for (void *ptr : {(void *)p->scr1, (void *)p->scr2, (void *)p->first_near, (void *)p->first_src, (void *)p->tile_leaf, (void *)p->tile_begin, (void *)p->tmp,
                     (void *)p->y_far, (void *)p->p2p_items[0], (void *)p->p2p_items[1], (void *)p->p2p_items[2],
                     (void *)p->dir_items, (void *)p->ux, (void *)p->uy, (void *)p->uz})
     if (ptr) cudaFree(ptr);
   p->first_near = nullptr, p->first_src = nullptr, p->tile_leaf = nullptr;
   p->tile_begin = nullptr, p->tmp = nullptr, p->y_far = nullptr;
+  p->scr1 = p->scr2 = nullptr;
   for (int k = 0; k < 3; ++k) p->p2p_items[k] = nullptr, p->p2p_nitems[k] = 0;
   p->dir_items = nullptr, p->dir_nitems = 0;
   p->ux = p->uy = p->uz = nullptr;
@@ -360,21 +369,44 @@ static int level_tables(hfmm_plan *p, LevelDev &L, double2 **T_out, double *F_ou
   return HFMM_OK;
 }
 
-static void grid_dirs(int nth, int nph, double kappa, std::vector<double> &ks) {
-  const int64_t h = nph / 2, K = (int64_t)nth * h;
+// kappa s at the stored points, row by row (rows[n] points on row n of a ragged level, R-15;
+// nph on every row otherwise): k = off[n] + m, phi = 2 pi m / N_phi(theta_n), m < N_phi(theta_n)/2
+static void grid_dirs(const LevelDev &L, double kappa, std::vector<double> &ks) {
+  const int64_t K = L.K;
   ks.assign(3 * K, 0.0);
-  for (int n = 0; n < nth; ++n) {
-    long double th = 2.0L * 3.141592653589793238462643383279502884L * n / nth;
+  int64_t k = 0;
+  for (int n = 0; n < L.nth; ++n) {
+    long double th = 2.0L * 3.141592653589793238462643383279502884L * n / L.nth;
     double st = (double)sinl(th), ct = (double)cosl(th);
-    for (int m = 0; m < h; ++m) {
+    const int nph = L.ragged ? L.rows_h[n] : L.nph;
+    for (int m = 0; m < nph / 2; ++m, ++k) {
       long double ph = 2.0L * 3.141592653589793238462643383279502884L * m / nph;
       double cp = (double)cosl(ph), sp = (double)sinl(ph);
-      int64_t k = (int64_t)n * h + m;
       ks[k] = kappa * (cp * st);
       ks[K + k] = kappa * (sp * st);
       ks[2 * K + k] = kappa * ct;
     }
   }
+}
+
+// perm[op][k] of the 34-table reflections on a ragged grid (row-local phi maps; row lengths are
+// symmetric under theta -> pi - theta and theta -> 2 pi - theta, R-15)
+static void symmetry_perms_ragged(const LevelDev &L, std::vector<int32_t> &perm) {
+  const int nth = L.nth;
+  perm.assign((size_t)16 * L.K, 0);
+  for (int op = 0; op < 16; ++op)
+    for (int n = 0; n < nth; ++n) {
+      const int N = L.rows_h[n];
+      for (int m = 0; m < N / 2; ++m) {
+        int nn = n, mm = m;
+        if (op & 1) mm = (N / 2 - mm + N) % N;
+        if (op & 2) mm = (N - mm) % N;
+        if (op & 4) nn = (nth / 2 - nn + nth) % nth;
+        if (op & 8) mm = ((N / 4 - mm) % N + N) % N;
+        if (mm >= N / 2) nn = (nth - nn) % nth, mm -= N / 2;
+        perm[(size_t)op * L.K + L.off_h[n] + m] = (int32_t)(L.off_h[nn] + mm);
+      }
+    }
 }
 
 static void partition(hfmm_plan *p) {
@@ -530,8 +562,39 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     }
   }
   partition(p);
+  // ragged rows on the active levels (R-15), their tables from the rectangular ones
+  if ((flags & HFMM_RAGGED) && p->L_f >= 2) {
+    const TwiddleSet &tw = global_twiddles(p->device);
+    for (int l = 2; l <= p->L_f; ++l) {
+      LevelDev &L = p->lv[l];
+      const double eps_l = (flags & HFMM_EPS_ABSOLUTE) ? eps : eps / L.a;
+      std::vector<int> rows;
+      if (select_nphi_rows(L.ell, kappa, L.alpha * std::sqrt(3.0) * L.a, 2.0 * L.a, eps_l, L.nth, L.nph, rows)) {
+        p->err = "hfmm_precompute: ragged row search failed at level " + std::to_string(l);
+        return HFMM_E_SEARCH;
+      }
+      L.ragged = true;
+      L.rows_h.assign(rows.begin(), rows.end());
+      L.off_h.assign(L.nth + 1, 0);
+      for (int n = 0; n < L.nth; ++n) L.off_h[n + 1] = L.off_h[n] + rows[n] / 2;
+      L.K_rect = (int64_t)L.nth * L.nph / 2;
+      L.K = L.off_h[L.nth];
+      L.rows_d = dupload(L.rows_h), L.off_d = dupload(L.off_h);
+      std::vector<int> cids, sym_of;
+      canonical_offsets(cids, sym_of);
+      double2 *Tr = dalloc<double2>((size_t)cids.size() * L.K);
+      if (!Tr || !L.rows_d || !L.off_d) {
+        p->err = "hfmm_precompute: allocation failed (ragged tables)";
+        return HFMM_E_NOMEM;
+      }
+      launch_ragged_tables(L.T, (int)cids.size(), L.nth, L.nph, L.rows_d, L.off_d, L.K, Tr, tw, p->stream);
+      CK(cudaStreamSynchronize(p->stream));
+      cudaFree(L.T);
+      L.T = Tr;
+    }
+  }
   // device data of the levels 2..D_s (M2L data only on the active levels 2..L_f)
-  size_t tmp_need = 0;
+  size_t tmp_need = 0, scr1_need = 0, scr2_need = 0;
   for (int l = 2; l <= p->D_s; ++l) {
     LevelDev &L = p->lv[l];
     const LevelBoxes &B = t.levels[l];
@@ -543,7 +606,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     }
     L.cx = dupload(cx), L.cy = dupload(cy), L.cz = dupload(cz);
     std::vector<double> ks;
-    grid_dirs(L.nth, L.nph, kappa, ks);
+    grid_dirs(L, kappa, ks);
     {
       std::vector<double> ksu(ks);  // kernels take kappa s in table steps (h = 2 pi / TAB_STEPS)
       for (auto &v : ksu) v *= (double)TAB_STEPS / (2.0 * kPi);
@@ -577,7 +640,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     L.il_nnz = (int64_t)src.size();
     if (L.active) {
       std::vector<int32_t> pm;
-      symmetry_perms(L.nth, L.nph, pm);
+      if (L.ragged) symmetry_perms_ragged(L, pm);
+      else symmetry_perms(L.nth, L.nph, pm);
       L.perm = dupload(pm);
       // sibling groups over the owned boxes: consecutive boxes (Morton order) with one parent
       std::vector<int64_t> gb;
@@ -609,6 +673,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       const LevelDev &C = p->lv[l + 1];
       tmp_need = std::max(tmp_need, (size_t)C.nbox * (C.nth / 2 + 1) * L.nph);  // M2M rows pass
       tmp_need = std::max(tmp_need, (size_t)C.nbox * C.nth * (L.nph / 2));      // L2L cols pass
+      if (C.ragged || L.ragged) {  // rectangular copies: children on the child / parent grids
+        scr1_need = std::max(scr1_need, (size_t)C.nbox * C.nth * (C.nph / 2));
+        scr2_need = std::max(scr2_need, (size_t)C.nbox * L.nth * (L.nph / 2));
+      }
     }
   }
   if (tmp_need) {
@@ -618,6 +686,19 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       p->err = "hfmm_precompute: allocation failed (resample scratch)";
       return HFMM_E_NOMEM;
     }
+  }
+  if (scr1_need) p->scr1 = dalloc<double2>(scr1_need);
+  if (scr2_need) p->scr2 = dalloc<double2>(scr2_need);
+  if ((scr1_need && !p->scr1) || (scr2_need && !p->scr2)) {
+    p->err = "hfmm_precompute: allocation failed (ragged scratch)";
+    return HFMM_E_NOMEM;
+  }
+  if (p->D_s >= 2 && p->lv[p->D_s].ragged) {  // per-point L2T weights on a ragged source level
+    const LevelDev &S = p->lv[p->D_s];
+    std::vector<double> w(S.K);
+    for (int n = 0; n < S.nth; ++n)
+      for (int64_t k = S.off_h[n]; k < S.off_h[n + 1]; ++k) w[k] = 8.0 * kPi * kPi / ((double)S.nth * S.rows_h[n]);
+    p->lv[p->D_s].wk = dupload(w);
   }
   // near field at L_f (neighbour lists) or all pairs at the root, as P2P work items
   p->near_level = p->L_f >= 2 ? p->L_f : 0;
@@ -741,6 +822,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     li.level = l, li.a = L.a, li.ell = L.ell, li.n_theta = L.nth, li.n_phi = L.nph, li.alpha = L.alpha, li.K = L.K,
     li.F = L.F, li.active = L.active ? 1 : 0, li.boxes = L.nbox, li.m2l_pairs = L.il_nnz;
     li.rep = L.rep ? 1 : 0;
+    li.ragged = L.ragged ? 1 : 0;
   }
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
   in.source_level = p->D_s;
@@ -817,10 +899,23 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user) {
     for (int l = Ds; l > 2; --l) {  // M2M, through the translation-only levels too
       LevelDev &C = p->lv[l], &P = p->lv[l - 1];
       if (C.own1 > C.own0) {
-        launch_rows_up(C.M + C.own0 * C.K, C.own1 - C.own0, C.nth, C.nph, P.nph, p->tmp, tw, s);
-        // parents own0..own1 have children C.own0.. (contiguous); child index relative to C.own0
-        launch_cols_up(p->tmp, C.nth, P.nph, P.nth, P.cbeg + P.own0, C.own0, C.oct, P.own1 - P.own0, P.shift,
-                       P.M + P.own0 * P.K, tw, s);
+        const int64_t nc = C.own1 - C.own0;
+        const double2 *src = C.M + C.own0 * C.K;
+        if (C.ragged) {  // 5-step step 1 on the ragged child rows -> rectangular child grid
+          launch_rag2rect(src, C.K, C.nth, C.rows_d, C.off_d, C.nph, nullptr, nullptr, nullptr, nc, C.nph, p->scr1,
+                          tw, s);
+          src = p->scr1;
+        }
+        launch_rows_up(src, nc, C.nth, C.nph, P.nph, p->tmp, tw, s);
+        if (P.ragged) {  // per-child parent fields, then step 5 + shift + sum on the ragged parent grid
+          launch_cols_up(p->tmp, C.nth, P.nph, P.nth, nullptr, 0, nullptr, nc, nullptr, p->scr2, tw, s);
+          launch_rect2rag(p->scr2, P.nth, P.nph, P.cbeg + P.own0, C.own0, C.oct, P.shift, nullptr, P.rows_d,
+                          P.off_d, P.K, P.own1 - P.own0, P.M + P.own0 * P.K, tw, s);
+        } else {
+          // parents own0..own1 have children C.own0.. (contiguous); child index relative to C.own0
+          launch_cols_up(p->tmp, C.nth, P.nph, P.nth, P.cbeg + P.own0, C.own0, C.oct, P.own1 - P.own0, P.shift,
+                         P.M + P.own0 * P.K, tw, s);
+        }
       }
     }
     for (int l = 2; l <= Lf; ++l) {
@@ -837,10 +932,22 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user) {
       LevelDev &P = p->lv[l], &C = p->lv[l + 1];
       const double2 *Lp = (l == 2) ? P.I : P.L;
       if (C.own1 > C.own0) {
-        launch_cols_down(Lp, P.nth, P.nph, C.nth, C.parent + C.own0, C.oct + C.own0, C.own1 - C.own0,
-                         P.shift, p->tmp, tw, s);
-        launch_rows_down(p->tmp, C.own1 - C.own0, C.nth, P.nph, C.nph, C.I ? C.I + C.own0 * C.K : nullptr,
-                         C.L + C.own0 * C.K, tw, s);
+        const int64_t nc = C.own1 - C.own0;
+        if (P.ragged) {  // conj shift on the ragged parent grid + step 1 -> rectangular, per child
+          launch_rag2rect(Lp, P.K, P.nth, P.rows_d, P.off_d, P.nph, C.parent + C.own0, C.oct + C.own0, P.shift, nc,
+                          P.nph, p->scr2, tw, s);
+          launch_cols_down(p->scr2, P.nth, P.nph, C.nth, nullptr, nullptr, nc, nullptr, p->tmp, tw, s);
+        } else {
+          launch_cols_down(Lp, P.nth, P.nph, C.nth, C.parent + C.own0, C.oct + C.own0, nc, P.shift, p->tmp, tw, s);
+        }
+        if (C.ragged) {  // rectangular child grid, then step 5 to the ragged rows + I_child
+          launch_rows_down(p->tmp, nc, C.nth, P.nph, C.nph, nullptr, p->scr1, tw, s);
+          launch_rect2rag(p->scr1, C.nth, C.nph, nullptr, 0, nullptr, nullptr, C.I ? C.I + C.own0 * C.K : nullptr,
+                          C.rows_d, C.off_d, C.K, nc, C.L + C.own0 * C.K, tw, s);
+        } else {
+          launch_rows_down(p->tmp, nc, C.nth, P.nph, C.nph, C.I ? C.I + C.own0 * C.K : nullptr, C.L + C.own0 * C.K,
+                           tw, s);
+        }
       }
     }
     if (prof) cudaEventRecord(p->sev[4], s);
@@ -848,10 +955,10 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user) {
     const double wq = 8.0 * kPi * kPi / ((double)F.nth * (double)F.nph);
     if (p->small_src)
       launch_l2t_small(pts, p->first_src, F.cx, F.cy, F.cz, (int32_t)F.own0, (int32_t)F.own1, F.ks, F.K, Lf_loc, wq,
-                       p->y_far, s);
+                       F.wk, p->y_far, s);
     else
       launch_l2t(pts, p->first_src, F.cx, F.cy, F.cz, p->tile_leaf, p->tile_begin, p->ntiles, F.ks, F.K, Lf_loc, wq,
-                 p->y_far, s);
+                 F.wk, p->y_far, s);
     if (prof) cudaEventRecord(p->sev[5], s);
   } else if (prof) {
     for (int k = 1; k <= 5; ++k) cudaEventRecord(p->sev[k], s);

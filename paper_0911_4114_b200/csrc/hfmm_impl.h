@@ -29,7 +29,9 @@ double collino_bound(int ell, double kappa, double r, double r0);
 int select_ell(double kappa, double r, double r0, double eps, int *ell);
 int select_ntheta(int ell, double kappa, double r, double r0, double eps, int *nth);
 int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth, int *nph,
-                std::vector<int> *ragged);
+                std::vector<int> *ragged, std::vector<int> *first7 = nullptr);
+int select_nphi_rows(int ell, double kappa, double r, double r0, double eps, int nth, int cap,
+                     std::vector<int> &rows);  // R-15
 bool seven_smooth(int n);
 int select_rep_grid(double kappa, double a, double eps, int *nth, int *nph);  // R-14
 
@@ -125,18 +127,34 @@ void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const dou
                 const double *cz, int32_t box0, int32_t box1, const double *ks /*[3][K]*/,
                 int64_t K, double2 *M, cudaStream_t s);
 
-// L2T: y_far[i] = w sum_k L[b][k] e^{i kappa s_k.(c_b - x_i)}; ks as for S2M
+// L2T: y_far[i] = sum_k w_k L[b][k] e^{i kappa s_k.(c_b - x_i)}; ks as for S2M;
+// w_k = wk[k] (ragged rows, R-15) or the constant w
 void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
                 const double *cz, const int32_t *tile_leaf, const int64_t *tile_begin,
                 int64_t ntiles, const double *ks, int64_t K, const double2 *L, double w,
-                double2 *y_far, cudaStream_t s);
+                const double *wk, double2 *y_far, cudaStream_t s);
+
+// Ragged quadrature (R-15, kernels_ragged.cu): tables from the rectangular ones; 5-step steps 1
+// (ragged rows -> rectangular calN_phi half) and 5 (rectangular -> ragged rows), one CTA per row.
+void launch_ragged_tables(const double2 *Trect, int ncanon, int nth, int nphr, const int32_t *rows, const int64_t *off,
+                          int64_t K, double2 *out, const TwiddleSet &tw, cudaStream_t s);
+// item o < nitem: input box par ? par[o] : o of `in` (stride in_K), times conj(shift[oct[o]]) if
+// shift; output rectangular half [nth][nphr/2] of box o.
+void launch_rag2rect(const double2 *in, int64_t in_K, int nth, const int32_t *rows, const int64_t *off, int maxrow,
+                     const int32_t *par, const int8_t *oct, const double2 *shift, int64_t nitem, int nphr,
+                     double2 *out, const TwiddleSet &tw, cudaStream_t s);
+// item o: sum over children c in [cbeg[o], cbeg[o+1]) (input box c - cbase; c = o without cbeg)
+// of shift[oct[c]] (if shift) * (row resample of child c to the ragged rows), + add[o]; into out[o].
+void launch_rect2rag(const double2 *in, int nth, int nphr, const int32_t *cbeg, int64_t cbase, const int8_t *oct,
+                     const double2 *shift, const double2 *add, const int32_t *rows, const int64_t *off, int64_t K,
+                     int64_t nitem, double2 *out, const TwiddleSet &tw, cudaStream_t s);
 
 // Small-box variants (source level below L_f, R-14): one warp per box, persistent grid.
 void launch_s2m_small(PointsDev pts, const int64_t *first, const double *cx, const double *cy, const double *cz,
                       int32_t box0, int32_t box1, const double *ks, int64_t K, double2 *M, cudaStream_t s);
 void launch_l2t_small(PointsDev pts, const int64_t *first, const double *cx, const double *cy, const double *cz,
                       int32_t box0, int32_t box1, const double *ks, int64_t K, const double2 *L, double w,
-                      double2 *y_far, cudaStream_t s);
+                      const double *wk, double2 *y_far, cudaStream_t s);
 
 // Sibling-group M2L (kernels_m2l.cu): plan once per level / operator, apply per matvec.
 struct M2LGroupPlan;

@@ -186,7 +186,7 @@ int select_ntheta(int ell, double kappa, double r, double r0, double eps, int *n
 }
 
 int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth, int *nph,
-                std::vector<int> *ragged) {
+                std::vector<int> *ragged, std::vector<int> *first7) {
   const double thr = eps / (4.0 * kPi * kPi);
   std::vector<cplx> c;
   transfer_series(ell, kappa, r0, c);
@@ -207,6 +207,7 @@ int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth,
   for (int N = 4; N <= nmaxphi; N += 4) cands.push_back(N);
   std::vector<char> all_ok(cands.size(), 1);
   if (ragged) ragged->assign(rows, 0);
+  if (first7) first7->assign(rows, -1);
   for (int n = 0; n < rows; ++n) {
     std::vector<double> tt(P);
     for (int f = -ell; f <= ell; ++f) {  // |F_m[T]| (Alg. 3 line 4)
@@ -229,6 +230,7 @@ int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth,
       for (int f = -ell; f <= ell; ++f) bound += tt[f + ell] * std::fabs(J[Mfun(N, f)]);
       bool ok = bound < thr;
       if (ok && !first) first = N;
+      if (ok && first7 && (*first7)[n] < 0 && seven_smooth(N)) (*first7)[n] = N;
       if (!ok) all_ok[ci] = 0;
     }
     if (!first) return HFMM_E_SEARCH;
@@ -240,6 +242,24 @@ int select_nphi(int ell, double kappa, double r, double r0, double eps, int nth,
       return 0;
     }
   return HFMM_E_SEARCH;
+}
+
+// Ragged quadrature (R-15): N_phi(theta_n) = the smallest 7-smooth multiple of 4 at
+// which row n passes Alg. 3's test at the level's final N_theta, capped at the rectangular N_phi;
+// rows n > N_theta/2 mirror N_theta - n.
+int select_nphi_rows(int ell, double kappa, double r, double r0, double eps, int nth, int cap,
+                     std::vector<int> &rows) {
+  int nph = 0;
+  std::vector<int> f7;
+  int rc = select_nphi(ell, kappa, r, r0, eps, nth, &nph, nullptr, &f7);
+  if (rc) return rc;
+  std::vector<int> half(nth / 2 + 1);
+  for (int n = 0; n <= nth / 2; ++n) half[n] = (f7[n] > 0 && f7[n] <= cap) ? f7[n] : cap;
+  std::vector<int> sym(half);  // exact theta -> pi - theta symmetry (rows n and N_theta/2 - n)
+  for (int n = 0; n <= nth / 2; ++n) sym[n] = std::max(half[n], half[nth / 2 - n]);
+  rows.assign(nth, cap);
+  for (int n = 0; n < nth; ++n) rows[n] = sym[n <= nth / 2 ? n : nth - n];
+  return 0;
 }
 
 // Translation-only level (R-14): the outgoing field of a box is a sum of plane waves
@@ -270,6 +290,18 @@ int select_rep_grid(double kappa, double a, double eps, int *nth, int *nph) {
 }
 
 }  // namespace hfmm
+
+extern "C" int hfmm_ragged_rows(double kappa, double a, double eps_level, double alpha, int ell, int n_theta,
+                                int n_phi_cap, int *rows) {
+  if (!(kappa > 0) || !(a > 0) || !(eps_level > 0) || !(alpha > 0) || ell < 1 || n_theta < 2 || n_phi_cap < 4 ||
+      !rows)
+    return HFMM_E_ARG;
+  std::vector<int> r;
+  int rc = hfmm::select_nphi_rows(ell, kappa, alpha * std::sqrt(3.0) * a, 2.0 * a, eps_level, n_theta, n_phi_cap, r);
+  if (rc) return rc;
+  for (int n = 0; n < n_theta; ++n) rows[n] = r[n];
+  return 0;
+}
 
 extern "C" int hfmm_rep_grid(double kappa, double a, double eps, int *n_theta, int *n_phi) {
   if (!(kappa > 0) || !(a > 0) || !(eps > 0) || !n_theta || !n_phi) return HFMM_E_ARG;

@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(L2T_TPB, 5) l2t_kernel(PointsDev pts, const in
                                                          const int64_t *__restrict__ tile_begin,
                                                          const double *__restrict__ ks, int64_t K,
                                                          const double2 *__restrict__ L, double w,
+                                                         const double *__restrict__ wk,
                                                          double2 *__restrict__ y_far) {
   __shared__ double2 tab[TAB];
   __shared__ double skx[L2T_TPB], sky[L2T_TPB], skz[L2T_TPB];
@@ -321,7 +322,9 @@ __global__ void __launch_bounds__(L2T_TPB, 5) l2t_kernel(PointsDev pts, const in
       skx[threadIdx.x] = ks[k];
       sky[threadIdx.x] = ks[K + k];
       skz[threadIdx.x] = ks[2 * K + k];
-      sl[threadIdx.x] = Lb[k];
+      const double2 lv = Lb[k];
+      const double wt = wk ? wk[k] : 1.0;  // per-point quadrature weight (ragged rows, R-15)
+      sl[threadIdx.x] = make_double2(wt * lv.x, wt * lv.y);
     }
     __syncthreads();
 #pragma unroll 2
@@ -336,6 +339,7 @@ __global__ void __launch_bounds__(L2T_TPB, 5) l2t_kernel(PointsDev pts, const in
       a1i = fma(e1.x, l.y, fma(e1.y, l.x, a1i));
     }
   }
+  if (wk) w = 1.0;
   if (i0 < tend) y_far[i0] = make_double2(w * a0r, w * a0i);
   if (i1 < tend) y_far[i1] = make_double2(w * a1r, w * a1i);
 }
@@ -343,9 +347,9 @@ __global__ void __launch_bounds__(L2T_TPB, 5) l2t_kernel(PointsDev pts, const in
 void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const double *cy,
                 const double *cz, const int32_t *tile_leaf, const int64_t *tile_begin,
                 int64_t ntiles, const double *ks, int64_t K, const double2 *L, double w,
-                double2 *y_far, cudaStream_t s) {
+                const double *wk, double2 *y_far, cudaStream_t s) {
   if (ntiles <= 0) return;
-  l2t_kernel<<<(unsigned)ntiles, L2T_TPB, 0, s>>>(pts, first, cx, cy, cz, tile_leaf, tile_begin, ks, K, L, w,
+  l2t_kernel<<<(unsigned)ntiles, L2T_TPB, 0, s>>>(pts, first, cx, cy, cz, tile_leaf, tile_begin, ks, K, L, w, wk,
                                                    y_far);
 }
 
@@ -421,6 +425,7 @@ __global__ void __launch_bounds__(SMALL_TPB) l2t_warp_kernel(PointsDev pts, cons
                                                              const double *__restrict__ cz, int32_t box0,
                                                              int32_t box1, const double *__restrict__ ks,
                                                              int64_t K, const double2 *__restrict__ L, double w,
+                                                             const double *__restrict__ wk,
                                                              double2 *__restrict__ y_far) {
   __shared__ double2 tab[TAB];
   fill_exp_table(tab);
@@ -443,14 +448,16 @@ __global__ void __launch_bounds__(SMALL_TPB) l2t_warp_kernel(PointsDev pts, cons
       double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
       for (int64_t k = slice; k < K; k += 2 * S) {
         {
-          const double2 l = Lb[k];
+          double2 l = Lb[k];
+          if (wk) l = make_double2(wk[k] * l.x, wk[k] * l.y);  // per-point weight (ragged rows, R-15)
           const double2 e = cexpi_u(fma(ks[k], dx, fma(ks[K + k], dy, ks[2 * K + k] * dz)), tab);
           ar = fma(e.x, l.x, fma(-e.y, l.y, ar));
           ai = fma(e.x, l.y, fma(e.y, l.x, ai));
         }
         const int64_t k2 = k + S;
         if (k2 < K) {
-          const double2 l = Lb[k2];
+          double2 l = Lb[k2];
+          if (wk) l = make_double2(wk[k2] * l.x, wk[k2] * l.y);
           const double2 e = cexpi_u(fma(ks[k2], dx, fma(ks[K + k2], dy, ks[2 * K + k2] * dz)), tab);
           br = fma(e.x, l.x, fma(-e.y, l.y, br));
           bi = fma(e.x, l.y, fma(e.y, l.x, bi));
@@ -461,7 +468,8 @@ __global__ void __launch_bounds__(SMALL_TPB) l2t_warp_kernel(PointsDev pts, cons
         ar += __shfl_xor_sync(0xffffffffu, ar, off);
         ai += __shfl_xor_sync(0xffffffffu, ai, off);
       }
-      if (slice == 0 && valid) y_far[i] = make_double2(w * ar, w * ai);
+      const double ws = wk ? 1.0 : w;
+      if (slice == 0 && valid) y_far[i] = make_double2(ws * ar, ws * ai);
     }
   }
 }
@@ -484,10 +492,10 @@ void launch_s2m_small(PointsDev pts, const int64_t *first, const double *cx, con
 
 void launch_l2t_small(PointsDev pts, const int64_t *first, const double *cx, const double *cy, const double *cz,
                       int32_t box0, int32_t box1, const double *ks, int64_t K, const double2 *L, double w,
-                      double2 *y_far, cudaStream_t s) {
+                      const double *wk, double2 *y_far, cudaStream_t s) {
   if (box1 <= box0) return;
   l2t_warp_kernel<<<persistent_grid(box1 - box0, (const void *)l2t_warp_kernel), SMALL_TPB, 0, s>>>(
-      pts, first, cx, cy, cz, box0, box1, ks, K, L, w, y_far);
+      pts, first, cx, cy, cz, box0, box1, ks, K, L, w, wk, y_far);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -51,6 +51,9 @@ def check_plan(g, plan):
         op = plan.levels[lv["level"]]
         assert (lv["ell"], lv["n_theta"], lv["n_phi"]) == (op.ell, op.n_theta, op.n_phi), lv["level"]
         assert lv["rep"] == op.rep, lv["level"]
+        assert lv["ragged"] == (op.rows is not None), lv["level"]
+        if lv["level"] <= (plan.source_level or 1):
+            assert lv["K"] == op.K, lv["level"]
         assert lv["alpha"] == op.alpha, lv["level"]
         if lv["level"] <= (plan.L_f or 1) + 1 and not math.isnan(op.F):
             assert lv["active"] == op.active
@@ -131,6 +134,55 @@ def test_deep_stages(deep):
 def test_deep_matvec_parity_and_accuracy(deep):
     cfg, x, q, plan, f, g, y = deep
     assert rel(y, f.matvec(q)) <= PARITY
+    assert rel(y, direct_sum(x, q, cfg.kappa)) <= cfg.eps
+
+
+# ---- ragged quadrature on the active levels (R-15, HFMM_RAGGED) ---------------------
+@pytest.fixture(scope="module")
+def ragged(hf):
+    cfg = small_config("rag", n=700, kappa=32 * math.pi, depth=3, eps=1e-6, seed=23)
+    x, q = points_and_charges(cfg)
+    g = gpu_plan(hf, cfg, x, flags=hf.HFMM_RAGGED)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, ragged=True)
+    f = OracleFMM(x, cfg.lo, cfg.size, plan)
+    y = g.matvec(q)
+    return cfg, x, q, plan, f, g, y
+
+
+def test_ragged_plan_and_tables(ragged):
+    cfg, x, q, plan, f, g, y = ragged
+    assert plan.L_f == 3 and all(plan.levels[l].rows is not None for l in (2, 3))
+    check_plan(g, plan)
+    offs = offsets316()
+    for l in (2, 3):
+        T = g.debug(3, l).reshape(316, -1)
+        for oid in (0, 57, 123, 200, 315):
+            assert rel(T[oid], f.table(l, offs[oid])) <= 1e-12, (l, oid)
+
+
+def test_ragged_stages_and_matvec(ragged):
+    cfg, x, q, plan, f, g, y = ragged
+    M, I, Lloc = f.far_locals(q)
+    for l in (2, 3):
+        mp = box_map(g, f, l)
+        K = plan.levels[l].K
+        for what, ref in ((0, M), (1, I), (2, Lloc)):
+            got = g.debug(what, l).reshape(-1, K)
+            assert rel(got, np.stack([ref[l][mp[b]] for b in range(len(mp))])) <= PARITY, (what, l)
+    assert rel(y, f.matvec(q)) <= PARITY
+    assert rel(y, direct_sum(x, q, cfg.kappa)) <= cfg.eps
+
+
+def test_ragged_with_translation_levels(hf):
+    """Ragged active levels + rectangular translation-only levels below L_f (R-14 + R-15)."""
+    cfg = small_config("ragdeep", n=2500, kappa=16 * math.pi, depth=5, eps=1e-6, seed=5)
+    x, q = points_and_charges(cfg)
+    g = gpu_plan(hf, cfg, x, flags=hf.HFMM_RAGGED | hf.HFMM_SOURCE_AT_DEPTH)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=cfg.depth, ragged=True)
+    check_plan(g, plan)
+    t = np.arange(0, cfg.n, 4)
+    y = g.matvec(q)
+    assert rel(y[t], OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q, t)) <= PARITY
     assert rel(y, direct_sum(x, q, cfg.kappa)) <= cfg.eps
 
 

@@ -76,6 +76,16 @@ def test_host_rep_grid_equals_oracle(ka, a, eps):
     assert hf.rep_grid(ka, a, eps) == rep_grid(ka, a, eps)
 
 
+@pytest.mark.parametrize("ka,eps", [(8 * math.pi, 1e-6), (16 * math.pi, 1e-8), (32 * math.pi, 2e-6)])
+def test_host_ragged_rows_equal_oracle(ka, eps):
+    """Ragged rows (R-15) of the library == the oracle's (independent implementations)."""
+    from oracle.plan import LevelPlan, ragged_rows
+    ell, nth, nph, _ = level_params(ka, 1.0, eps, 0.8)
+    lp = LevelPlan(2, 1.0, ell, nth, nph, alpha=0.8)
+    want = ragged_rows(lp, ka, eps, eps_absolute=True)
+    assert hf.ragged_rows(ka, 1.0, eps, 0.8, ell, nth, nph) == want
+
+
 def test_plan_rejects_bad_args():
     with pytest.raises(hf.HFMMError):
         hf.level_quadrature(-1.0, 1.0, 1e-6, 0.8)
