@@ -391,6 +391,13 @@ __device__ __forceinline__ double2 *fft_batch_padin(double2 *X, double2 *a, doub
 }
 
 constexpr int RS_TPB = 128;
+#ifndef HFMM_RS_COLS_TPB
+#define HFMM_RS_COLS_TPB 128
+#endif
+#ifndef HFMM_RS_COLS_KB
+#define HFMM_RS_COLS_KB 0  // 0: the size plan's budget
+#endif
+constexpr int RS_COLS_TPB = HFMM_RS_COLS_TPB;
 
 // 16-byte global -> shared copies issued asynchronously (cp.async, L2 only): a thread's whole
 // share of a tile is in flight at once instead of one load-store round trip at a time.
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict_
 // DOWN (L2L): item = child c, columns m < h of conj(shift[oct[c]]) * in[par[c]] ([nth][h]),
 // resampled nth -> nth2 into out[c][t][m] ([nth2][h]).
 template <bool UP, int MAXR>
-__global__ void __launch_bounds__(RS_TPB) cols_kernel(const double2 *__restrict__ in, int64_t nitem, int nth,
+__global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__restrict__ in, int64_t nitem, int nth,
                                                       int ncols, int rowlen, int nth2, int CB, int cp,
                                                       const int32_t *__restrict__ cbeg, int64_t cbase,
                                                       const int32_t *__restrict__ par,
@@ -579,7 +586,7 @@ static void launch_cols_t(const double2 *in, int64_t nitem, int nth, int ncols, 
   const size_t smem = (size_t)2 * maxn * cp * sizeof(double2);
   set_smem((const void *)cols_kernel<UP, MAXR>, smem);
   const int64_t nstrip = (ncols + CB - 1) / CB;
-  cols_kernel<UP, MAXR><<<(unsigned)(nitem * nstrip), RS_TPB, smem, s>>>(
+  cols_kernel<UP, MAXR><<<(unsigned)(nitem * nstrip), RS_COLS_TPB, smem, s>>>(
       in, nitem, nth, ncols, rowlen, nth2, CB, cp, cbeg, cbase, par, oct, shift, rlen(tw, nth, MAXR),
       rlen(tw, nth2, MAXR), out);
 }
@@ -589,7 +596,8 @@ static void launch_cols(const double2 *in, int64_t nitem, int nth, int ncols, in
                         const int32_t *cbeg, int64_t cbase, const int32_t *par, const int8_t *oct,
                         const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
   if (nitem <= 0 || ncols <= 0) return;
-  const TilePlan tp = tile_plan(std::max(nth, nth2));
+  TilePlan tp = tile_plan(std::max(nth, nth2));
+  if (HFMM_RS_COLS_KB > 0) tp.smem_budget = (size_t)HFMM_RS_COLS_KB * 1024;
   if (tp.maxr >= 16)
     launch_cols_t<UP, 16>(in, nitem, nth, ncols, rowlen, nth2, cbeg, cbase, par, oct, shift, out, tp.smem_budget, tw, s);
   else
