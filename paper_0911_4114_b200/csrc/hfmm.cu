@@ -1166,9 +1166,11 @@ struct OpCache {
     n = nparent;
   }
 };
-OpCache &op_cache() {
-  static OpCache c;
-  return c;
+OpCache &op_cache() {  // per device: the index arrays live in that device's memory
+  static std::map<int, OpCache> caches;
+  int d = 0;
+  cudaGetDevice(&d);
+  return caches[d];
 }
 int cur_device() {
   int d = 0;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <set>
 #include <vector>
 
 #include "hfmm_impl.h"
@@ -116,14 +117,16 @@ struct M2LGroupPlan {
   int16_t *tid8 = nullptr;
 };
 
-static void upload_sym_table() {
-  static bool done = false;
-  if (done) return;
+static void upload_sym_table() {  // __constant__ memory is per device: upload once per device
+  static std::set<int> done;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (done.count(d)) return;
   std::vector<int> cids, sym_of;
   canonical_offsets(cids, sym_of);
   std::vector<int32_t> v(sym_of.begin(), sym_of.end());
   cudaMemcpyToSymbol(c_sym_of, v.data(), sizeof(int32_t) * M2LG_NOFF);
-  done = true;
+  done.insert(d);
 }
 
 // targets [box0, box1) of a level with interaction CSR (row / src / oid: host, row indexed by box

@@ -8,6 +8,7 @@
 // are a small part of the matvec.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <map>
 
 #include "hfmm_impl.h"
 
@@ -167,15 +168,14 @@ __global__ void __launch_bounds__(RG_TPB) rect2rag_kernel(const double2 *__restr
 }
 
 static const int32_t *twiddle_offsets_device(const TwiddleSet &tw) {
-  // device copy of TwiddleSet::offset (lengths < 1024), cached per TwiddleSet
-  static const TwiddleSet *owner = nullptr;
-  static int32_t *d = nullptr;
-  if (owner != &tw || !d) {
-    if (d) cudaFree(d);
-    cudaMalloc(&d, 1024 * sizeof(int32_t));
-    cudaMemcpy(d, tw.offset, 1024 * sizeof(int32_t), cudaMemcpyHostToDevice);
-    owner = &tw;
-  }
+  // device copy of TwiddleSet::offset (lengths < 1024), one per TwiddleSet (one set per device)
+  static std::map<const TwiddleSet *, int32_t *> copies;
+  auto it = copies.find(&tw);
+  if (it != copies.end()) return it->second;
+  int32_t *d = nullptr;
+  cudaMalloc(&d, 1024 * sizeof(int32_t));
+  cudaMemcpy(d, tw.offset, 1024 * sizeof(int32_t), cudaMemcpyHostToDevice);
+  copies[&tw] = d;
   return d;
 }
 
