@@ -31,10 +31,10 @@ import numpy as np  # noqa: E402
 
 # FP64 flops (FMA = 2) of the P2P arithmetic as implemented (DESIGN.md "Kernels and their
 # rooflines"): one kernel evaluation G = e^{i kappa R}/R on positions pre-scaled to table steps
-# costs 38 (difference 3, r^2 5, rsqrt Newton step 8, R 1, e^{ih R_u} 19, 1/R scaling 2; the
+# costs 39 (difference 3, r^2 5, rsqrt Newton step 8, e^{ih R_u} from the product r^2 (1/r) 21, 1/R scaling 2; the
 # MUFU.RSQ64H seed is not an FP64-pipe op); every ORDERED pair adds a complex MAC (8).  The
 # symmetric kernel evaluates G once per unordered pair and applies it to both rows.
-P2P_FLOPS_PER_EVAL = 38
+P2P_FLOPS_PER_EVAL = 39
 P2P_FLOPS_PER_MAC = 8
 
 

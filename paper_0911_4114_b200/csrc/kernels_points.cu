@@ -49,6 +49,20 @@ __device__ __forceinline__ double2 cexpi_u(double u, const double2 *__restrict__
   return make_double2(fma(e.x, c, -e.y * s), fma(e.x, s, e.y * c));
 }
 
+// e^{i h a b} for a phase given as a product a b (P2P: r^2 * (1/r)): the rounding to the nearest
+// step comes straight from the exact product, k = round(a b) = fma(a, b, 1.5 * 2^52) - 1.5 * 2^52,
+// and the remainder r = fma(a, b, -k) is rounded once -- one DMUL fewer than forming a b first.
+__device__ __forceinline__ double2 cexpi_prod(double a, double b, const double2 *__restrict__ tab) {
+  const double t = fma(a, b, kMagic);
+  const int k = __double2loint(t);
+  const double r = fma(a, b, -(t - kMagic));
+  const double r2 = r * r;
+  const double s = r * fma(r2, fma(r2, kS5, kS3), kS1);
+  const double c = fma(r2, fma(r2, kC4, kC2), 1.0);
+  const double2 e = tab[k & (TAB - 1)];
+  return make_double2(fma(e.x, c, -e.y * s), fma(e.x, s, e.y * c));
+}
+
 // 1/sqrt(r2) for r2 > 0: hardware approximation of the high word, one cubic Newton step.
 __device__ __forceinline__ double rsqrt_fast(double r2) {
   double y;
@@ -77,7 +91,7 @@ __device__ __forceinline__ double2 green_u(double tx, double ty, double tz, doub
   const double dx = tx - xs, dy = ty - ys, dz = tz - zs;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   const double ri = rsqrt_fast(r2);
-  const double2 e = cexpi_u(r2 * ri, tab);
+  const double2 e = cexpi_prod(r2, ri, tab);  // e^{i h R_u}, R_u = r2 / sqrt(r2)
   return make_double2(e.x * ri, e.y * ri);
 }
 
@@ -120,7 +134,7 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU
         const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
         double ri = rsqrt_fast(r2);
         if (DIAG) ri = (r2 > 0.0) ? ri : 0.0;  // self pair excluded
-        const double2 e = cexpi_u(r2 * ri, tab);
+        const double2 e = cexpi_prod(r2, ri, tab);
         const double gr = e.x * ri, gi = e.y * ri;
         ar[p] = fma(gr, q.x, fma(-gi, q.y, ar[p]));
         ai[p] = fma(gr, q.y, fma(gi, q.x, ai[p]));
