@@ -84,7 +84,7 @@ TwiddleSet &global_twiddles(int device) {
   auto it = sets.find(device);
   if (it != sets.end()) return *it->second;
   std::vector<int> lens;
-  for (int N = 2; N < 1024; ++N)
+  for (int N = 2; N < kMaxFFT; ++N)
     if (seven_smooth(N)) lens.push_back(N);
   auto ts = std::make_unique<TwiddleSet>();
   ts->build(lens);
@@ -593,6 +593,12 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       L.T = Tr;
     }
   }
+  for (int l = 2; l <= p->D_s; ++l)
+    if (p->lv[l].nth >= kMaxFFT || p->lv[l].nph >= kMaxFFT) {
+      p->err = "hfmm_precompute: level " + std::to_string(l) + " grid " + std::to_string(p->lv[l].nth) + " x " +
+               std::to_string(p->lv[l].nph) + " exceeds the resampling kernels' limit (" + std::to_string(kMaxFFT) + ")";
+      return HFMM_E_SEARCH;
+    }
   // device data of the levels 2..D_s (M2L data only on the active levels 2..L_f)
   size_t tmp_need = 0, scr1_need = 0, scr2_need = 0;
   for (int l = 2; l <= p->D_s; ++l) {
@@ -1182,8 +1188,8 @@ bool up_or_down(int nth, int nph, int nth2, int nph2, bool *up) {
   else if (nth2 <= nth && nph2 <= nph) *up = false;
   else return false;
   return (nth % 2 == 0) && (nth2 % 2 == 0) && (nph % 2 == 0) && (nph2 % 2 == 0) && seven_smooth(nth) &&
-         seven_smooth(nth2) && seven_smooth(nph) && seven_smooth(nph2) && nth < 1024 && nth2 < 1024 &&
-         nph < 1024 && nph2 < 1024;
+         seven_smooth(nth2) && seven_smooth(nph) && seven_smooth(nph2) && nth < kMaxFFT && nth2 < kMaxFFT &&
+         nph < kMaxFFT && nph2 < kMaxFFT;
 }
 }  // namespace
 

@@ -77,10 +77,12 @@ struct ResampleDims {
   int nth2, nph2;  // target grid
 };
 
+// Longest 1-D transform supported by the resampling kernels (grids N_theta, N_phi < kMaxFFT).
+constexpr int kMaxFFT = 4096;
 // twiddle table e^{-2 pi i t / N}, t < N, for every length of a plan (device, concatenated)
 struct TwiddleSet {
   double2 *d = nullptr;
-  int offset[1024];  // offset[N] into d, -1 if absent (N < 1024)
+  int offset[kMaxFFT];  // offset[N] into d, -1 if absent (N < kMaxFFT)
   void build(const std::vector<int> &lengths);
   void free_all();
 };

@@ -35,10 +35,10 @@
 namespace hfmm {
 
 void TwiddleSet::build(const std::vector<int> &lengths) {
-  for (int i = 0; i < 1024; ++i) offset[i] = -1;
+  for (int i = 0; i < kMaxFFT; ++i) offset[i] = -1;
   std::vector<double2> h;
   for (int N : lengths) {
-    if (N <= 0 || N >= 1024 || offset[N] >= 0) continue;
+    if (N <= 0 || N >= kMaxFFT || offset[N] >= 0) continue;
     offset[N] = (int)h.size();
     for (int t = 0; t < N; ++t) {
       long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)t / (long double)N;

@@ -168,13 +168,13 @@ __global__ void __launch_bounds__(RG_TPB) rect2rag_kernel(const double2 *__restr
 }
 
 static const int32_t *twiddle_offsets_device(const TwiddleSet &tw) {
-  // device copy of TwiddleSet::offset (lengths < 1024), one per TwiddleSet (one set per device)
+  // device copy of TwiddleSet::offset (lengths < kMaxFFT), one per TwiddleSet (one set per device)
   static std::map<const TwiddleSet *, int32_t *> copies;
   auto it = copies.find(&tw);
   if (it != copies.end()) return it->second;
   int32_t *d = nullptr;
-  cudaMalloc(&d, 1024 * sizeof(int32_t));
-  cudaMemcpy(d, tw.offset, 1024 * sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaMalloc(&d, kMaxFFT * sizeof(int32_t));
+  cudaMemcpy(d, tw.offset, kMaxFFT * sizeof(int32_t), cudaMemcpyHostToDevice);
   copies[&tw] = d;
   return d;
 }

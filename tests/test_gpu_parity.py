@@ -320,16 +320,21 @@ def test_edge_cases(hf):
 
 
 @pytest.mark.parametrize("up", [True, False])
-@pytest.mark.parametrize("grids", [((16, 16), (24, 28)), ((90, 96), (120, 120)), ((54, 56), (108, 108))])
+@pytest.mark.parametrize("grids", [((16, 16), (24, 28)), ((90, 96), (120, 120)), ((54, 56), (108, 108)),
+                                   ((432, 432), (1080, 1080))])    # beyond 1024 points (kMaxFFT = 4096)
 def test_resample_operator(hf, up, grids):
     import torch
     from oracle.resample import resample_half_batch
     (a, b) = grids if up else grids[::-1]
     rng = np.random.default_rng(7)
-    F = rng.standard_normal((5, a[0], a[1] // 2)) + 1j * rng.standard_normal((5, a[0], a[1] // 2))
+    nb = 5 if max(a + b) < 1000 else 2
+    F = rng.standard_normal((nb, a[0], a[1] // 2)) + 1j * rng.standard_normal((nb, a[0], a[1] // 2))
     inp = torch.from_numpy(F).cuda()
-    out = torch.empty((5, b[0], b[1] // 2), dtype=torch.complex128, device="cuda")
+    out = torch.empty((nb, b[0], b[1] // 2), dtype=torch.complex128, device="cuda")
     hf.resample(inp, a[0], a[1], b[0], b[1], out)
     torch.cuda.synchronize()
     ref = resample_half_batch(F, a[1], b[0], b[1])
-    assert rel(out.cpu().numpy(), ref) <= 1e-13
+    # the oracle's dense DFT matrices evaluate e^{-2 pi i j k / N} at arguments up to ~pi N, so
+    # their own entries carry ~u pi N / 2 relative error (2e-13 at N = 1080): tolerance grows with N
+    tol = max(1e-13, 1.1e-16 * 3.14159 * max(a + b) * 2)
+    assert rel(out.cpu().numpy(), ref) <= tol
