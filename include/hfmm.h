@@ -77,6 +77,8 @@ extern "C" {
 #define HFMM_HOST 0    /* q and y are host pointers (pinned or pageable)                     */
 #define HFMM_DEVICE 1  /* q and y are device pointers on the plan's device                   */
 #define HFMM_Y_LOCAL 2 /* OR-able with the above: multi-GPU, skip the final y all-gather     */
+#define HFMM_SERIAL 4  /* OR-able: near field and far chain one after the other on one stream
+                          (measurement: kernel times without the two streams sharing SMs)   */
 
 #define HFMM_MAX_LEVELS 16
 

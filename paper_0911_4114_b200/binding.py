@@ -28,6 +28,7 @@ HFMM_RAGGED = 0x20
 HFMM_HOST = 0
 HFMM_DEVICE = 1
 HFMM_Y_LOCAL = 2
+HFMM_SERIAL = 4
 MAX_LEVELS = 16
 
 EXPORTED = [
@@ -211,8 +212,8 @@ class HFMM:
     def precompute(self, kappa: float, eps: float, alpha: float = 0.8, tau: float = 0.0, flags: int = 0):
         return self._check(self.lib.hfmm_precompute(self.h, kappa, eps, alpha, tau, flags))
 
-    def _apply(self, fn, q, out=None, stream=None, local=False):
-        mem_local = HFMM_Y_LOCAL if local else 0
+    def _apply(self, fn, q, out=None, stream=None, local=False, serial=False):
+        mem_local = (HFMM_Y_LOCAL if local else 0) | (HFMM_SERIAL if serial else 0)
         if hasattr(q, "is_cuda") and q.is_cuda:
             import torch
             if out is None:
@@ -235,9 +236,9 @@ class HFMM:
         self._check(fn(self.h, q.ctypes.data, out.ctypes.data, HFMM_HOST | mem_local, None))
         return out
 
-    def matvec(self, q, out=None, stream=None, local=False):
+    def matvec(self, q, out=None, stream=None, local=False, serial=False):
         """y = A q (eqn:HelmholtzMatrixVector); numpy/CPU tensors use the host path."""
-        return self._apply(self.lib.hfmm_matvec, q, out, stream, local)
+        return self._apply(self.lib.hfmm_matvec, q, out, stream, local, serial)
 
     def direct(self, q, out=None, stream=None):
         return self._apply(self.lib.hfmm_direct, q, out, stream)

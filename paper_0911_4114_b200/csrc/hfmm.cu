@@ -871,7 +871,7 @@ static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
   return HFMM_OK;
 }
 
-static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user) {
+static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool serial) {
   const Tree &t = p->tree;
   const int64_t n = t.n;
   const bool prof = p->profile;
@@ -881,7 +881,6 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user) {
   // near field (low priority) and far-field chain (high priority) forked from the caller's stream
   CK(cudaEventRecord(p->ev_fork, s_user));
   CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
-  CK(cudaStreamWaitEvent(p->stream_hi, p->ev_fork, 0));
   cudaStream_t s = p->stream_hi;
   if (prof) cudaEventRecord(p->sev[7], p->stream2);
   CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), p->stream2));
@@ -893,6 +892,8 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user) {
   }
   if (prof) cudaEventRecord(p->sev[8], p->stream2);
   CK(cudaEventRecord(p->ev_join, p->stream2));
+  // HFMM_SERIAL: the far chain starts after the near field (measurement of undisturbed kernels)
+  CK(cudaStreamWaitEvent(p->stream_hi, serial ? p->ev_join : p->ev_fork, 0));
   const TwiddleSet &tw = global_twiddles(p->device);
   if (p->L_f >= 2) {
     const int Lf = p->L_f, Ds = p->D_s;
@@ -1015,7 +1016,7 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
     launch_p2p_items(pu, p->dir_items, p->dir_nitems, P2P_DIAG, p->uscale, p->dummy_t, p->dummy_s, p->y_near, s);
     launch_combine(p->y_near, nullptr, p->perm, p->y_out, n, 0, n, s);
   } else {
-    int rc = run_matvec(p, qd, s);
+    int rc = run_matvec(p, qd, s, (mem & HFMM_SERIAL) != 0);
     if (rc) return rc;
     if (!local) {
       rc = gather_y(p, s);
