@@ -114,7 +114,10 @@ struct PointsU {
 constexpr int P2P_T = HFMM_P2P_T;
 constexpr int P2P_THREADS = HFMM_P2P_TPB;
 constexpr int64_t P2P_TILE = (int64_t)HFMM_P2P_TPB * HFMM_P2P_T;  // targets per P2P work item
-constexpr int TAB_STEPS = 1024;  // e^{i h k} table size; h = 2 pi / TAB_STEPS
+#ifndef HFMM_TAB_STEPS
+#define HFMM_TAB_STEPS 1024
+#endif
+constexpr int TAB_STEPS = HFMM_TAB_STEPS;  // e^{i h k} table size; h = 2 pi / TAB_STEPS
 enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2 };
 // P2P work items, int64 [nitems][4] = (t0, t1, s0, s1): targets [t0, t1) (<= P2P_TILE), sources
 // [s0, s1).  P2P_SYM: disjoint ranges, rows and columns (each unordered pair once);

@@ -27,6 +27,13 @@ constexpr double kH = 6.283185307179586476925286766559 / TAB;
 constexpr double kS1 = kH, kS3 = -kH * kH * kH / 6.0, kS5 = kH * kH * kH * kH * kH / 120.0;
 constexpr double kC2 = -kH * kH / 2.0, kC4 = kH * kH * kH * kH / 24.0;
 
+// sin(h r) / (h-scaled) polynomial: degree 5 for TAB = 1024 (truncation 2e-18); degree 3 for
+// TAB >= 2048 (|h r| <= pi/2048: truncation (h r)^5/120 <= 7e-17 < u = 2^-53).
+__device__ __forceinline__ double sin_poly(double r, double r2) {
+  if constexpr (TAB >= 2048) return r * fma(r2, kS3, kS1);
+  else return r * fma(r2, fma(r2, kS5, kS3), kS1);
+}
+
 __device__ __forceinline__ void fill_exp_table(double2 *tab) {
   for (int t = threadIdx.x; t < TAB; t += blockDim.x) {
     double s, c;
@@ -43,7 +50,7 @@ __device__ __forceinline__ double2 cexpi_u(double u, const double2 *__restrict__
   const int k = __double2loint(t);
   const double r = u - (t - kMagic);
   const double r2 = r * r;
-  const double s = r * fma(r2, fma(r2, kS5, kS3), kS1);
+  const double s = sin_poly(r, r2);
   const double c = fma(r2, fma(r2, kC4, kC2), 1.0);
   const double2 e = tab[k & (TAB - 1)];
   return make_double2(fma(e.x, c, -e.y * s), fma(e.x, s, e.y * c));
@@ -57,7 +64,7 @@ __device__ __forceinline__ double2 cexpi_prod(double a, double b, const double2 
   const int k = __double2loint(t);
   const double r = fma(a, b, -(t - kMagic));
   const double r2 = r * r;
-  const double s = r * fma(r2, fma(r2, kS5, kS3), kS1);
+  const double s = sin_poly(r, r2);
   const double c = fma(r2, fma(r2, kC4, kC2), 1.0);
   const double2 e = tab[k & (TAB - 1)];
   return make_double2(fma(e.x, c, -e.y * s), fma(e.x, s, e.y * c));

@@ -110,3 +110,27 @@ def test_fullsize_stage_samples(hf, name):
     yn_gpu = g.debug(4)[inv[t]]
     yn_or = f.p2p(q, t)
     assert rel(yn_gpu, yn_or) <= 1e-11
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_fullsize_every_output_vs_gpu_direct(hf, name):
+    """All N outputs, not a sample (SURVEY 8(d) D-4 "full-N direct coverage"): the library's
+    all-pairs sum hfmm_direct (P2P kernel over every ordered pair, eqn:HelmholtzMatrixVector) is
+    first pinned to the compensated CPU direct sum on sampled targets, then the FMM matvec must
+    agree with it within eps over the whole output vector.
+
+    Tolerance of the pin: the GPU sums the n - 1 terms of row i in one FP64 accumulator per target
+    (tile order), whose rounding error is O(sqrt(n) u sum_j |G_ij q_j|) for random rounding; the
+    test allows 8 sqrt(n) u sum_j |G_ij q_j| per target (u = 2^-53), from the oracle's own term sums."""
+    cfg, x, q, g, y = run(hf, name)
+    import torch
+    yd_gpu = g.direct(torch.from_numpy(q).cuda()).cpu().numpy()
+    t = sample_indices(cfg.n, 24, seed=11)
+    yd = direct_sum(x, q, cfg.kappa, t)
+    u = 2.0 ** -53
+    for k, i in enumerate(t):
+        R = np.sqrt(np.sum((x - x[i]) ** 2, axis=1))
+        R[i] = np.inf
+        bound = 8.0 * math.sqrt(cfg.n) * u * float(np.sum(np.abs(q) / R))
+        assert abs(yd_gpu[i] - yd[k]) <= bound, (name, i, abs(yd_gpu[i] - yd[k]), bound)
+    assert rel(y, yd_gpu) <= cfg.eps, (name, rel(y, yd_gpu))
