@@ -98,6 +98,8 @@ typedef struct {
   int64_t m2l_pairs;/* interaction-list entries at this level (all ranks)                  */
   int rep;          /* 1: translation-only level L_f < l <= D_s (R-14; ell = 0, F = NaN)   */
   int ragged;       /* 1: ragged rows N_phi(theta_n) (R-15, HFMM_RAGGED); K = stored points   */
+  int m2l_block;    /* 1: M2L runs the parent-block kernel, 0: the merged-list kernel (both
+                       compute exactly the interaction-list sum; M2L)             */
 } hfmm_level_info;
 
 typedef struct {
@@ -237,6 +239,11 @@ int hfmm_m2l_op(int nbox, int64_t K, const int *row, const int *src, const int *
 int hfmm_m2l_op_plan(int nbox, int64_t K, const int *row, const int *src, const int *oid, void **plan);
 int hfmm_m2l_op_apply(const void *plan, const double *T, const double *M, double *out, void *stream);
 void hfmm_m2l_op_free(void *plan);
+/* Kernel a plan runs: 1 parent-block (every group of 8 is the children of one parent and its lists
+ * are exactly the admissible children of the 26 neighbour parents -- proven per group at plan
+ * time), 0 merged-list; -1 for NULL.  Setting HFMM_M2L_LIST=1 in the environment before a plan is
+ * made forces the merged-list kernel (A/B testing). */
+int hfmm_m2l_op_kind(const void *plan);
 
 #ifdef __cplusplus
 }

@@ -36,7 +36,7 @@ EXPORTED = [
     "hfmm_direct", "hfmm_get_info", "hfmm_stage_times", "hfmm_debug_copy", "hfmm_last_error",
     "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
     "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
-    "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free", "hfmm_ragged_rows",
+    "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free", "hfmm_m2l_op_kind", "hfmm_ragged_rows",
 ]
 
 
@@ -44,7 +44,8 @@ class LevelInfo(C.Structure):
     _fields_ = [("level", C.c_int), ("a", C.c_double), ("ell", C.c_int), ("n_theta", C.c_int),
                 ("n_phi", C.c_int), ("alpha", C.c_double), ("K", C.c_int64), ("F", C.c_double),
                 ("active", C.c_int),
-                ("boxes", C.c_int64), ("m2l_pairs", C.c_int64), ("rep", C.c_int), ("ragged", C.c_int)]
+                ("boxes", C.c_int64), ("m2l_pairs", C.c_int64), ("rep", C.c_int), ("ragged", C.c_int),
+                ("m2l_block", C.c_int)]
 
 
 class Info(C.Structure):
@@ -99,6 +100,7 @@ def load() -> C.CDLL:
         "hfmm_m2l_op_plan": (ci, [ci, i64, vp, vp, vp, C.POINTER(vp)]),
         "hfmm_m2l_op_apply": (ci, [vp, vp, vp, vp, vp]),
         "hfmm_m2l_op_free": (None, [vp]),
+        "hfmm_m2l_op_kind": (ci, [vp]),
         "hfmm_ragged_rows": (ci, [dbl, dbl, dbl, dbl, ci, ci, ci, vp]),
     }
     for name, (res, args) in sig.items():
@@ -252,7 +254,7 @@ class HFMM:
             levels.append(dict(level=lv.level, a=lv.a, ell=lv.ell, n_theta=lv.n_theta, n_phi=lv.n_phi,
                                alpha=lv.alpha, K=lv.K,
                                F=lv.F, active=bool(lv.active), boxes=lv.boxes, m2l_pairs=lv.m2l_pairs,
-                               rep=bool(lv.rep), ragged=bool(lv.ragged)))
+                               rep=bool(lv.rep), ragged=bool(lv.ragged), m2l_block=bool(lv.m2l_block)))
         return dict(n=inf.n, depth=inf.depth, L_f=(None if inf.L_f < 0 else inf.L_f), kappa=inf.kappa,
                     eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
                     p2p_sym_pairs=inf.p2p_sym_pairs,
@@ -342,6 +344,11 @@ class M2LOp:
         if rc < 0:
             raise HFMMError(rc, "hfmm_m2l_op_plan")
         self.h = h
+
+    @property
+    def kind(self) -> str:
+        """"block" (parent-block kernel) or "list" (merged-list kernel): hfmm_m2l_op_kind."""
+        return {1: "block", 0: "list"}[self.lib.hfmm_m2l_op_kind(self.h)]
 
     def apply(self, T, M, out, stream=None):
         rc = self.lib.hfmm_m2l_op_apply(self.h, T.data_ptr(), M.data_ptr(), out.data_ptr(), _stream(stream))

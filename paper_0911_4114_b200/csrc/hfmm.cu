@@ -829,6 +829,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     li.F = L.F, li.active = L.active ? 1 : 0, li.boxes = L.nbox, li.m2l_pairs = L.il_nnz;
     li.rep = L.rep ? 1 : 0;
     li.ragged = L.ragged ? 1 : 0;
+    li.m2l_block = (L.m2lg && m2l_group_plan_kind(L.m2lg) == 1) ? 1 : 0;
   }
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
   in.source_level = p->D_s;
@@ -1291,6 +1292,8 @@ extern "C" int hfmm_m2l_op_apply(const void *plan, const double *T, const double
 }
 
 extern "C" void hfmm_m2l_op_free(void *plan) { m2l_group_plan_destroy((M2LGroupPlan *)plan); }
+
+extern "C" int hfmm_m2l_op_kind(const void *plan) { return m2l_group_plan_kind((const M2LGroupPlan *)plan); }
 
 extern "C" int hfmm_m2l_op(int nbox, int64_t K, const int *row, const int *src, const int *oid, const double *T,
                            const double *M, double *out, void *stream) {

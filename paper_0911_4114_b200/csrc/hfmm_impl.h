@@ -115,7 +115,7 @@ constexpr int P2P_T = HFMM_P2P_T;
 constexpr int P2P_THREADS = HFMM_P2P_TPB;
 constexpr int64_t P2P_TILE = (int64_t)HFMM_P2P_TPB * HFMM_P2P_T;  // targets per P2P work item
 #ifndef HFMM_TAB_STEPS
-#define HFMM_TAB_STEPS 1024
+#define HFMM_TAB_STEPS 2048
 #endif
 constexpr int TAB_STEPS = HFMM_TAB_STEPS;  // e^{i h k} table size; h = 2 pi / TAB_STEPS
 enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2 };
@@ -168,6 +168,7 @@ struct M2LGroupPlan;
 M2LGroupPlan *m2l_group_plan_create(int64_t nbox, int64_t K, const int32_t *row, const int32_t *src,
                                     const int32_t *oid, const std::vector<int64_t> *gbeg);
 void m2l_group_plan_destroy(M2LGroupPlan *pl);
+int m2l_group_plan_kind(const M2LGroupPlan *pl);  // 1 parent-block, 0 merged-list, -1 none
 // T: [316][K] (perm == nullptr) or the 34 canonical tables [34][K] with perm [16][K]
 void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *perm, const double2 *M, double2 *I,
                      cudaStream_t s);

@@ -14,12 +14,22 @@
 // per complex MAC bounds the kernel at ~50% of the FP64 pipe (128 B/clk/SM shared vs 2 DFMA
 // warp-instructions/clk/SM).
 //
+// Parent-block variant (m2l_dense_kernel, used when a group's targets are the children of one
+// parent P and its lists are the standard ones): the sources are the children e of the 26
+// neighbour parents P + D, and target d / source (D, e) have offset o = 2D + e - d.  All 64
+// (d, e) pairs of one neighbour parent with the same delta = e - d share one table T[2D + delta]
+// (admissible iff |2D + delta|_inf >= 2), so one shared-memory table load serves 1..8 MACs
+// (1,512 MACs from 604 table loads per interior group instead of 1,512): the shared-memory
+// bound moves above the FP64 pipe.  Both variants compute exactly the CSR's terms; the plan
+// proves the equivalence per group (else it keeps the list variant).
+//
 // Tables: explicit [316][K] (operator entry point, random tables) or the 34 canonical tables
 // + reflection permutations of the matvec (NEXT 3): T_o[k] = T34[c(o)][perm[op(o)][k]].
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <set>
 #include <vector>
 
@@ -43,6 +53,28 @@ __device__ __forceinline__ double2 g_cfma(double2 a, double2 b, double2 c) {
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
 
+// c_did[D][delta] = offset id of o = 2D + delta (D, delta in {-1,0,1}^3, index (x+1)*9 + (y+1)*3
+// + (z+1)), or -1 when |o|_inf <= 1 (adjacent: not in the interaction list)
+__constant__ int16_t c_did[27 * 27];
+
+__device__ __forceinline__ void fill_tables(double2 *Ts, const double2 *__restrict__ T, const int32_t *__restrict__ perm,
+                                            int64_t K, int64_t k0) {
+  for (int i = threadIdx.x; i < M2LG_NOFF * M2LG_KC; i += blockDim.x) {
+    const int o = i / M2LG_KC, kk = i % M2LG_KC;
+    const int64_t kg = k0 + kk;
+    double2 v = make_double2(0.0, 0.0);
+    if (kg < K) {
+      if (perm) {
+        const int32_t code = c_sym_of[o];
+        v = T[(int64_t)(code >> 4) * K + perm[(int64_t)(code & 15) * K + kg]];
+      } else {
+        v = T[(int64_t)o * K + kg];
+      }
+    }
+    Ts[i] = v;
+  }
+}
+
 __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_group_kernel(
     int64_t K, int64_t ngroups, int64_t groups_per_unit, int64_t nunits,
     const int32_t *__restrict__ gtarget /*[G][8]*/, const int32_t *__restrict__ gsrc_row /*[G+1]*/,
@@ -59,20 +91,7 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_group_kernel(
     const int64_t k = k0 + lane;
     const bool kval = k < K;
     __syncthreads();  // previous unit done with Ts
-    for (int i = threadIdx.x; i < M2LG_NOFF * M2LG_KC; i += blockDim.x) {
-      const int o = i / M2LG_KC, kk = i % M2LG_KC;
-      const int64_t kg = k0 + kk;
-      double2 v = make_double2(0.0, 0.0);
-      if (kg < K) {
-        if (perm) {
-          const int32_t code = c_sym_of[o];
-          v = T[(int64_t)(code >> 4) * K + perm[(int64_t)(code & 15) * K + kg]];
-        } else {
-          v = T[(int64_t)o * K + kg];
-        }
-      }
-      Ts[i] = v;
-    }
+    fill_tables(Ts, T, perm, K, k0);
     __syncthreads();
     const int64_t g0 = range * groups_per_unit, g1 = min(ngroups, g0 + groups_per_unit);
     for (int64_t g = g0 + warp; g < g1; g += M2LG_WARPS) {
@@ -110,12 +129,197 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_group_kernel(
   }
 }
 
+// Child slot c = x << 2 | y << 1 | z of a box inside its parent.  gtarget [G][8] by child slot d,
+// gsrc [G][27][8] by neighbour-parent slot D and child slot e (-1: no box), gmask [G] bit D set
+// when parent slot D holds a source.
+__global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
+    int64_t K, int64_t ngroups, int64_t groups_per_unit, int64_t nunits, const int32_t *__restrict__ gtarget,
+    const int32_t *__restrict__ gsrc, const uint32_t *__restrict__ gmask, const double2 *__restrict__ T,
+    const int32_t *__restrict__ perm, const double2 *__restrict__ M, double2 *__restrict__ I) {
+  extern __shared__ double2 Ts[];  // [316][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (K + M2LG_KC - 1) / M2LG_KC;
+  const int64_t ranges = (nunits + nchunks - 1) / nchunks;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t chunk = u / ranges, range = u % ranges;
+    const int64_t k0 = chunk * M2LG_KC;
+    const int64_t k = k0 + lane;
+    const bool kval = k < K;
+    __syncthreads();  // previous unit done with Ts
+    fill_tables(Ts, T, perm, K, k0);
+    __syncthreads();
+    const int64_t g0 = range * groups_per_unit, g1 = min(ngroups, g0 + groups_per_unit);
+    for (int64_t g = g0 + warp; g < g1; g += M2LG_WARPS) {
+      double2 acc[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) acc[a] = make_double2(0.0, 0.0);
+      const uint32_t mask = __ldg(&gmask[g]);
+      for (int D = 0; D < 27; ++D) {
+        if (!((mask >> D) & 1u)) continue;
+        const int4 *sp = reinterpret_cast<const int4 *>(gsrc + (g * 27 + D) * 8);
+        const int4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+        const int32_t sid[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        double2 m[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          m[e] = (sid[e] >= 0 && kval) ? __ldg(&M[(int64_t)sid[e] * K + k]) : make_double2(0.0, 0.0);
+        const int16_t *ids = c_did + D * 27;
+#pragma unroll
+        for (int dl = 0; dl < 27; ++dl) {
+          const int id = ids[dl];
+          if (id < 0) continue;
+          const double2 t = Ts[id * M2LG_KC + lane];
+          const int dx = dl / 9 - 1, dy = (dl / 3) % 3 - 1, dz = dl % 3 - 1;
+#pragma unroll
+          for (int d = 0; d < 8; ++d) {
+            const int ex = (d >> 2) + dx, ey = ((d >> 1) & 1) + dy, ez = (d & 1) + dz;
+            if (ex < 0 || ex > 1 || ey < 0 || ey > 1 || ez < 0 || ez > 1) continue;
+            acc[d] = g_cfma(t, m[(ex << 2) | (ey << 1) | ez], acc[d]);
+          }
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        const int32_t b = gtarget[g * 8 + d];
+        if (b >= 0 && kval) I[(int64_t)b * K + k] = acc[d];
+      }
+    }
+  }
+}
+
 // ---- host plan -----------------------------------------------------------------------------------
 struct M2LGroupPlan {
   int64_t nbox = 0, K = 0, ngroups = 0, nentries = 0;
   int32_t *gtarget = nullptr, *gsrc_row = nullptr, *src_box = nullptr;
   int16_t *tid8 = nullptr;
+  // parent-block variant (dense == true): targets by child slot, sources by (parent slot, child slot)
+  bool dense = false;
+  int64_t dense_macs = 0;  // MACs the parent-block kernel issues (>= nentries)
+  int32_t *dtarget = nullptr, *dsrc = nullptr;
+  uint32_t *dmask = nullptr;
 };
+
+#ifndef HFMM_M2L_DENSE_MIN
+#define HFMM_M2L_DENSE_MIN 0.5  // use the parent-block kernel when useful / issued MACs >= this
+#endif
+
+static void upload_did_table() {
+  static std::set<int> done;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (done.count(d)) return;
+  int16_t t[27 * 27];
+  for (int D = 0; D < 27; ++D)
+    for (int dl = 0; dl < 27; ++dl) {
+      const int o[3] = {2 * (D / 9 - 1) + dl / 9 - 1, 2 * ((D / 3) % 3 - 1) + (dl / 3) % 3 - 1,
+                        2 * (D % 3 - 1) + dl % 3 - 1};
+      const bool adm = std::max(std::abs(o[0]), std::max(std::abs(o[1]), std::abs(o[2]))) >= 2;
+      t[D * 27 + dl] = (int16_t)(adm ? offset_id(o[0], o[1], o[2]) : -1);
+    }
+  cudaMemcpyToSymbol(c_did, t, sizeof(t));
+  done.insert(d);
+}
+
+// Parent-block form of one group, derived from the CSR alone and proven equivalent to it: the
+// targets' relative positions follow from shared sources (o_a(beta) - o_b(beta) = x_b - x_a);
+// a choice of child slots d_a in {0,1}^3 places every source at r = d_a + o_a(beta) relative to
+// the parent's corner (child units), i.e. neighbour parent D = floor(r / 2) in {-1,0,1}^3 \ {0}
+// and child slot e = r - 2D.  Accepted when the placement is consistent and the number of
+// admissible (d, D, e) triples over existing boxes equals the group's CSR entries (each entry is
+// one such triple with the same offset, so the two sums then have the same terms).
+static bool dense_group(int na, const int32_t *tgt, const int32_t *row, const int32_t *src, const int32_t *oid,
+                        int32_t dt[8], int32_t ds[27 * 8], uint32_t &mask, int64_t &macs) {
+  struct Ent { int a; int32_t s; int o[3]; };
+  std::vector<Ent> ents;
+  for (int a = 0; a < na; ++a)
+    for (int32_t e = row[tgt[a]]; e < row[tgt[a] + 1]; ++e) {
+      Ent x{a, src[e], {0, 0, 0}};
+      offset_vec(oid[e], x.o);
+      ents.push_back(x);
+    }
+  // relative target positions p_a (p_0 = 0) through shared sources (entries sorted by source)
+  std::sort(ents.begin(), ents.end(), [](const Ent &x, const Ent &y) { return x.s < y.s; });
+  int p[8][3];
+  bool known[8] = {false};
+  known[0] = true, p[0][0] = p[0][1] = p[0][2] = 0;
+  for (int round = 0; round < 8; ++round) {
+    bool changed = false;
+    for (size_t i = 0; i < ents.size();) {
+      size_t j = i;
+      int ref = -1;
+      while (j < ents.size() && ents[j].s == ents[i].s) {
+        if (ref < 0 && known[ents[j].a]) ref = (int)j;
+        ++j;
+      }
+      if (ref >= 0)
+        for (size_t t = i; t < j; ++t)
+          if (!known[ents[t].a]) {
+            for (int c = 0; c < 3; ++c) p[ents[t].a][c] = p[ents[ref].a][c] + ents[ref].o[c] - ents[t].o[c];
+            known[ents[t].a] = changed = true;
+          }
+      i = j;
+    }
+    if (!changed) break;
+  }
+  for (int a = 0; a < na; ++a)
+    if (!known[a]) return false;
+  for (int c0 = 0; c0 < 8; ++c0) {
+    const int d0[3] = {c0 >> 2, (c0 >> 1) & 1, c0 & 1};
+    bool ok = true;
+    int slot[8];
+    int used = 0;
+    for (int a = 0; a < na && ok; ++a) {
+      int c = 0;
+      for (int i = 0; i < 3; ++i) {
+        const int v = d0[i] + p[a][i];
+        if (v < 0 || v > 1) ok = false;
+        c = 2 * c + v;
+      }
+      if (!ok || (used >> c) & 1) ok = false;
+      used |= 1 << c, slot[a] = c;
+    }
+    if (!ok) continue;
+    for (int i = 0; i < 8; ++i) dt[i] = -1;
+    for (int i = 0; i < 27 * 8; ++i) ds[i] = -1;
+    for (int a = 0; a < na; ++a) dt[slot[a]] = tgt[a];
+    mask = 0;
+    int32_t prev_s = -1, prev_cell = -1;
+    for (const Ent &x : ents) {  // sorted by source: one source, one cell
+      int D = 0, e = 0;
+      for (int i = 0; i < 3; ++i) {
+        const int r = ((slot[x.a] >> (2 - i)) & 1) + x.o[i];
+        const int Q = (r >= 0) ? r / 2 : -((1 - r) / 2);  // floor(r / 2)
+        if (Q < -1 || Q > 1) ok = false;
+        D = 3 * D + (Q + 1), e = 2 * e + (r - 2 * Q);
+      }
+      if (!ok || D == 13) { ok = false; break; }
+      int32_t &cell = ds[D * 8 + e];
+      if ((cell >= 0 && cell != x.s) || (x.s == prev_s && D * 8 + e != prev_cell)) { ok = false; break; }
+      cell = x.s;
+      prev_s = x.s, prev_cell = D * 8 + e;
+      mask |= 1u << D;
+    }
+    if (!ok) continue;
+    int64_t triples = 0, issued = 0;
+    for (int D = 0; D < 27; ++D) {
+      if (!((mask >> D) & 1u)) continue;
+      const int Dv[3] = {D / 9 - 1, (D / 3) % 3 - 1, D % 3 - 1};
+      for (int d = 0; d < 8; ++d)
+        for (int e = 0; e < 8; ++e) {
+          int inf = 0;
+          for (int i = 0; i < 3; ++i)
+            inf = std::max(inf, std::abs(2 * Dv[i] + ((e >> (2 - i)) & 1) - ((d >> (2 - i)) & 1)));
+          if (inf < 2) continue;
+          ++issued;
+          if (dt[d] >= 0 && ds[D * 8 + e] >= 0) ++triples;
+        }
+    }
+    if (triples != (int64_t)ents.size()) continue;
+    macs += issued;
+    return true;
+  }
+  return false;
+}
 
 static void upload_sym_table() {  // __constant__ memory is per device: upload once per device
   static std::set<int> done;
@@ -170,6 +374,24 @@ M2LGroupPlan *m2l_group_plan_create(int64_t nbox, int64_t K, const int32_t *row,
   }
   pl->ngroups = G;
   pl->nentries = (int64_t)sbox.size();
+  // parent-block form when every group has one and it does not waste too many MACs
+  std::vector<int32_t> dtg((size_t)G * 8), dsr((size_t)G * 27 * 8);
+  std::vector<uint32_t> dmk((size_t)G);
+  bool dense = G > 0;
+  int64_t macs = 0, entries = 0;
+  for (int64_t g = 0; g < G && dense; ++g) {
+    const int na = (int)(gb[g + 1] - gb[g]);
+    int32_t tg[8];
+    for (int a = 0; a < na; ++a) tg[a] = (int32_t)(gb[g] + a);
+    entries += row[gb[g + 1]] - row[gb[g]];
+    dense = dense_group(na, tg, row, src, oid, &dtg[(size_t)g * 8], &dsr[(size_t)g * 27 * 8], dmk[g], macs);
+  }
+  const char *force_list = getenv("HFMM_M2L_LIST");
+  if (force_list && atoi(force_list) != 0) dense = false;
+  if (dense && macs > 0 && (double)entries >= HFMM_M2L_DENSE_MIN * (double)macs) {
+    pl->dense = true;
+    pl->dense_macs = macs;
+  }
   auto up = [](const void *h, size_t bytes) -> void * {
     void *d = nullptr;
     if (bytes && cudaMalloc(&d, bytes) == cudaSuccess) cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice);
@@ -179,12 +401,20 @@ M2LGroupPlan *m2l_group_plan_create(int64_t nbox, int64_t K, const int32_t *row,
   pl->gsrc_row = (int32_t *)up(grow.data(), grow.size() * 4);
   pl->src_box = (int32_t *)up(sbox.data(), sbox.size() * 4);
   pl->tid8 = (int16_t *)up(t8.data(), t8.size() * 2);
+  if (pl->dense) {
+    pl->dtarget = (int32_t *)up(dtg.data(), dtg.size() * 4);
+    pl->dsrc = (int32_t *)up(dsr.data(), dsr.size() * 4);
+    pl->dmask = (uint32_t *)up(dmk.data(), dmk.size() * 4);
+  }
   return pl;
 }
 
+int m2l_group_plan_kind(const M2LGroupPlan *pl) { return pl ? (pl->dense ? 1 : 0) : -1; }
+
 void m2l_group_plan_destroy(M2LGroupPlan *pl) {
   if (!pl) return;
-  for (void *p : {(void *)pl->gtarget, (void *)pl->gsrc_row, (void *)pl->src_box, (void *)pl->tid8})
+  for (void *p : {(void *)pl->gtarget, (void *)pl->gsrc_row, (void *)pl->src_box, (void *)pl->tid8,
+                  (void *)pl->dtarget, (void *)pl->dsrc, (void *)pl->dmask})
     if (p) cudaFree(p);
   delete pl;
 }
@@ -206,8 +436,15 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
   ranges = (pl->ngroups + gpu - 1) / gpu;
   const int64_t nunits = nchunks * ranges;
   const unsigned grid = (unsigned)std::min<int64_t>(nunits, nsm);
-  m2l_group_kernel<<<grid, 32 * M2LG_WARPS, smem, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->gtarget, pl->gsrc_row,
-                                                       pl->src_box, pl->tid8, T, perm, M, I);
+  if (pl->dense) {
+    upload_did_table();
+    cudaFuncSetAttribute(m2l_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    m2l_dense_kernel<<<grid, 32 * M2LG_WARPS, smem, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget, pl->dsrc,
+                                                         pl->dmask, T, perm, M, I);
+  } else {
+    m2l_group_kernel<<<grid, 32 * M2LG_WARPS, smem, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->gtarget,
+                                                         pl->gsrc_row, pl->src_box, pl->tid8, T, perm, M, I);
+  }
 }
 
 }  // namespace hfmm

@@ -4,12 +4,13 @@
 //   L2T  field computation int L e^{i kappa s.(c_a - x_i)} dS
 //   permute / combine (Morton order <-> caller order)
 // The three main kernels are bound by the FP64 pipe: one complex exponential per pair or per
-// (point, direction).  Every phase arrives in units of the table step h = 2 pi/1024 (positions
+// (point, direction).  Every phase arrives in units of the table step h = 2 pi/TAB (positions
 // pre-scaled by kappa/h for P2P, directions kappa s/h for S2M/L2T, both at precompute), so e^{ix}
 // (cexpi_u below) needs no range-reduction multiply: round to the nearest step with the
 // 1.5 * 2^52 "magic number" (no FRND/F2I), exact remainder |r| <= 1/2 step, table
-// e^{2 pi i k/1024} in shared memory, Taylor polynomials of degree 5 (sin) and 4 (cos) whose
-// truncation error (< 2e-18) is below the double rounding of the result: 13 FP64 instructions.
+// e^{2 pi i k/TAB} in shared memory (TAB = 2048: 32 KB), Taylor polynomials of degree 3 (sin) and
+// 4 (cos) whose truncation error (< 7e-17, |h r| <= pi/2048) is below the double rounding of the
+// result: 12 FP64 instructions (TAB = 1024 needs a degree-5 sine, 13; A/B on C4: -1.6%).
 // Each thread evaluates two items per source (ILP and source-load reuse).
 #include <cuda_runtime.h>
 #include <algorithm>
@@ -22,7 +23,7 @@ namespace hfmm {
 constexpr int TAB = TAB_STEPS;
 constexpr double kMagic = 6755399441055744.0;          // 1.5 * 2^52
 // Taylor coefficients in table-step units h = 2 pi / TAB:  sin(h r) = r (S1 + r^2 (S3 + r^2 S5)),
-// cos(h r) = 1 + r^2 (C2 + r^2 C4), |r| <= 1/2 (|h r| <= pi/1024, truncation < 2e-18).
+// cos(h r) = 1 + r^2 (C2 + r^2 C4), |r| <= 1/2 (|h r| <= pi/TAB, truncation (h r)^6/720).
 constexpr double kH = 6.283185307179586476925286766559 / TAB;
 constexpr double kS1 = kH, kS3 = -kH * kH * kH / 6.0, kS5 = kH * kH * kH * kH * kH / 120.0;
 constexpr double kC2 = -kH * kH / 2.0, kC4 = kH * kH * kH * kH / 24.0;
@@ -44,7 +45,7 @@ __device__ __forceinline__ void fill_exp_table(double2 *tab) {
 
 // e^{i h u} for a phase u given in table steps (h = 2 pi / TAB): u is rounded to the nearest
 // integer k with the 1.5 * 2^52 magic number (exact for |u| < 2^51), the remainder r = u - k is
-// exact (Sterbenz), and e^{i h u} = e^{2 pi i k / TAB} * e^{i h r}.  13 FP64 instructions.
+// exact (Sterbenz), and e^{i h u} = e^{2 pi i k / TAB} * e^{i h r}.
 __device__ __forceinline__ double2 cexpi_u(double u, const double2 *__restrict__ tab) {
   const double t = u + kMagic;
   const int k = __double2loint(t);

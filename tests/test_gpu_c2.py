@@ -106,7 +106,7 @@ class _Periodic(dict):
 
 
 @pytest.mark.parametrize("B", [8, 32])
-def test_c2_m2l(hf, lattice, B):
+def test_c2_m2l(hf, lattice, B, monkeypatch):
     import torch
     g, row, src, oid, offs = lattice
     nbox = len(g)
@@ -122,9 +122,21 @@ def test_c2_m2l(hf, lattice, B):
     hf.m2l_op(r, s_, o_, T, M, I)
     # the plan-once entry point (what bench.py times) gives the same result
     I2 = torch.empty_like(M)
-    hf.M2LOp(row, src, oid, K).apply(T, M, I2)
+    op = hf.M2LOp(row, src, oid, K)
+    # Morton-ordered lattice: every group of 8 is one parent's children with the standard lists,
+    # so the plan takes the parent-block kernel; the merged-list kernel (forced) sums the same
+    # terms in another order
+    assert op.kind == "block"
+    op.apply(T, M, I2)
+    monkeypatch.setenv("HFMM_M2L_LIST", "1")
+    op_list = hf.M2LOp(row, src, oid, K)
+    monkeypatch.delenv("HFMM_M2L_LIST")
+    assert op_list.kind == "list"
+    I3 = torch.empty_like(M)
+    op_list.apply(T, M, I3)
     torch.cuda.synchronize()
     assert torch.equal(I, I2)
+    assert float(torch.linalg.norm(I3 - I) / torch.linalg.norm(I)) <= 1e-14
     lev = Level(0, 1.0, [tuple(c) for c in g], _Periodic(g, MICROBENCH["lattice"]), [], np.zeros((nbox, 3)))
     tid = {tuple(int(v) for v in o): k for k, o in enumerate(offs)}
     Th = T.cpu().numpy()
@@ -139,3 +151,4 @@ def test_c2_m2l(hf, lattice, B):
         Mh = M[ks].cpu().numpy()
         ref = sum(Th[tid[o]] * Mh[j] for j, (_, o) in enumerate(il))
         assert rel(I[a].cpu().numpy(), ref) <= TOL
+        assert rel(I3[a].cpu().numpy(), ref) <= TOL

@@ -338,3 +338,26 @@ def test_resample_operator(hf, up, grids):
     # their own entries carry ~u pi N / 2 relative error (2e-13 at N = 1080): tolerance grows with N
     tol = max(1e-13, 1.1e-16 * 3.14159 * max(a + b) * 2)
     assert rel(out.cpu().numpy(), ref) <= tol
+
+
+# ---- the two M2L kernels (M2L): parent-block vs merged-list -------------------------
+@pytest.mark.parametrize("kind", ["cube", "sphere"])
+def test_m2l_kernels_agree(hf, kind, monkeypatch):
+    """The plan proves per group that the parent-block kernel sums exactly the interaction-list
+    terms; forcing the merged-list kernel must then give the same matvec up to summation order,
+    and both match the oracle."""
+    cfg = small_config("m2lk_" + kind, kind=kind, n=4000, kappa=24 * math.pi, depth=4, eps=1e-6, seed=21)
+    x, q = points_and_charges(cfg)
+    g = gpu_plan(hf, cfg, x)
+    monkeypatch.setenv("HFMM_M2L_LIST", "1")
+    g_list = gpu_plan(hf, cfg, x)
+    monkeypatch.delenv("HFMM_M2L_LIST")
+    act = [lv for lv in g.info()["levels"] if lv["active"]]
+    assert act and not any(lv["m2l_block"] for lv in g_list.info()["levels"])
+    if kind == "cube":   # uniform cube: every group is a full parent block
+        assert all(lv["m2l_block"] for lv in act)
+    y, y_list = g.matvec(q), g_list.matvec(q)
+    assert rel(y, y_list) <= 1e-13
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=g.info()["source_level"])
+    y_or = OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q)
+    assert rel(y, y_or) <= PARITY

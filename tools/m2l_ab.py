@@ -19,6 +19,6 @@ for B in (16, 32, 64):
         torch.cuda.synchronize(); e0.record(); op.apply(T, M, I); e1.record(); torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
     t = statistics.median(ms)
-    print(f"{os.path.basename(os.environ.get('HFMM_LIB', 'default'))} B{B}: {t:.3f} ms  "
+    print(f"{os.path.basename(os.environ.get('HFMM_LIB', 'default'))} [{op.kind}] B{B}: {t:.3f} ms  "
           f"{8 * 189 * 65536 * K / t / 1e9 / 37.22:.3f} of FP64", flush=True)
     del M, T, I; op.close(); torch.cuda.empty_cache()
