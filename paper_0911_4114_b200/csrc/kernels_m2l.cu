@@ -19,9 +19,9 @@
 // neighbour parents P + D, and target d / source (D, e) have offset o = 2D + e - d.  All 64
 // (d, e) pairs of one neighbour parent with the same delta = e - d share one table T[2D + delta]
 // (admissible iff |2D + delta|_inf >= 2), so one shared-memory table load serves 1..8 MACs
-// (1,512 MACs from 604 table loads per interior group instead of 1,512): the shared-memory
-// bound moves above the FP64 pipe.  Both variants compute exactly the CSR's terms; the plan
-// proves the equivalence per group (else it keeps the list variant).
+// (an interior group: 702 table loads for 1,664 MACs instead of 1,512 for 1,512) with no
+// per-pair index or branch work.  Both variants compute exactly the CSR's terms; the plan proves
+// the equivalence per group (else it keeps the list variant).
 //
 // Tables: explicit [316][K] (operator entry point, random tables) or the 34 canonical tables
 // + reflection permutations of the matvec (NEXT 3): T_o[k] = T34[c(o)][perm[op(o)][k]].
@@ -44,6 +44,9 @@ constexpr int M2LG_KC = 32;       // directions per chunk (lanes)
 #ifndef HFMM_M2L_PF
 #define HFMM_M2L_PF 4
 #endif
+#ifndef HFMM_M2L_DPF
+#define HFMM_M2L_DPF 0  // parent-block kernel: prefetch the next neighbour parent's sources
+#endif
 constexpr int M2LG_WARPS = HFMM_M2L_WARPS;  // groups in flight per CTA (one CTA per SM: 162 KB table chunk)
 constexpr int M2LG_NOFF = 316;
 
@@ -53,9 +56,10 @@ __device__ __forceinline__ double2 g_cfma(double2 a, double2 b, double2 c) {
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
 
-// c_did[D][delta] = offset id of o = 2D + delta (D, delta in {-1,0,1}^3, index (x+1)*9 + (y+1)*3
-// + (z+1)), or -1 when |o|_inf <= 1 (adjacent: not in the interaction list)
-__constant__ int16_t c_did[27 * 27];
+// c_slot_id[s] = offset id of the cube position s = (ox+3)*49 + (oy+3)*7 + (oz+3), o in [-3,3]^3,
+// or -1 for the 27 adjacent offsets |o|_inf <= 1 (parent-block kernel: their tables are zero)
+constexpr int M2LB_SLOTS = 343;
+__constant__ int16_t c_slot_id[M2LB_SLOTS];
 
 __device__ __forceinline__ void fill_tables(double2 *Ts, const double2 *__restrict__ T, const int32_t *__restrict__ perm,
                                             int64_t K, int64_t k0) {
@@ -131,12 +135,35 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_group_kernel(
 
 // Child slot c = x << 2 | y << 1 | z of a box inside its parent.  gtarget [G][8] by child slot d,
 // gsrc [G][27][8] by neighbour-parent slot D and child slot e (-1: no box), gmask [G] bit D set
-// when parent slot D holds a source.
+// when parent slot D holds a source.  The chunk's tables sit in shared memory by cube position
+// (343 slots, 176 KB) with zero tables at the adjacent offsets, so every (D, delta) reads
+// T[2D + delta] at a compile-time offset from a per-D base and all 64 (d, e) pairs of a
+// neighbour parent run without branches (the adjacent pairs add exact zeros: 9% extra MACs for an
+// interior group, 1,664 issued for 1,512 terms).
+__device__ __forceinline__ void fill_tables_cube(double2 *Ts, const double2 *__restrict__ T,
+                                                 const int32_t *__restrict__ perm, int64_t K, int64_t k0) {
+  for (int i = threadIdx.x; i < M2LB_SLOTS * M2LG_KC; i += blockDim.x) {
+    const int sl = i / M2LG_KC, kk = i % M2LG_KC;
+    const int o = c_slot_id[sl];
+    const int64_t kg = k0 + kk;
+    double2 v = make_double2(0.0, 0.0);
+    if (o >= 0 && kg < K) {
+      if (perm) {
+        const int32_t code = c_sym_of[o];
+        v = T[(int64_t)(code >> 4) * K + perm[(int64_t)(code & 15) * K + kg]];
+      } else {
+        v = T[(int64_t)o * K + kg];
+      }
+    }
+    Ts[i] = v;
+  }
+}
+
 __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
     int64_t K, int64_t ngroups, int64_t groups_per_unit, int64_t nunits, const int32_t *__restrict__ gtarget,
     const int32_t *__restrict__ gsrc, const uint32_t *__restrict__ gmask, const double2 *__restrict__ T,
     const int32_t *__restrict__ perm, const double2 *__restrict__ M, double2 *__restrict__ I) {
-  extern __shared__ double2 Ts[];  // [316][32]
+  extern __shared__ double2 Ts[];  // [343][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nchunks = (K + M2LG_KC - 1) / M2LG_KC;
   const int64_t ranges = (nunits + nchunks - 1) / nchunks;
@@ -146,7 +173,7 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
     const int64_t k = k0 + lane;
     const bool kval = k < K;
     __syncthreads();  // previous unit done with Ts
-    fill_tables(Ts, T, perm, K, k0);
+    fill_tables_cube(Ts, T, perm, K, k0);
     __syncthreads();
     const int64_t g0 = range * groups_per_unit, g1 = min(ngroups, g0 + groups_per_unit);
     for (int64_t g = g0 + warp; g < g1; g += M2LG_WARPS) {
@@ -154,22 +181,33 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
 #pragma unroll
       for (int a = 0; a < 8; ++a) acc[a] = make_double2(0.0, 0.0);
       const uint32_t mask = __ldg(&gmask[g]);
-      for (int D = 0; D < 27; ++D) {
-        if (!((mask >> D) & 1u)) continue;
+      // neighbour parents in mask order; the next parent's 8 source loads are issued before the
+      // current parent's MACs (software pipelining across the L2 latency)
+      auto load8 = [&](int D, double2 *m) {
         const int4 *sp = reinterpret_cast<const int4 *>(gsrc + (g * 27 + D) * 8);
         const int4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
         const int32_t sid[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-        double2 m[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e)
           m[e] = (sid[e] >= 0 && kval) ? __ldg(&M[(int64_t)sid[e] * K + k]) : make_double2(0.0, 0.0);
-        const int16_t *ids = c_did + D * 27;
+      };
+      int D = mask ? __ffs(mask) - 1 : 27;
+      double2 m[8];
+      if (D < 27) load8(D, m);
+      while (D < 27) {
+        const uint32_t rest = mask & ~((2u << D) - 1u);
+        const int Dn = rest ? __ffs(rest) - 1 : 27;
+#if HFMM_M2L_DPF
+        double2 mn[8];
+        if (Dn < 27) load8(Dn, mn);
+#endif
+        // T[2D + delta] = Tb[delta slot offset]: base at cube position 2D + (-1,-1,-1)
+        const int Dx = D / 9 - 1, Dy = (D / 3) % 3 - 1, Dz = D % 3 - 1;
+        const double2 *Tb = Ts + ((2 * Dx + 2) * 49 + (2 * Dy + 2) * 7 + (2 * Dz + 2)) * M2LG_KC + lane;
 #pragma unroll
         for (int dl = 0; dl < 27; ++dl) {
-          const int id = ids[dl];
-          if (id < 0) continue;
-          const double2 t = Ts[id * M2LG_KC + lane];
           const int dx = dl / 9 - 1, dy = (dl / 3) % 3 - 1, dz = dl % 3 - 1;
+          const double2 t = Tb[((dx + 1) * 49 + (dy + 1) * 7 + (dz + 1)) * M2LG_KC];
 #pragma unroll
           for (int d = 0; d < 8; ++d) {
             const int ex = (d >> 2) + dx, ey = ((d >> 1) & 1) + dy, ez = (d & 1) + dz;
@@ -177,6 +215,13 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
             acc[d] = g_cfma(t, m[(ex << 2) | (ey << 1) | ez], acc[d]);
           }
         }
+#if HFMM_M2L_DPF
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m[e] = mn[e];
+#else
+        if (Dn < 27) load8(Dn, m);
+#endif
+        D = Dn;
       }
 #pragma unroll
       for (int d = 0; d < 8; ++d) {
@@ -203,20 +248,18 @@ struct M2LGroupPlan {
 #define HFMM_M2L_DENSE_MIN 0.5  // use the parent-block kernel when useful / issued MACs >= this
 #endif
 
-static void upload_did_table() {
+static void upload_slot_table() {
   static std::set<int> done;
   int d = 0;
   cudaGetDevice(&d);
   if (done.count(d)) return;
-  int16_t t[27 * 27];
-  for (int D = 0; D < 27; ++D)
-    for (int dl = 0; dl < 27; ++dl) {
-      const int o[3] = {2 * (D / 9 - 1) + dl / 9 - 1, 2 * ((D / 3) % 3 - 1) + (dl / 3) % 3 - 1,
-                        2 * (D % 3 - 1) + dl % 3 - 1};
-      const bool adm = std::max(std::abs(o[0]), std::max(std::abs(o[1]), std::abs(o[2]))) >= 2;
-      t[D * 27 + dl] = (int16_t)(adm ? offset_id(o[0], o[1], o[2]) : -1);
-    }
-  cudaMemcpyToSymbol(c_did, t, sizeof(t));
+  int16_t t[M2LB_SLOTS];
+  for (int sl = 0; sl < M2LB_SLOTS; ++sl) {
+    const int o[3] = {sl / 49 - 3, (sl / 7) % 7 - 3, sl % 7 - 3};
+    const bool adm = std::max(std::abs(o[0]), std::max(std::abs(o[1]), std::abs(o[2]))) >= 2;
+    t[sl] = (int16_t)(adm ? offset_id(o[0], o[1], o[2]) : -1);
+  }
+  cudaMemcpyToSymbol(c_slot_id, t, sizeof(t));
   done.insert(d);
 }
 
@@ -309,8 +352,8 @@ static bool dense_group(int na, const int32_t *tgt, const int32_t *row, const in
           int inf = 0;
           for (int i = 0; i < 3; ++i)
             inf = std::max(inf, std::abs(2 * Dv[i] + ((e >> (2 - i)) & 1) - ((d >> (2 - i)) & 1)));
+          ++issued;  // the kernel runs all 64 pairs (adjacent ones against zero tables)
           if (inf < 2) continue;
-          ++issued;
           if (dt[d] >= 0 && ds[D * 8 + e] >= 0) ++triples;
         }
     }
@@ -429,17 +472,19 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nchunks = (pl->K + M2LG_KC - 1) / M2LG_KC;
-  // group ranges per chunk: one chunk spread over all SMs at a time (chunk-major units), so the
-  // chunk's slice of M stays L2-resident while every CTA works on it; >= 8 groups per unit
-  int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((pl->ngroups + M2LG_WARPS - 1) / M2LG_WARPS, nsm));
-  const int64_t gpu = (pl->ngroups + ranges - 1) / ranges;
-  ranges = (pl->ngroups + gpu - 1) / gpu;
+  // units = (chunk, range of groups) in chunk-major order over persistent CTAs, so the CTAs
+  // running at any time share about one chunk and its slice of M stays L2-resident.  A unit holds
+  // whole groups per warp (1..4: balanced warps, the table fill amortised over up to 64 groups).
+  const int64_t per_warp = std::max<int64_t>(1, std::min<int64_t>(4, pl->ngroups / ((int64_t)nsm * M2LG_WARPS)));
+  const int64_t gpu = per_warp * M2LG_WARPS;
+  const int64_t ranges = (pl->ngroups + gpu - 1) / gpu;
   const int64_t nunits = nchunks * ranges;
   const unsigned grid = (unsigned)std::min<int64_t>(nunits, nsm);
   if (pl->dense) {
-    upload_did_table();
-    cudaFuncSetAttribute(m2l_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    m2l_dense_kernel<<<grid, 32 * M2LG_WARPS, smem, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget, pl->dsrc,
+    upload_slot_table();
+    const size_t smem_b = (size_t)M2LB_SLOTS * M2LG_KC * sizeof(double2);
+    cudaFuncSetAttribute(m2l_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
+    m2l_dense_kernel<<<grid, 32 * M2LG_WARPS, smem_b, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget, pl->dsrc,
                                                          pl->dmask, T, perm, M, I);
   } else {
     m2l_group_kernel<<<grid, 32 * M2LG_WARPS, smem, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->gtarget,
