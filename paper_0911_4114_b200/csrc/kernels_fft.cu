@@ -250,33 +250,43 @@ struct FDiv {
   }
 };
 
-// ---- batched vectors: vector v = (group g = v / vper, member u = v % vper) at
-//      base(v) = g * gstride + u * vstride, element e at base + e * estride ----------------------
+// ---- batched vectors: vector v at base v * vstride, element e at base + e * estride ----------------
 struct VecSet {
-  int nvec, vper, gstride, vstride, estride;
+  int nvec, vstride, estride;
 };
-__device__ __forceinline__ int vbase(const VecSet &vs, const FDiv &fper, int v) {
-  int u;
-  const int g = fper.div(v, u);
-  return g * vs.gstride + u * vs.vstride;
-}
+
+// Flat index w = o * n + i visited as w = t, t + T, t + 2T, ... (t = threadIdx.x, T = blockDim.x):
+// (o, i) advance incrementally -- one division per loop instead of one per element.
+struct Walk {
+  int o, i, n, dO, dI;
+  __device__ __forceinline__ Walk(int t, int T, int n_) : n(n_) {
+    o = t / n_, i = t - o * n_;
+    dO = T / n_, dI = T - dO * n_;
+  }
+  __device__ __forceinline__ void next() {
+    i += dI, o += dO;
+    if (i >= n) i -= n, ++o;
+  }
+};
 
 template <int R>
 __device__ __forceinline__ void stockham_pass(const double2 *__restrict__ src, double2 *__restrict__ dst,
                                               const VecSet &vs, int N, int Ns, const double2 *__restrict__ tw) {
-  const int nb = N / R, tstep = N / (Ns * R), total = vs.nvec * nb, es = vs.estride;
-  const FDiv fv(vs.nvec), fper(vs.vper), fns(Ns);
-  for (int w = threadIdx.x; w < total; w += blockDim.x) {
-    int v, k;
-    const int j = fv.div(w, v);
+  const int nb = N / R, tstep = N / (Ns * R), es = vs.estride;
+  const FDiv fns(Ns);
+  // work item w = j * nvec + v: butterfly j of vector v (vector index fastest)
+  for (Walk it(threadIdx.x, blockDim.x, vs.nvec); it.o < nb; it.next()) {
+    const int j = it.o;
+    int k;
     fns.div(j, k);
-    const int b = vbase(vs, fper, v);
+    const int b = it.i * vs.vstride;
     double2 x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = src[b + (j + r * nb) * es];
     if (Ns > 1) {
+      const int kt = k * tstep;
 #pragma unroll
-      for (int r = 1; r < R; ++r) x[r] = c_mul(x[r], __ldg(&tw[k * r * tstep]));
+      for (int r = 1; r < R; ++r) x[r] = c_mul(x[r], __ldg(&tw[r * kt]));
     }
     dft<R>(x);
     const int o = (j - k) * R + k;
@@ -319,14 +329,12 @@ __device__ __forceinline__ double2 *fft_batch(double2 *a, double2 *b, const VecS
 template <int R>
 __device__ __forceinline__ void stockham_pass_padin(const double2 *__restrict__ X, double2 *__restrict__ dst,
                                                     const VecSet &vs, int N, int N2) {
-  const int nb = N2 / R, total = vs.nvec * nb, es = vs.estride;
+  const int nb = N2 / R, es = vs.estride;
   const int K = (min(N, N2) - 1) / 2;
   const double sc = 1.0 / (double)N;
-  const FDiv fv(vs.nvec), fper(vs.vper);
-  for (int w = threadIdx.x; w < total; w += blockDim.x) {
-    int v;
-    const int j = fv.div(w, v);
-    const int b = vbase(vs, fper, v);
+  for (Walk it(threadIdx.x, blockDim.x, vs.nvec); it.o < nb; it.next()) {
+    const int j = it.o;
+    const int b = it.i * vs.vstride;
     double2 x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -421,44 +429,47 @@ __global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict_
   const int64_t total = nbox * nrow;
   const int64_t r0 = (int64_t)blockIdx.x * RB;
   const int nr = (int)min((int64_t)RB, total - r0);
-  // load (e fastest: coalesced half-rows)
-  const FDiv fn(nph);
-  for (int w = threadIdx.x; w < nr * nph; w += blockDim.x) {
-    int e;
-    const int v = fn.div(w, e);
-    const int64_t r = r0 + v;
-    const int64_t b = r / nrow;
-    const int n = (int)(r - b * nrow);
-    const int row = (e < h || n == 0) ? n : nth - n;
-    cp_async16(&A[v * pitch + e], &in[(b * nth + row) * h + (e < h ? e : e - h)]);
+  // load (e fastest: coalesced half-rows); row r0 + v = (box b, grid row n) advanced incrementally
+  {
+    Walk it(threadIdx.x, blockDim.x, nph);
+    int64_t b = (r0 + it.o) / nrow;
+    int n = (int)(r0 + it.o - b * nrow);
+    while (it.o < nr) {
+      const int v = it.o, e = it.i;
+      const int row = (e < h || n == 0) ? n : nth - n;
+      cp_async16(&A[v * pitch + e], &in[(b * nth + row) * h + (e < h ? e : e - h)]);
+      it.next();
+      for (n += it.o - v; n >= nrow; n -= nrow) ++b;
+    }
   }
   cp_async_wait_all();
   __syncthreads();
-  const VecSet vs{nr, nr, 0, pitch, 1};
+  const VecSet vs{nr, pitch, 1};
   double2 *X = fft_batch<MAXR>(A, Bf, vs, L1);
   double2 *Z = fft_batch_padin<MAXR>(X, A, Bf, vs, L2, nph);  // conj of the resampled rows
-  const FDiv fn2(nph2);
-  for (int w = threadIdx.x; w < nr * nph2; w += blockDim.x) {
-    int t;
-    const int v = fn2.div(w, t);
-    const int64_t r = r0 + v;
-    const int64_t b = r / nrow;
-    const int n = (int)(r - b * nrow);
+  Walk it(threadIdx.x, blockDim.x, nph2);
+  int64_t b = (r0 + it.o) / nrow;
+  int n = (int)(r0 + it.o - b * nrow);
+  for (; it.o < nr;) {
+    const int v = it.o, t = it.i;
     double2 val = c_conj(Z[v * pitch + t]);
     if (UP) {
       out[(b * nrow + n) * nph2 + t] = val;
     } else {
-      int orow, oc;
-      if (t < h2) {
-        orow = n, oc = t;
-      } else {
-        if (n == 0 || 2 * n == nth) continue;   // both halves are the same points
+      int orow = n, oc = t;
+      bool st = true;
+      if (t >= h2) {
+        st = !(n == 0 || 2 * n == nth);   // both halves are the same points
         orow = nth - n, oc = t - h2;
       }
-      const int64_t o = (b * nth + orow) * h2 + oc;
-      if (add) val = c_add(val, add[o]);
-      out[o] = val;
+      if (st) {
+        const int64_t o = (b * nth + orow) * h2 + oc;
+        if (add) val = c_add(val, add[o]);
+        out[o] = val;
+      }
     }
+    it.next();
+    for (n += it.o - v; n >= nrow; n -= nrow) ++b;
   }
 }
 
@@ -486,48 +497,48 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
   const int nc = min(CB, ncols - m0);
   const int64_t c0 = UP ? (cbeg ? cbeg[item] : item) : item;
   const int64_t c1 = UP ? (cbeg ? cbeg[item + 1] : item + 1) : item + 1;
-  const FDiv fc(nc);
-  const VecSet vs{nc, nc, 0, 1, cp};
+  const VecSet vs{nc, 1, cp};
   for (int64_t c = c0; c < c1; ++c) {
     if (c > c0) __syncthreads();  // previous child's tile consumed
-    for (int w = threadIdx.x; w < nth * nc; w += blockDim.x) {
-      int mm;
-      const int n = fc.div(w, mm);
-      const int m = m0 + mm;
-      if (UP) {
-        const double2 *t = in + (c - cbase) * (int64_t)(nth / 2 + 1) * rowlen;
-        cp_async16(&A[n * cp + mm],
-                   (2 * n <= nth) ? &t[(int64_t)n * rowlen + m] : &t[(int64_t)(nth - n) * rowlen + m + ncols]);
-      } else {
-        const int64_t p = par ? par[c] : c;
-        cp_async16(&A[n * cp + mm], &in[(p * nth + n) * (int64_t)ncols + m]);
+    const int octc = oct ? oct[c] : 0;
+    if (UP) {
+      const double2 *tb = in + (c - cbase) * (int64_t)(nth / 2 + 1) * rowlen + m0;
+      for (Walk it(threadIdx.x, blockDim.x, nc); it.o < nth; it.next()) {
+        const int n = it.o, mm = it.i;
+        cp_async16(&A[n * cp + mm], (2 * n <= nth) ? &tb[(int64_t)n * rowlen + mm]
+                                                   : &tb[(int64_t)(nth - n) * rowlen + mm + ncols]);
       }
+    } else {
+      const double2 *pb = in + (int64_t)(par ? par[c] : c) * nth * ncols + m0;
+      for (Walk it(threadIdx.x, blockDim.x, nc); it.o < nth; it.next())
+        cp_async16(&A[it.o * cp + it.i], &pb[(int64_t)it.o * ncols + it.i]);
     }
     cp_async_wait_all();
     __syncthreads();
     if (!UP && shift) {  // e^{i kappa s.(c_parent - c_child)} on the parent grid
-      const int64_t so = (int64_t)(oct ? oct[c] : 0) * nth * ncols;
-      for (int w = threadIdx.x; w < nth * nc; w += blockDim.x) {
-        int mm;
-        const int n = fc.div(w, mm);
-        A[n * cp + mm] = c_mul(A[n * cp + mm], c_conj(__ldg(&shift[so + (int64_t)n * ncols + m0 + mm])));
+      const double2 *sb = shift + (int64_t)octc * nth * ncols + m0;
+      for (Walk it(threadIdx.x, blockDim.x, nc); it.o < nth; it.next()) {
+        double2 &a = A[it.o * cp + it.i];
+        a = c_mul(a, c_conj(__ldg(&sb[it.o * ncols + it.i])));
       }
       __syncthreads();
     }
     double2 *X = fft_batch<MAXR>(A, Bf, vs, L1);
     double2 *Z = fft_batch_padin<MAXR>(X, A, Bf, vs, L2, nth);
-    for (int w = threadIdx.x; w < nth2 * nc; w += blockDim.x) {
-      int mm;
-      const int t = fc.div(w, mm);
-      const int m = m0 + mm;
-      double2 v = c_conj(Z[t * cp + mm]);
-      if (UP) {
-        const int64_t o = (item * nth2 + t) * (int64_t)ncols + m;
-        if (shift) v = c_mul(v, shift[((int64_t)(oct ? oct[c] : 0) * nth2 + t) * ncols + m]);
-        out[o] = (c == c0) ? v : c_add(out[o], v);   // same thread owns o for every child
-      } else {
-        out[(c * nth2 + t) * (int64_t)ncols + m] = v;
+    if (UP) {
+      double2 *ob = out + item * nth2 * (int64_t)ncols + m0;
+      const double2 *sb = shift ? shift + (int64_t)octc * nth2 * ncols + m0 : nullptr;
+      for (Walk it(threadIdx.x, blockDim.x, nc); it.o < nth2; it.next()) {
+        const int t = it.o, mm = it.i;
+        double2 v = c_conj(Z[t * cp + mm]);
+        if (sb) v = c_mul(v, sb[t * ncols + mm]);
+        double2 &o = ob[(int64_t)t * ncols + mm];
+        o = (c == c0) ? v : c_add(o, v);   // same thread owns o for every child
       }
+    } else {
+      double2 *ob = out + c * nth2 * (int64_t)ncols + m0;
+      for (Walk it(threadIdx.x, blockDim.x, nc); it.o < nth2; it.next())
+        ob[(int64_t)it.o * ncols + it.i] = c_conj(Z[it.o * cp + it.i]);
     }
   }
 }
