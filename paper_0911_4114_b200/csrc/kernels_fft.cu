@@ -271,11 +271,12 @@ struct Walk {
 
 template <int R>
 __device__ __forceinline__ void stockham_pass(const double2 *__restrict__ src, double2 *__restrict__ dst,
-                                              const VecSet &vs, int N, int Ns, const double2 *__restrict__ tw) {
+                                              const VecSet &vs, const Walk &w0, int N, int Ns,
+                                              const double2 *__restrict__ tw) {
   const int nb = N / R, tstep = N / (Ns * R), es = vs.estride;
   const FDiv fns(Ns);
   // work item w = j * nvec + v: butterfly j of vector v (vector index fastest)
-  for (Walk it(threadIdx.x, blockDim.x, vs.nvec); it.o < nb; it.next()) {
+  for (Walk it = w0; it.o < nb; it.next()) {
     const int j = it.o;
     int k;
     fns.div(j, k);
@@ -298,21 +299,22 @@ __device__ __forceinline__ void stockham_pass(const double2 *__restrict__ src, d
 // forward FFT of every vector (length L.N) in buffer a, ping-pong with b; returns the result buffer
 template <int MAXR>
 __device__ __forceinline__ double2 *fft_batch(double2 *a, double2 *b, const VecSet &vs, const RLen &L) {
+  const Walk w0(threadIdx.x, blockDim.x, vs.nvec);  // (butterfly, vector) walk shared by every pass
   double2 *src = a, *dst = b;
   int Ns = 1;
   for (int s = 0; s < L.nr; ++s) {
     int R;
     switch ((L.codes >> (3 * s)) & 7u) {
       case 0:
-        if (MAXR >= 16) stockham_pass<MAXR >= 16 ? 16 : 8>(src, dst, vs, L.N, Ns, L.tw);
+        if (MAXR >= 16) stockham_pass<MAXR >= 16 ? 16 : 8>(src, dst, vs, w0, L.N, Ns, L.tw);
         R = 16;
         break;
-      case 1: stockham_pass<8>(src, dst, vs, L.N, Ns, L.tw); R = 8; break;
-      case 2: stockham_pass<4>(src, dst, vs, L.N, Ns, L.tw); R = 4; break;
-      case 3: stockham_pass<2>(src, dst, vs, L.N, Ns, L.tw); R = 2; break;
-      case 4: stockham_pass<3>(src, dst, vs, L.N, Ns, L.tw); R = 3; break;
-      case 5: stockham_pass<5>(src, dst, vs, L.N, Ns, L.tw); R = 5; break;
-      default: stockham_pass<7>(src, dst, vs, L.N, Ns, L.tw); R = 7; break;
+      case 1: stockham_pass<8>(src, dst, vs, w0, L.N, Ns, L.tw); R = 8; break;
+      case 2: stockham_pass<4>(src, dst, vs, w0, L.N, Ns, L.tw); R = 4; break;
+      case 3: stockham_pass<2>(src, dst, vs, w0, L.N, Ns, L.tw); R = 2; break;
+      case 4: stockham_pass<3>(src, dst, vs, w0, L.N, Ns, L.tw); R = 3; break;
+      case 5: stockham_pass<5>(src, dst, vs, w0, L.N, Ns, L.tw); R = 5; break;
+      default: stockham_pass<7>(src, dst, vs, w0, L.N, Ns, L.tw); R = 7; break;
     }
     __syncthreads();
     double2 *t = src;
@@ -328,11 +330,11 @@ __device__ __forceinline__ double2 *fft_batch(double2 *a, double2 *b, const VecS
 // (R-6) -- the pad never touches shared memory.
 template <int R>
 __device__ __forceinline__ void stockham_pass_padin(const double2 *__restrict__ X, double2 *__restrict__ dst,
-                                                    const VecSet &vs, int N, int N2) {
+                                                    const VecSet &vs, const Walk &w0, int N, int N2) {
   const int nb = N2 / R, es = vs.estride;
   const int K = (min(N, N2) - 1) / 2;
   const double sc = 1.0 / (double)N;
-  for (Walk it(threadIdx.x, blockDim.x, vs.nvec); it.o < nb; it.next()) {
+  for (Walk it = w0; it.o < nb; it.next()) {
     const int j = it.o;
     const int b = it.i * vs.vstride;
     double2 x[R];
@@ -359,18 +361,19 @@ template <int MAXR>
 __device__ __forceinline__ double2 *fft_batch_padin(double2 *X, double2 *a, double2 *b, const VecSet &vs,
                                                     const RLen &L, int N) {
   double2 *dst = (X == a) ? b : a;
+  const Walk w0(threadIdx.x, blockDim.x, vs.nvec);
   int R0;
   switch (L.codes & 7u) {
     case 0:
-      if (MAXR >= 16) stockham_pass_padin<MAXR >= 16 ? 16 : 8>(X, dst, vs, N, L.N);
+      if (MAXR >= 16) stockham_pass_padin<MAXR >= 16 ? 16 : 8>(X, dst, vs, w0, N, L.N);
       R0 = 16;
       break;
-    case 1: stockham_pass_padin<8>(X, dst, vs, N, L.N); R0 = 8; break;
-    case 2: stockham_pass_padin<4>(X, dst, vs, N, L.N); R0 = 4; break;
-    case 3: stockham_pass_padin<2>(X, dst, vs, N, L.N); R0 = 2; break;
-    case 4: stockham_pass_padin<3>(X, dst, vs, N, L.N); R0 = 3; break;
-    case 5: stockham_pass_padin<5>(X, dst, vs, N, L.N); R0 = 5; break;
-    default: stockham_pass_padin<7>(X, dst, vs, N, L.N); R0 = 7; break;
+    case 1: stockham_pass_padin<8>(X, dst, vs, w0, N, L.N); R0 = 8; break;
+    case 2: stockham_pass_padin<4>(X, dst, vs, w0, N, L.N); R0 = 4; break;
+    case 3: stockham_pass_padin<2>(X, dst, vs, w0, N, L.N); R0 = 2; break;
+    case 4: stockham_pass_padin<3>(X, dst, vs, w0, N, L.N); R0 = 3; break;
+    case 5: stockham_pass_padin<5>(X, dst, vs, w0, N, L.N); R0 = 5; break;
+    default: stockham_pass_padin<7>(X, dst, vs, w0, N, L.N); R0 = 7; break;
   }
   __syncthreads();
   double2 *src = dst, *nxt = X;
@@ -379,15 +382,15 @@ __device__ __forceinline__ double2 *fft_batch_padin(double2 *X, double2 *a, doub
     int R;
     switch ((L.codes >> (3 * s)) & 7u) {
       case 0:
-        if (MAXR >= 16) stockham_pass<MAXR >= 16 ? 16 : 8>(src, nxt, vs, L.N, Ns, L.tw);
+        if (MAXR >= 16) stockham_pass<MAXR >= 16 ? 16 : 8>(src, nxt, vs, w0, L.N, Ns, L.tw);
         R = 16;
         break;
-      case 1: stockham_pass<8>(src, nxt, vs, L.N, Ns, L.tw); R = 8; break;
-      case 2: stockham_pass<4>(src, nxt, vs, L.N, Ns, L.tw); R = 4; break;
-      case 3: stockham_pass<2>(src, nxt, vs, L.N, Ns, L.tw); R = 2; break;
-      case 4: stockham_pass<3>(src, nxt, vs, L.N, Ns, L.tw); R = 3; break;
-      case 5: stockham_pass<5>(src, nxt, vs, L.N, Ns, L.tw); R = 5; break;
-      default: stockham_pass<7>(src, nxt, vs, L.N, Ns, L.tw); R = 7; break;
+      case 1: stockham_pass<8>(src, nxt, vs, w0, L.N, Ns, L.tw); R = 8; break;
+      case 2: stockham_pass<4>(src, nxt, vs, w0, L.N, Ns, L.tw); R = 4; break;
+      case 3: stockham_pass<2>(src, nxt, vs, w0, L.N, Ns, L.tw); R = 2; break;
+      case 4: stockham_pass<3>(src, nxt, vs, w0, L.N, Ns, L.tw); R = 3; break;
+      case 5: stockham_pass<5>(src, nxt, vs, w0, L.N, Ns, L.tw); R = 5; break;
+      default: stockham_pass<7>(src, nxt, vs, w0, L.N, Ns, L.tw); R = 7; break;
     }
     __syncthreads();
     double2 *t = src;
@@ -447,15 +450,19 @@ __global__ void __launch_bounds__(RS_TPB) rows_kernel(const double2 *__restrict_
   const VecSet vs{nr, pitch, 1};
   double2 *X = fft_batch<MAXR>(A, Bf, vs, L1);
   double2 *Z = fft_batch_padin<MAXR>(X, A, Bf, vs, L2, nph);  // conj of the resampled rows
+  if (UP) {  // output row r0 + v = (box b, grid row n) is row b * nrow + n of out
+    double2 *ob = out + r0 * nph2;
+    for (Walk it(threadIdx.x, blockDim.x, nph2); it.o < nr; it.next())
+      ob[it.o * nph2 + it.i] = c_conj(Z[it.o * pitch + it.i]);
+    return;
+  }
   Walk it(threadIdx.x, blockDim.x, nph2);
   int64_t b = (r0 + it.o) / nrow;
   int n = (int)(r0 + it.o - b * nrow);
   for (; it.o < nr;) {
     const int v = it.o, t = it.i;
     double2 val = c_conj(Z[v * pitch + t]);
-    if (UP) {
-      out[(b * nrow + n) * nph2 + t] = val;
-    } else {
+    {
       int orow = n, oc = t;
       bool st = true;
       if (t >= h2) {
@@ -492,8 +499,9 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
   const int maxn = max(nth, nth2);
   double2 *A = sm, *Bf = sm + (size_t)maxn * cp;
   const int nstrip = (ncols + CB - 1) / CB;
-  const int64_t item = blockIdx.x / nstrip;
-  const int m0 = (int)(blockIdx.x % nstrip) * CB;
+  const unsigned bq = blockIdx.x / (unsigned)nstrip;  // 32-bit division (grid < 2^32)
+  const int64_t item = bq;
+  const int m0 = (int)(blockIdx.x - bq * (unsigned)nstrip) * CB;
   const int nc = min(CB, ncols - m0);
   const int64_t c0 = UP ? (cbeg ? cbeg[item] : item) : item;
   const int64_t c1 = UP ? (cbeg ? cbeg[item + 1] : item + 1) : item + 1;
