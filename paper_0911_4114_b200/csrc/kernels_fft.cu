@@ -401,7 +401,10 @@ __device__ __forceinline__ double2 *fft_batch_padin(double2 *X, double2 *a, doub
   return src;
 }
 
-constexpr int RS_TPB = 128;
+#ifndef HFMM_RS_TPB
+#define HFMM_RS_TPB 128
+#endif
+constexpr int RS_TPB = HFMM_RS_TPB;
 #ifndef HFMM_RS_COLS_TPB
 #define HFMM_RS_COLS_TPB 128
 #endif
@@ -557,7 +560,18 @@ struct TilePlan {
   int maxr;
   size_t smem_budget;
 };
-static TilePlan tile_plan(int maxn) { return maxn > 128 ? TilePlan{16, 72 * 1024} : TilePlan{8, 48 * 1024}; }
+#ifndef HFMM_RS_BIG_MAXR
+#define HFMM_RS_BIG_MAXR 16
+#endif
+#ifndef HFMM_RS_BIG_KB
+#define HFMM_RS_BIG_KB 72
+#endif
+#ifndef HFMM_RS_SMALL_KB
+#define HFMM_RS_SMALL_KB 48
+#endif
+static TilePlan tile_plan(int maxn) {
+  return maxn > 128 ? TilePlan{HFMM_RS_BIG_MAXR, (size_t)HFMM_RS_BIG_KB * 1024} : TilePlan{8, (size_t)HFMM_RS_SMALL_KB * 1024};
+}
 
 static void set_smem(const void *fn, size_t bytes) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
