@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "hfmm_impl.h"
@@ -554,6 +555,349 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
   }
 }
 
+// ---- register-resident two-level rows pass (upward) -------------------------------------------
+// A 1-D resample N -> N' with N = N1 N2 and N' = M1 M2 (factors in {1, 2, 4, 8, 16}) by one group of
+// G lanes (G = the largest factor) inside a warp, data in registers between the passes:
+//   forward N:  lane n2 < N2 holds x[N2 n1 + n2] (n1 < N1): DFT_N1, twiddle w_N^{n2 k1}; exchange;
+//               lane k1 < N1 holds the N2 values: DFT_N2 -> X[k1 + N1 k2];
+//   pad:        X through the group's shared buffer; lane m2 < M2 reads Z[M2 m1 + m2] =
+//               conj(X[f]) / N for the kept band |f| <= K (R-6), else 0;
+//   forward N': the same two stages on Z; conj of the result = the resampled vector.
+// Three __syncwarp exchanges per vector instead of one shared round trip per radix pass.
+template <bool UP, int FN1, int FN2, int IN1, int IN2>
+__global__ void __launch_bounds__(128, 3) rows2_kernel(const double2 *__restrict__ in, int64_t nbox, int nth,
+                                                      const double2 *__restrict__ twN,
+                                                      const double2 *__restrict__ twN2,
+                                                      const double2 *__restrict__ add, double2 *__restrict__ out) {
+  constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
+  constexpr int G = (FN1 > IN1 ? FN1 : IN1) > (FN2 > IN2 ? FN2 : IN2) ? (FN1 > IN1 ? FN1 : IN1) : (FN2 > IN2 ? FN2 : IN2);
+  constexpr int BF = FN1 * (FN2 + 1), BI = IN1 * (IN2 + 1);
+  constexpr int BUFW = (BF > BI ? BF : BI) > (N > N2 ? N : N2) ? (BF > BI ? BF : BI) : (N > N2 ? N : N2);
+  constexpr int VW = 32 / G;
+  extern __shared__ double2 sm[];
+  double2 *tw1 = sm, *tw2 = sm + N;           // w_N^j, w_N'^j
+  double2 *bufs = sm + N + N2;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) tw1[j] = twN[j];
+  for (int j = threadIdx.x; j < N2; j += blockDim.x) tw2[j] = twN2[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / G, g = lane - grp * G;
+  double2 *buf = bufs + (size_t)(warp * VW + grp) * BUFW;
+  const int nrow = nth / 2 + 1;
+  constexpr int h = N / 2;
+  const int64_t total = nbox * nrow;
+  constexpr int K = ((N < N2 ? N : N2) - 1) / 2;
+  constexpr double sc = 1.0 / (double)N;
+  const int64_t vstep = (int64_t)gridDim.x * (blockDim.x >> 5) * VW;
+  for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * VW; r0 < total; r0 += vstep) {
+    const int64_t r = r0 + grp;
+    const bool vok = r < total;
+    const int64_t b = vok ? r / nrow : 0;
+    const int n = vok ? (int)(r - b * nrow) : 0;
+    double2 x[16];
+    // forward N, stage 1: lane g < FN2 loads elements e = FN2 n1 + g of the full row (eqn:NumSphereSym)
+    if (vok && g < FN2) {
+      const double2 *lo = in + (b * nth + n) * h, *hi = in + (b * nth + (n == 0 ? 0 : nth - n)) * h;
+#pragma unroll
+      for (int n1 = 0; n1 < FN1; ++n1) {
+        const int e = FN2 * n1 + g;
+        x[n1] = e < h ? lo[e] : hi[e - h];
+      }
+      dft<FN1>(x);
+#pragma unroll
+      for (int k1 = 1; k1 < FN1; ++k1) x[k1] = c_mul(x[k1], tw1[g * k1]);
+#pragma unroll
+      for (int k1 = 0; k1 < FN1; ++k1) buf[k1 * (FN2 + 1) + g] = x[k1];
+    }
+    __syncwarp();
+    if (vok && g < FN1) {  // stage 2: lane k1 -> X[k1 + FN1 k2]
+#pragma unroll
+      for (int n2 = 0; n2 < FN2; ++n2) x[n2] = buf[g * (FN2 + 1) + n2];
+    }
+    __syncwarp();
+    if (vok && g < FN1) {
+      dft<FN2>(x);
+#pragma unroll
+      for (int k2 = 0; k2 < FN2; ++k2) buf[g + FN1 * k2] = x[k2];
+    }
+    __syncwarp();
+    if (vok && g < IN2) {  // padded conj spectrum: lane g holds Z[IN2 m1 + g]
+#pragma unroll
+      for (int m1 = 0; m1 < IN1; ++m1) {
+        const int i = IN2 * m1 + g;
+        const int f = (i <= N2 / 2) ? i : i - N2;
+        double2 z = make_double2(0.0, 0.0);
+        if (f <= K && f >= -K) {
+          const double2 y = buf[f >= 0 ? f : f + N];
+          z = make_double2(y.x * sc, -y.y * sc);
+        }
+        x[m1] = z;
+      }
+    }
+    __syncwarp();
+    if (vok && g < IN2) {
+      dft<IN1>(x);
+#pragma unroll
+      for (int k1 = 1; k1 < IN1; ++k1) x[k1] = c_mul(x[k1], tw2[g * k1]);
+#pragma unroll
+      for (int k1 = 0; k1 < IN1; ++k1) buf[k1 * (IN2 + 1) + g] = x[k1];
+    }
+    __syncwarp();
+    if (vok && g < IN1) {
+#pragma unroll
+      for (int n2 = 0; n2 < IN2; ++n2) x[n2] = buf[g * (IN2 + 1) + n2];
+      dft<IN2>(x);
+      if (UP) {  // full row n of box b
+        double2 *o = out + r * N2;
+#pragma unroll
+        for (int k2 = 0; k2 < IN2; ++k2) o[g + IN1 * k2] = c_conj(x[k2]);
+      } else {   // back to half storage: t < N2/2 -> row n, beyond -> row nth - n (+ add)
+        constexpr int h2 = N2 / 2;
+        const bool mirror = !(n == 0 || 2 * n == nth);
+#pragma unroll
+        for (int k2 = 0; k2 < IN2; ++k2) {
+          const int t = g + IN1 * k2;
+          if (t >= h2 && !mirror) continue;   // both halves are the same points
+          const int64_t o = (b * nth + (t < h2 ? n : nth - n)) * h2 + (t < h2 ? t : t - h2);
+          double2 val = c_conj(x[k2]);
+          if (add) val = c_add(val, add[o]);
+          out[o] = val;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Register-resident two-level columns pass.  CTA = 4 warps = CW = 8 columns (lane & 7) x 16 group
+// lanes (g = 4 warp + lane / 8): every global access of a warp is 4 runs of 8 consecutive columns.
+// UP (M2M / interpolation): unit = (parent, strip); children c in [cbeg[p], cbeg[p+1]) (or the box
+// itself) resampled nth -> nth2 along theta, times shift[oct[c]], summed in registers, stored once.
+// DOWN (L2L / anterpolation): unit = (child c, strip) of conj(shift[oct[c]]) * in[par[c]].
+constexpr int RS2_CW = 8, RS2_CWP = 9;
+template <int A, int B>
+struct Max2 {
+  static constexpr int v = A > B ? A : B;
+};
+
+template <bool UP, int FN1, int FN2, int IN1, int IN2>
+__global__ void __launch_bounds__(128, 3) cols2_kernel(const double2 *__restrict__ in, int64_t nitem, int ncols,
+                                                   int rowlen, const int32_t *__restrict__ cbeg, int64_t cbase,
+                                                   const int32_t *__restrict__ par, const int8_t *__restrict__ oct,
+                                                   const double2 *__restrict__ shift,
+                                                   const double2 *__restrict__ twN,
+                                                   const double2 *__restrict__ twN2, double2 *__restrict__ out) {
+  constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
+  constexpr int BUFR = Max2<Max2<FN1 * (FN2 + 1), IN1 * (IN2 + 1)>::v, Max2<N, N2>::v>::v;
+  extern __shared__ double2 sm[];
+  double2 *tw1 = sm, *tw2 = sm + N, *buf = sm + N + N2;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) tw1[j] = twN[j];
+  for (int j = threadIdx.x; j < N2; j += blockDim.x) tw2[j] = twN2[j];
+  const int v = threadIdx.x & (RS2_CW - 1), g = threadIdx.x >> 3;  // column in strip, group lane
+  const int nstrip = (ncols + RS2_CW - 1) / RS2_CW;
+  constexpr int K = ((N < N2 ? N : N2) - 1) / 2;
+  constexpr double sc = 1.0 / (double)N;
+  const int64_t nunit = nitem * nstrip;
+  for (int64_t u = blockIdx.x; u < nunit; u += gridDim.x) {
+    const int64_t item = u / nstrip;
+    const int m = (int)(u - item * nstrip) * RS2_CW + v;
+    const bool mok = m < ncols;
+    int64_t c0 = item, c1 = item + 1;
+    if (UP && cbeg) c0 = cbeg[item], c1 = cbeg[item + 1];
+    for (int64_t c = c0; c < c1; ++c) {
+      double2 x[16];
+      __syncthreads();  // twiddles staged / previous use of buf done
+      if (g < FN2) {     // forward nth, stage 1: x[n1] = column element FN2 n1 + g
+        const double2 *sb = nullptr;
+        const double2 *cb;
+        if (UP) {
+          cb = in + (c - cbase) * (int64_t)(N / 2 + 1) * rowlen;
+        } else {
+          cb = in + (int64_t)(par ? par[c] : c) * N * ncols;
+          if (shift) sb = shift + (int64_t)(oct ? oct[c] : 0) * N * ncols;
+        }
+        // all loads of the column first (no branch between them: one DRAM latency per column)
+#pragma unroll
+        for (int n1 = 0; n1 < FN1; ++n1) {
+          const int n = FN2 * n1 + g;
+          const int64_t o = UP ? ((2 * n <= N) ? (int64_t)n * rowlen + m : (int64_t)(N - n) * rowlen + m + ncols)
+                               : (int64_t)n * ncols + m;
+          x[n1] = mok ? cb[o] : make_double2(0.0, 0.0);
+        }
+        if (!UP && sb && mok) {
+          double2 t[FN1];
+#pragma unroll
+          for (int n1 = 0; n1 < FN1; ++n1) t[n1] = __ldg(&sb[(int64_t)(FN2 * n1 + g) * ncols + m]);
+#pragma unroll
+          for (int n1 = 0; n1 < FN1; ++n1) x[n1] = c_mul(x[n1], c_conj(t[n1]));
+        }
+        dft<FN1>(x);
+#pragma unroll
+        for (int k1 = 1; k1 < FN1; ++k1) x[k1] = c_mul(x[k1], tw1[g * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < FN1; ++k1) buf[(k1 * (FN2 + 1) + g) * RS2_CWP + v] = x[k1];
+      }
+      __syncthreads();
+      if (g < FN1) {
+#pragma unroll
+        for (int n2 = 0; n2 < FN2; ++n2) x[n2] = buf[(g * (FN2 + 1) + n2) * RS2_CWP + v];
+      }
+      __syncthreads();
+      if (g < FN1) {
+        dft<FN2>(x);
+#pragma unroll
+        for (int k2 = 0; k2 < FN2; ++k2) buf[(g + FN1 * k2) * RS2_CWP + v] = x[k2];
+      }
+      __syncthreads();
+      if (g < IN2) {  // padded / truncated conj spectrum: Z[IN2 m1 + g]
+#pragma unroll
+        for (int m1 = 0; m1 < IN1; ++m1) {
+          const int i = IN2 * m1 + g;
+          const int f = (i <= N2 / 2) ? i : i - N2;
+          double2 z = make_double2(0.0, 0.0);
+          if (f <= K && f >= -K) {
+            const double2 y = buf[(f >= 0 ? f : f + N) * RS2_CWP + v];
+            z = make_double2(y.x * sc, -y.y * sc);
+          }
+          x[m1] = z;
+        }
+      }
+      __syncthreads();
+      if (g < IN2) {
+        dft<IN1>(x);
+#pragma unroll
+        for (int k1 = 1; k1 < IN1; ++k1) x[k1] = c_mul(x[k1], tw2[g * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < IN1; ++k1) buf[(k1 * (IN2 + 1) + g) * RS2_CWP + v] = x[k1];
+      }
+      __syncthreads();
+      if (g < IN1) {
+#pragma unroll
+        for (int n2 = 0; n2 < IN2; ++n2) x[n2] = buf[(g * (IN2 + 1) + n2) * RS2_CWP + v];
+        dft<IN2>(x);
+        if (UP) {
+          if (mok) {  // shift and sum over the children (same thread owns the outputs for every child)
+            double2 *ob = out + item * (int64_t)N2 * ncols + m;
+#pragma unroll
+            for (int k2 = 0; k2 < IN2; ++k2) x[k2] = c_conj(x[k2]);
+            if (shift) {
+              const double2 *sb = shift + (int64_t)(oct ? oct[c] : 0) * N2 * ncols + m;
+              double2 t[IN2];
+#pragma unroll
+              for (int k2 = 0; k2 < IN2; ++k2) t[k2] = __ldg(&sb[(int64_t)(g + IN1 * k2) * ncols]);
+#pragma unroll
+              for (int k2 = 0; k2 < IN2; ++k2) x[k2] = c_mul(x[k2], t[k2]);
+            }
+            if (c != c0) {
+              double2 t[IN2];
+#pragma unroll
+              for (int k2 = 0; k2 < IN2; ++k2) t[k2] = ob[(int64_t)(g + IN1 * k2) * ncols];
+#pragma unroll
+              for (int k2 = 0; k2 < IN2; ++k2) x[k2] = c_add(x[k2], t[k2]);
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < IN2; ++k2) ob[(int64_t)(g + IN1 * k2) * ncols] = x[k2];
+          }
+        } else if (mok) {
+          double2 *ob = out + c * (int64_t)N2 * ncols + m;
+#pragma unroll
+          for (int k2 = 0; k2 < IN2; ++k2) ob[(int64_t)(g + IN1 * k2) * ncols] = c_conj(x[k2]);
+        }
+      }
+    }
+  }
+}
+
+template <bool UP, int FN1, int FN2, int IN1, int IN2>
+static void launch_cols2_t(const double2 *in, int64_t nitem, int ncols, int rowlen, const int32_t *cbeg,
+                           int64_t cbase, const int32_t *par, const int8_t *oct, const double2 *shift, double2 *out,
+                           const TwiddleSet &tw, cudaStream_t s) {
+  constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
+  constexpr int BUFR = Max2<Max2<FN1 * (FN2 + 1), IN1 * (IN2 + 1)>::v, Max2<N, N2>::v>::v;
+  const size_t smem = ((size_t)N + N2 + (size_t)BUFR * RS2_CWP) * sizeof(double2);
+  auto kern = cols2_kernel<UP, FN1, FN2, IN1, IN2>;
+  cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, nsm = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
+  const int64_t nunit = nitem * ((ncols + RS2_CW - 1) / RS2_CW);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nunit, (int64_t)nsm * std::max(per, 1)));
+  kern<<<grid, 128, smem, s>>>(in, nitem, ncols, rowlen, cbeg, cbase, par, oct, shift, tw.d + tw.offset[N],
+                               tw.d + tw.offset[N2], out);
+}
+
+static int rs2_enabled() {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char *e = getenv("HFMM_RS2");   // 0: tiled passes only (A/B)
+    enabled = e ? atoi(e) : 1;
+  }
+  return enabled;
+}
+
+// (nth, nth2) pairs with a register-resident columns pass; false: use the tiled kernel
+template <bool UP>
+static bool launch_cols2(const double2 *in, int64_t nitem, int nth, int ncols, int rowlen, int nth2,
+                         const int32_t *cbeg, int64_t cbase, const int32_t *par, const int8_t *oct,
+                         const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
+  if (!rs2_enabled() || std::max(nth, nth2) < (UP ? 128 : 64)) return false;
+  switch (nth * 1000 + nth2) {
+#define RS2C(a, b, F1, F2, I1, I2) \
+  case a * 1000 + b: launch_cols2_t<UP, F1, F2, I1, I2>(in, nitem, ncols, rowlen, cbeg, cbase, par, oct, shift, out, tw, s); return true;
+    RS2C(16, 32, 4, 4, 8, 4)
+    RS2C(32, 64, 8, 4, 8, 8)
+    RS2C(64, 128, 8, 8, 16, 8)
+    RS2C(128, 256, 16, 8, 16, 16)
+    RS2C(32, 16, 8, 4, 4, 4)
+    RS2C(64, 32, 8, 8, 8, 4)
+    RS2C(128, 64, 16, 8, 8, 8)
+    RS2C(256, 128, 16, 16, 16, 8)
+#undef RS2C
+    default: return false;
+  }
+}
+
+template <bool UP, int FN1, int FN2, int IN1, int IN2>
+static void launch_rows2_t(const double2 *in, int64_t nbox, int nth, const double2 *add, double2 *out,
+                           const TwiddleSet &tw, cudaStream_t s) {
+  constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
+  constexpr int G = std::max(std::max(FN1, FN2), std::max(IN1, IN2));
+  constexpr int BUFW = std::max(std::max(FN1 * (FN2 + 1), IN1 * (IN2 + 1)), std::max(N, N2));
+  constexpr int VW = 32 / G, warps = 4;
+  const size_t smem = ((size_t)N + N2 + (size_t)warps * VW * BUFW) * sizeof(double2);
+  auto kern = rows2_kernel<UP, FN1, FN2, IN1, IN2>;
+  cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, nsm = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * warps, smem);
+  const int64_t total = nbox * (nth / 2 + 1);
+  const int64_t need = (total + (int64_t)warps * VW - 1) / ((int64_t)warps * VW);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)nsm * std::max(per, 1)));
+  kern<<<grid, 32 * warps, smem, s>>>(in, nbox, nth, tw.d + tw.offset[N], tw.d + tw.offset[N2], add, out);
+}
+
+// Per-size plan of the register-resident passes (same-box A/Bs, profiles/r01/rs2_ab*.txt): rows
+// passes and downward column passes from 64-point grids up, upward column passes from 128.
+template <bool UP>
+static bool launch_rows2(const double2 *in, int64_t nbox, int nth, int nph, int nph2, const double2 *add,
+                         double2 *out, const TwiddleSet &tw, cudaStream_t s) {
+  if (!rs2_enabled() || std::max(nph, nph2) < 64) return false;
+  switch (nph * 1000 + nph2) {
+#define RS2R(a, b, F1, F2, I1, I2) \
+  case a * 1000 + b: launch_rows2_t<UP, F1, F2, I1, I2>(in, nbox, nth, add, out, tw, s); return true;
+    RS2R(32, 64, 8, 4, 8, 8)
+    RS2R(64, 128, 8, 8, 16, 8)
+    RS2R(128, 256, 16, 8, 16, 16)
+    RS2R(64, 32, 8, 8, 8, 4)
+    RS2R(128, 64, 16, 8, 8, 8)
+    RS2R(256, 128, 16, 16, 16, 8)
+#undef RS2R
+    default: return false;
+  }
+}
+
 // Tile plan per size (A/B on the C2 sizes): grids of <= 128 points use radix <= 8 butterflies
 // (~75 registers) in 48 KB tiles; larger grids radix-16 butterflies (~140 registers) in 72 KB tiles.
 struct TilePlan {
@@ -639,23 +983,28 @@ static void launch_cols(const double2 *in, int64_t nitem, int nth, int ncols, in
 
 void launch_rows_up(const double2 *in, int64_t nbox, int nth, int nph, int nph2, double2 *tmp,
                     const TwiddleSet &tw, cudaStream_t s) {
+  if (launch_rows2<true>(in, nbox, nth, nph, nph2, nullptr, tmp, tw, s)) return;
   launch_rows<true>(in, nbox, nth, nph, nph2, nullptr, tmp, tw, s);
 }
 
 void launch_cols_up(const double2 *tmp, int nth, int nph2, int nth2, const int32_t *cbeg,
                     int64_t cbase, const int8_t *oct, int64_t nparent, const double2 *shift, double2 *out,
                     const TwiddleSet &tw, cudaStream_t s) {
+  if (launch_cols2<true>(tmp, nparent, nth, nph2 / 2, nph2, nth2, cbeg, cbase, nullptr, oct, shift, out, tw, s))
+    return;
   launch_cols<true>(tmp, nparent, nth, nph2 / 2, nph2, nth2, cbeg, cbase, nullptr, oct, shift, out, tw, s);
 }
 
 void launch_cols_down(const double2 *in, int nth, int nph, int nth2, const int32_t *par,
                       const int8_t *oct, int64_t nchild, const double2 *shift, double2 *tmp,
                       const TwiddleSet &tw, cudaStream_t s) {
+  if (launch_cols2<false>(in, nchild, nth, nph / 2, nph / 2, nth2, nullptr, 0, par, oct, shift, tmp, tw, s)) return;
   launch_cols<false>(in, nchild, nth, nph / 2, nph / 2, nth2, nullptr, 0, par, oct, shift, tmp, tw, s);
 }
 
 void launch_rows_down(const double2 *tmp, int64_t nbox, int nth2, int nph, int nph2,
                       const double2 *add, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
+  if (launch_rows2<false>(tmp, nbox, nth2, nph, nph2, add, out, tw, s)) return;
   launch_rows<false>(tmp, nbox, nth2, nph, nph2, add, out, tw, s);
 }
 
