@@ -235,6 +235,74 @@ __device__ __forceinline__ void dft<16>(double2 *v) {
   for (int t = 0; t < 16; ++t) v[t] = o[t];
 }
 
+// ---- composite small DFTs N = P Q in registers (Cooley-Tukey, twiddles folded at compile time) ---
+constexpr double kPiC = 3.14159265358979323846264338327950288;
+__host__ __device__ constexpr double ct_sin(double x) {
+  double t = x, s = x;
+  for (int i = 1; i < 16; ++i) t *= -x * x / ((2.0 * i) * (2.0 * i + 1)), s += t;
+  return s;
+}
+__host__ __device__ constexpr double ct_cos(double x) {
+  double t = 1, s = 1;
+  for (int i = 1; i < 16; ++i) t *= -x * x / ((2.0 * i - 1) * (2.0 * i)), s += t;
+  return s;
+}
+// cos / sin of 2 pi K / N (argument reduced to [0, pi/2]; constant-folded when K, N are)
+__host__ __device__ constexpr double cx_cos(int K, int N) {
+  K %= N;
+  double a = 2 * kPiC * K / N;
+  if (a > kPiC) a -= 2 * kPiC;
+  const double b = a < 0 ? -a : a;
+  return b <= kPiC / 2 ? ct_cos(b) : -ct_cos(kPiC - b);
+}
+__host__ __device__ constexpr double cx_sin(int K, int N) {
+  K %= N;
+  double a = 2 * kPiC * K / N;
+  if (a > kPiC) a -= 2 * kPiC;
+  const double b = a < 0 ? -a : a;
+  const double sb = b <= kPiC / 2 ? ct_sin(b) : ct_sin(kPiC - b);
+  return a < 0 ? -sb : sb;
+}
+template <int P, int Q>
+__device__ __forceinline__ void dft_pq(double2 *v) {  // X[k1 + P k2], n = Q n1 + n2
+  constexpr int N = P * Q;
+  double2 t[N];
+#pragma unroll
+  for (int n2 = 0; n2 < Q; ++n2) {
+    double2 a[P];
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) a[n1] = v[Q * n1 + n2];
+    dft<P>(a);
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1)
+      t[n2 * P + k1] = (n2 * k1 == 0) ? a[k1]
+                                      : c_mul(a[k1], make_double2(cx_cos(n2 * k1, N), -cx_sin(n2 * k1, N)));
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < P; ++k1) {
+    double2 b[Q];
+#pragma unroll
+    for (int n2 = 0; n2 < Q; ++n2) b[n2] = t[n2 * P + k1];
+    dft<Q>(b);
+#pragma unroll
+    for (int k2 = 0; k2 < Q; ++k2) v[k1 + P * k2] = b[k2];
+  }
+}
+template <>
+__device__ __forceinline__ void dft<1>(double2 *) {}
+template <>
+__device__ __forceinline__ void dft<6>(double2 *v) { dft_pq<3, 2>(v); }
+template <>
+__device__ __forceinline__ void dft<9>(double2 *v) { dft_pq<3, 3>(v); }
+template <>
+__device__ __forceinline__ void dft<10>(double2 *v) { dft_pq<5, 2>(v); }
+template <>
+__device__ __forceinline__ void dft<12>(double2 *v) { dft_pq<4, 3>(v); }
+template <>
+__device__ __forceinline__ void dft<14>(double2 *v) { dft_pq<7, 2>(v); }
+template <>
+__device__ __forceinline__ void dft<15>(double2 *v) { dft_pq<5, 3>(v); }
+
 // ---- integer division by a runtime divisor without the ~25-instruction IDIV sequence: float
 //      reciprocal estimate + one correction (exact for 0 <= x < 2^22) -------------------------------
 struct FDiv {
@@ -555,8 +623,8 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
   }
 }
 
-// ---- register-resident two-level rows pass (upward) -------------------------------------------
-// A 1-D resample N -> N' with N = N1 N2 and N' = M1 M2 (factors in {1, 2, 4, 8, 16}) by one group of
+// ---- register-resident two-level resample passes ----------------------------------------------
+// A 1-D resample N -> N' with N = N1 N2 and N' = M1 M2 (factors: register DFT sizes) by one group of
 // G lanes (G = the largest factor) inside a warp, data in registers between the passes:
 //   forward N:  lane n2 < N2 holds x[N2 n1 + n2] (n1 < N1): DFT_N1, twiddle w_N^{n2 k1}; exchange;
 //               lane k1 < N1 holds the N2 values: DFT_N2 -> X[k1 + N1 k2];
@@ -570,7 +638,8 @@ __global__ void __launch_bounds__(128, 3) rows2_kernel(const double2 *__restrict
                                                       const double2 *__restrict__ twN2,
                                                       const double2 *__restrict__ add, double2 *__restrict__ out) {
   constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
-  constexpr int G = (FN1 > IN1 ? FN1 : IN1) > (FN2 > IN2 ? FN2 : IN2) ? (FN1 > IN1 ? FN1 : IN1) : (FN2 > IN2 ? FN2 : IN2);
+  constexpr int GM = (FN1 > IN1 ? FN1 : IN1) > (FN2 > IN2 ? FN2 : IN2) ? (FN1 > IN1 ? FN1 : IN1) : (FN2 > IN2 ? FN2 : IN2);
+  constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;  // lanes per group (divides 32)
   constexpr int BF = FN1 * (FN2 + 1), BI = IN1 * (IN2 + 1);
   constexpr int BUFW = (BF > BI ? BF : BI) > (N > N2 ? N : N2) ? (BF > BI ? BF : BI) : (N > N2 ? N : N2);
   constexpr int VW = 32 / G;
@@ -853,6 +922,14 @@ static bool launch_cols2(const double2 *in, int64_t nitem, int nth, int ncols, i
     RS2C(64, 32, 8, 8, 8, 4)
     RS2C(128, 64, 16, 8, 8, 8)
     RS2C(256, 128, 16, 16, 16, 8)
+    // 7-smooth grids of the BASELINE matvec configs (C3: 54 <-> 120, C4: 60 <-> 140 <-> 240,
+    // C5: 54 <-> 120; factors from the register DFTs incl. the composite 6, 9, 10, 12, 14, 15)
+    RS2C(54, 120, 9, 6, 12, 10)
+    RS2C(120, 54, 12, 10, 9, 6)
+    RS2C(60, 140, 10, 6, 14, 10)
+    RS2C(140, 60, 14, 10, 10, 6)
+    RS2C(140, 240, 14, 10, 16, 15)
+    RS2C(240, 140, 16, 15, 14, 10)
 #undef RS2C
     default: return false;
   }
@@ -862,7 +939,8 @@ template <bool UP, int FN1, int FN2, int IN1, int IN2>
 static void launch_rows2_t(const double2 *in, int64_t nbox, int nth, const double2 *add, double2 *out,
                            const TwiddleSet &tw, cudaStream_t s) {
   constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
-  constexpr int G = std::max(std::max(FN1, FN2), std::max(IN1, IN2));
+  constexpr int GM = std::max(std::max(FN1, FN2), std::max(IN1, IN2));
+  constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;
   constexpr int BUFW = std::max(std::max(FN1 * (FN2 + 1), IN1 * (IN2 + 1)), std::max(N, N2));
   constexpr int VW = 32 / G, warps = 4;
   const size_t smem = ((size_t)N + N2 + (size_t)warps * VW * BUFW) * sizeof(double2);
@@ -893,6 +971,12 @@ static bool launch_rows2(const double2 *in, int64_t nbox, int nth, int nph, int 
     RS2R(64, 32, 8, 8, 8, 4)
     RS2R(128, 64, 16, 8, 8, 8)
     RS2R(256, 128, 16, 16, 16, 8)
+    RS2R(56, 120, 8, 7, 12, 10)
+    RS2R(120, 56, 12, 10, 8, 7)
+    RS2R(60, 140, 10, 6, 14, 10)
+    RS2R(140, 60, 14, 10, 10, 6)
+    RS2R(140, 240, 14, 10, 16, 15)
+    RS2R(240, 140, 16, 15, 14, 10)
 #undef RS2R
     default: return false;
   }
