@@ -767,33 +767,62 @@ __global__ void __launch_bounds__(128, 3) cols2_kernel(const double2 *__restrict
   constexpr int K = ((N < N2 ? N : N2) - 1) / 2;
   constexpr double sc = 1.0 / (double)N;
   const int64_t nunit = nitem * nstrip;
-  for (int64_t u = blockIdx.x; u < nunit; u += gridDim.x) {
+  // Steps (unit u, child c) in CTA order.  Upward: the input strip of the next step is fetched into
+  // `stg` with cp.async while the current one is transformed (hides the global-memory latency;
+  // same-box A/B: C2 B64 interp 20.1 -> 17.6 ms).  Downward the extra 37 KB cost a CTA per SM
+  // (B64 anterp 16.8 -> 19.0 ms), so it loads straight into registers.
+  constexpr bool PF = UP;
+  double2 *stg = buf + BUFR * RS2_CWP;  // [N][CWP] (PF only)
+  auto crange = [&](int64_t uu, int64_t &a0, int64_t &a1) {
+    const int64_t it = uu / nstrip;
+    a0 = it, a1 = it + 1;
+    if (UP && cbeg) a0 = cbeg[it], a1 = cbeg[it + 1];
+  };
+  auto issue = [&](int64_t uu, int64_t cc) {
+    const int64_t it = uu / nstrip;
+    const int mb = (int)(uu - it * nstrip) * RS2_CW;
+    const double2 *cb = UP ? in + (cc - cbase) * (int64_t)(N / 2 + 1) * rowlen
+                           : in + (int64_t)(par ? par[cc] : cc) * N * ncols;
+    for (int e = threadIdx.x; e < N * RS2_CW; e += blockDim.x) {
+      const int n = e >> 3, vv = e & (RS2_CW - 1), mm = mb + vv;
+      if (mm >= ncols) continue;
+      const double2 *src = UP ? ((2 * n <= N) ? &cb[(int64_t)n * rowlen + mm] : &cb[(int64_t)(N - n) * rowlen + mm + ncols])
+                              : &cb[(int64_t)n * ncols + mm];
+      cp_async16(&stg[n * RS2_CWP + vv], src);
+    }
+  };
+  int64_t u = blockIdx.x;
+  if (u >= nunit) return;
+  int64_t c0, c1;
+  crange(u, c0, c1);
+  int64_t c = c0;
+  if (PF) issue(u, c);
+  for (;;) {
     const int64_t item = u / nstrip;
     const int m = (int)(u - item * nstrip) * RS2_CW + v;
     const bool mok = m < ncols;
-    int64_t c0 = item, c1 = item + 1;
-    if (UP && cbeg) c0 = cbeg[item], c1 = cbeg[item + 1];
-    for (int64_t c = c0; c < c1; ++c) {
+    int64_t nu = u, nc = c + 1, n0 = c0, n1_ = c1;  // next step
+    {
       double2 x[16];
-      __syncthreads();  // twiddles staged / previous use of buf done
+      if (PF) cp_async_wait_all();
+      __syncthreads();  // stg holds step (u, c); previous use of buf done; twiddles staged
       if (g < FN2) {     // forward nth, stage 1: x[n1] = column element FN2 n1 + g
-        const double2 *sb = nullptr;
-        const double2 *cb;
-        if (UP) {
-          cb = in + (c - cbase) * (int64_t)(N / 2 + 1) * rowlen;
-        } else {
-          cb = in + (int64_t)(par ? par[c] : c) * N * ncols;
-          if (shift) sb = shift + (int64_t)(oct ? oct[c] : 0) * N * ncols;
-        }
-        // all loads of the column first (no branch between them: one DRAM latency per column)
+        if (PF) {
 #pragma unroll
-        for (int n1 = 0; n1 < FN1; ++n1) {
-          const int n = FN2 * n1 + g;
-          const int64_t o = UP ? ((2 * n <= N) ? (int64_t)n * rowlen + m : (int64_t)(N - n) * rowlen + m + ncols)
-                               : (int64_t)n * ncols + m;
-          x[n1] = mok ? cb[o] : make_double2(0.0, 0.0);
+          for (int n1 = 0; n1 < FN1; ++n1) x[n1] = mok ? stg[(FN2 * n1 + g) * RS2_CWP + v] : make_double2(0.0, 0.0);
+        } else {  // all loads of the column first (no branch between them: one latency per column)
+          const double2 *cb = UP ? in + (c - cbase) * (int64_t)(N / 2 + 1) * rowlen
+                                 : in + (int64_t)(par ? par[c] : c) * N * ncols;
+#pragma unroll
+          for (int n1 = 0; n1 < FN1; ++n1) {
+            const int n = FN2 * n1 + g;
+            const int64_t o = UP ? ((2 * n <= N) ? (int64_t)n * rowlen + m : (int64_t)(N - n) * rowlen + m + ncols)
+                                 : (int64_t)n * ncols + m;
+            x[n1] = mok ? cb[o] : make_double2(0.0, 0.0);
+          }
         }
-        if (!UP && sb && mok) {
+        if (!UP && shift && mok) {
+          const double2 *sb = shift + (int64_t)(oct ? oct[c] : 0) * N * ncols;
           double2 t[FN1];
 #pragma unroll
           for (int n1 = 0; n1 < FN1; ++n1) t[n1] = __ldg(&sb[(int64_t)(FN2 * n1 + g) * ncols + m]);
@@ -806,7 +835,12 @@ __global__ void __launch_bounds__(128, 3) cols2_kernel(const double2 *__restrict
 #pragma unroll
         for (int k1 = 0; k1 < FN1; ++k1) buf[(k1 * (FN2 + 1) + g) * RS2_CWP + v] = x[k1];
       }
-      __syncthreads();
+      __syncthreads();  // stg consumed: fetch the next step's strip
+      if (nc >= c1) {
+        nu = u + gridDim.x;
+        if (nu < nunit) crange(nu, n0, n1_), nc = n0;
+      }
+      if (PF && nu < nunit) issue(nu, nc);
       if (g < FN1) {
 #pragma unroll
         for (int n2 = 0; n2 < FN2; ++n2) x[n2] = buf[(g * (FN2 + 1) + n2) * RS2_CWP + v];
@@ -874,6 +908,8 @@ __global__ void __launch_bounds__(128, 3) cols2_kernel(const double2 *__restrict
         }
       }
     }
+    if (nu >= nunit) break;
+    u = nu, c = nc, c0 = n0, c1 = n1_;
   }
 }
 
@@ -883,7 +919,7 @@ static void launch_cols2_t(const double2 *in, int64_t nitem, int ncols, int rowl
                            const TwiddleSet &tw, cudaStream_t s) {
   constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
   constexpr int BUFR = Max2<Max2<FN1 * (FN2 + 1), IN1 * (IN2 + 1)>::v, Max2<N, N2>::v>::v;
-  const size_t smem = ((size_t)N + N2 + (size_t)BUFR * RS2_CWP) * sizeof(double2);
+  const size_t smem = ((size_t)N + N2 + (size_t)(BUFR + (UP ? N : 0)) * RS2_CWP) * sizeof(double2);
   auto kern = cols2_kernel<UP, FN1, FN2, IN1, IN2>;
   cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 148, per = 0;
