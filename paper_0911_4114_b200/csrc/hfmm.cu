@@ -837,7 +837,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     int nl = 2;
     for (int k = 0; k < 3; ++k) nl += p->p2p_nitems[k] > 0 ? 1 : 0;
     if (p->L_f >= 2) {
-      for (int l = p->D_s; l > 2; --l) nl += 2;   // M2M: rows + cols pass per level
+      for (int l = p->D_s; l > 2; --l) {          // M2M: rows + cols pass per level (or one pass)
+        const LevelDev &C = p->lv[l], &P = p->lv[l - 1];
+        nl += (!C.ragged && !P.ragged && box2_up_applies(C.nth, C.nph, P.nth, P.nph)) ? 1 : 2;
+      }
       for (int l = 2; l < p->D_s; ++l) nl += 2;   // L2L: cols + rows pass per level
       nl += 2 + (p->L_f - 1);                      // S2M, L2T, M2L per active level
     }
@@ -914,6 +917,10 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, b
                           tw, s);
           src = p->scr1;
         }
+        if (!C.ragged && !P.ragged &&
+            launch_box2_up(src, P.own1 - P.own0, C.nth, C.nph, P.nth, P.nph, P.cbeg + P.own0, C.own0, C.oct, P.shift,
+                           P.M + P.own0 * P.K, tw, s))
+          continue;  // single pass (small square grids)
         launch_rows_up(src, nc, C.nth, C.nph, P.nph, p->tmp, tw, s);
         if (P.ragged) {  // per-child parent fields, then step 5 + shift + sum on the ragged parent grid
           launch_cols_up(p->tmp, C.nth, P.nph, P.nth, nullptr, 0, nullptr, nc, nullptr, p->scr2, tw, s);
@@ -1215,8 +1222,11 @@ extern "C" int hfmm_resample(int nbatch, int nth, int nph, int nth2, int nph2, c
     own = true;
   }
   if (up) {
-    launch_rows_up((const double2 *)in, nbatch, nth, nph, nph2, tmp, tw, s);
-    launch_cols_up(tmp, nth, nph2, nth2, nullptr, 0, nullptr, nbatch, nullptr, (double2 *)out, tw, s);
+    if (!launch_box2_up((const double2 *)in, nbatch, nth, nph, nth2, nph2, nullptr, 0, nullptr, nullptr,
+                        (double2 *)out, tw, s)) {
+      launch_rows_up((const double2 *)in, nbatch, nth, nph, nph2, tmp, tw, s);
+      launch_cols_up(tmp, nth, nph2, nth2, nullptr, 0, nullptr, nbatch, nullptr, (double2 *)out, tw, s);
+    }
   } else {
     launch_cols_down((const double2 *)in, nth, nph, nth2, nullptr, nullptr, nbatch, nullptr, tmp, tw, s);
     launch_rows_down(tmp, nbatch, nth2, nph, nph2, nullptr, (double2 *)out, tw, s);
@@ -1242,8 +1252,11 @@ extern "C" int hfmm_m2m_op(int nparent, int nth, int nph, int nth2, int nph2, co
     if (cudaMalloc(&tmp, hfmm_resample_workspace(nparent * 8, nth, nph, nth2, nph2)) != cudaSuccess) return HFMM_E_NOMEM;
     own = true;
   }
-  launch_rows_up((const double2 *)child, (int64_t)nparent * 8, nth, nph, nph2, tmp, tw, s);
-  launch_cols_up(tmp, nth, nph2, nth2, c.cbeg, 0, c.oct, nparent, (const double2 *)shift, (double2 *)parent, tw, s);
+  if (!launch_box2_up((const double2 *)child, nparent, nth, nph, nth2, nph2, c.cbeg, 0, c.oct, (const double2 *)shift,
+                      (double2 *)parent, tw, s)) {
+    launch_rows_up((const double2 *)child, (int64_t)nparent * 8, nth, nph, nph2, tmp, tw, s);
+    launch_cols_up(tmp, nth, nph2, nth2, c.cbeg, 0, c.oct, nparent, (const double2 *)shift, (double2 *)parent, tw, s);
+  }
   if (own) {
     cudaStreamSynchronize(s);
     cudaFree(tmp);

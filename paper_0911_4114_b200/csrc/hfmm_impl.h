@@ -173,6 +173,13 @@ int m2l_group_plan_kind(const M2LGroupPlan *pl);  // 1 parent-block, 0 merged-li
 void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *perm, const double2 *M, double2 *I,
                      cudaStream_t s);
 
+// Single-pass upward resample (rows + columns of each child on chip) for the small square grids
+// it is instantiated for: out[item] = sum_{c in [cbeg[item], cbeg[item+1])} shift[oct[c]] * R(in[c - cbase])
+// (cbeg == nullptr: one box per item, no shift).  Returns false when not applicable.
+bool box2_up_applies(int nth, int nph, int nth2, int nph2);
+bool launch_box2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *cbeg,
+                    int64_t cbase, const int8_t *oct, const double2 *shift, double2 *out, const TwiddleSet &tw,
+                    cudaStream_t s);
 // Fourier resampling building blocks, warp-per-sequence shared-memory FFTs.
 // Row pass of an upward resample: for each box b and row n <= nth/2, full row of length nph
 // (stored rows n and (nth-n)%nth) resampled to nph2 -> tmp[b][n][0..nph2).
