@@ -841,7 +841,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
         const LevelDev &C = p->lv[l], &P = p->lv[l - 1];
         nl += (!C.ragged && !P.ragged && box2_up_applies(C.nth, C.nph, P.nth, P.nph)) ? 1 : 2;
       }
-      for (int l = 2; l < p->D_s; ++l) nl += 2;   // L2L: cols + rows pass per level
+      for (int l = 2; l < p->D_s; ++l) {          // L2L: cols + rows pass per level (or one pass)
+        const LevelDev &P = p->lv[l], &C = p->lv[l + 1];
+        nl += (!C.ragged && !P.ragged && box2_down_applies(P.nth, P.nph, C.nth, C.nph)) ? 1 : 2;
+      }
       nl += 2 + (p->L_f - 1);                      // S2M, L2T, M2L per active level
     }
     in.launches = nl;
@@ -948,6 +951,10 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, b
       const double2 *Lp = (l == 2) ? P.I : P.L;
       if (C.own1 > C.own0) {
         const int64_t nc = C.own1 - C.own0;
+        if (!P.ragged && !C.ragged &&
+            launch_box2_down(Lp, nc, P.nth, P.nph, C.nth, C.nph, C.parent + C.own0, C.oct + C.own0, P.shift,
+                             C.I ? C.I + C.own0 * C.K : nullptr, C.L + C.own0 * C.K, tw, s))
+          continue;  // single pass (small square grids)
         if (P.ragged) {  // conj shift on the ragged parent grid + step 1 -> rectangular, per child
           launch_rag2rect(Lp, P.K, P.nth, P.rows_d, P.off_d, P.nph, C.parent + C.own0, C.oct + C.own0, P.shift, nc,
                           P.nph, p->scr2, tw, s);
@@ -1227,7 +1234,8 @@ extern "C" int hfmm_resample(int nbatch, int nth, int nph, int nth2, int nph2, c
       launch_rows_up((const double2 *)in, nbatch, nth, nph, nph2, tmp, tw, s);
       launch_cols_up(tmp, nth, nph2, nth2, nullptr, 0, nullptr, nbatch, nullptr, (double2 *)out, tw, s);
     }
-  } else {
+  } else if (!launch_box2_down((const double2 *)in, nbatch, nth, nph, nth2, nph2, nullptr, nullptr, nullptr, nullptr,
+                               (double2 *)out, tw, s)) {
     launch_cols_down((const double2 *)in, nth, nph, nth2, nullptr, nullptr, nbatch, nullptr, tmp, tw, s);
     launch_rows_down(tmp, nbatch, nth2, nph, nph2, nullptr, (double2 *)out, tw, s);
   }
@@ -1279,9 +1287,12 @@ extern "C" int hfmm_l2l_op(int nparent, int nth, int nph, int nth2, int nph2, co
     if (cudaMalloc(&tmp, hfmm_resample_workspace(nparent * 8, nth, nph, nth2, nph2)) != cudaSuccess) return HFMM_E_NOMEM;
     own = true;
   }
-  launch_cols_down((const double2 *)parent, nth, nph, nth2, c.par, c.oct, (int64_t)nparent * 8,
-                   (const double2 *)shift, tmp, tw, s);
-  launch_rows_down(tmp, (int64_t)nparent * 8, nth2, nph, nph2, (const double2 *)incoming, (double2 *)child_out, tw, s);
+  if (!launch_box2_down((const double2 *)parent, (int64_t)nparent * 8, nth, nph, nth2, nph2, c.par, c.oct,
+                        (const double2 *)shift, (const double2 *)incoming, (double2 *)child_out, tw, s)) {
+    launch_cols_down((const double2 *)parent, nth, nph, nth2, c.par, c.oct, (int64_t)nparent * 8,
+                     (const double2 *)shift, tmp, tw, s);
+    launch_rows_down(tmp, (int64_t)nparent * 8, nth2, nph, nph2, (const double2 *)incoming, (double2 *)child_out, tw, s);
+  }
   if (own) {
     cudaStreamSynchronize(s);
     cudaFree(tmp);

@@ -177,6 +177,10 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
 // it is instantiated for: out[item] = sum_{c in [cbeg[item], cbeg[item+1])} shift[oct[c]] * R(in[c - cbase])
 // (cbeg == nullptr: one box per item, no shift).  Returns false when not applicable.
 bool box2_up_applies(int nth, int nph, int nth2, int nph2);
+bool box2_down_applies(int nth, int nph, int nth2, int nph2);
+bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *par,
+                      const int8_t *oct, const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
+                      cudaStream_t s);
 bool launch_box2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *cbeg,
                     int64_t cbase, const int8_t *oct, const double2 *shift, double2 *out, const TwiddleSet &tw,
                     cudaStream_t s);

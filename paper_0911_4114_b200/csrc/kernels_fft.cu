@@ -1203,6 +1203,201 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
   }
 }
 
+// Single-pass downward resample (anterpolation / L2L): per child c, the columns of
+// conj(shift[oct[c]]) * in[par[c]] (nth -> nth2, steps 1-3) into a shared [nth2][nph/2]
+// intermediate, then the rows n <= nth2/2 (steps 4-5, nph -> nph2) back to half storage (+ add).
+template <int RF1, int RF2, int RI1, int RI2, int CF1, int CF2, int CI1, int CI2>
+__global__ void __launch_bounds__(128) box2_down_kernel(const double2 *__restrict__ in, int64_t nitem,
+                                                       const int32_t *__restrict__ par,
+                                                       const int8_t *__restrict__ oct,
+                                                       const double2 *__restrict__ shift,
+                                                       const double2 *__restrict__ twR, const double2 *__restrict__ twR2,
+                                                       const double2 *__restrict__ twC, const double2 *__restrict__ twC2,
+                                                       const double2 *__restrict__ add, double2 *__restrict__ out) {
+  constexpr int NR = RF1 * RF2, NR2 = RI1 * RI2;   // nph -> nph2 (rows)
+  constexpr int NC = CF1 * CF2, NC2 = CI1 * CI2;   // nth -> nth2 (columns)
+  constexpr int h = NR / 2, h2 = NR2 / 2, nrow = NC2 / 2 + 1;
+  constexpr int GM = Max2<Max2<RF1, RF2>::v, Max2<RI1, RI2>::v>::v;
+  constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;
+  constexpr int VW = 32 / G;
+  constexpr int RBUF = Max2<Max2<RF1 * (RF2 + 1), RI1 * (RI2 + 1)>::v, Max2<NR, NR2>::v>::v;
+  constexpr int CBUF = Max2<Max2<CF1 * (CF2 + 1), CI1 * (CI2 + 1)>::v, Max2<NC, NC2>::v>::v;
+  constexpr int IP = h + 1;                        // intermediate [NC2][IP]
+  constexpr int KR = ((NR < NR2 ? NR : NR2) - 1) / 2, KC = ((NC < NC2 ? NC : NC2) - 1) / 2;
+  extern __shared__ double2 sm[];
+  double2 *tr1 = sm, *tr2 = tr1 + NR, *tc1 = tr2 + NR2, *tc2 = tc1 + NC;
+  double2 *inter = tc2 + NC2;
+  double2 *rbuf = inter + NC2 * IP;
+  double2 *cbuf = rbuf + 4 * VW * RBUF;
+  for (int j = threadIdx.x; j < NR; j += blockDim.x) tr1[j] = twR[j];
+  for (int j = threadIdx.x; j < NR2; j += blockDim.x) tr2[j] = twR2[j];
+  for (int j = threadIdx.x; j < NC; j += blockDim.x) tc1[j] = twC[j];
+  for (int j = threadIdx.x; j < NC2; j += blockDim.x) tc2[j] = twC2[j];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / G, gr = lane - grp * G;
+  double2 *rb = rbuf + (warp * VW + grp) * RBUF;
+  const int v = threadIdx.x & (RS2_CW - 1), g = threadIdx.x >> 3;
+  for (int64_t c = blockIdx.x; c < nitem; c += gridDim.x) {
+    double2 x[16];
+    const double2 *pb = in + (int64_t)(par ? par[c] : c) * NC * h;
+    const double2 *sbase = shift ? shift + (int64_t)(oct ? oct[c] : 0) * NC * h : nullptr;
+    // ---- columns m < h of the shifted parent: nth -> nth2 into inter[t][m] ----
+    for (int m0 = 0; m0 < h; m0 += RS2_CW) {
+      const int m = m0 + v;
+      const bool mok = m < h;
+      __syncthreads();
+      if (g < CF2) {
+#pragma unroll
+        for (int n1 = 0; n1 < CF1; ++n1) x[n1] = mok ? pb[(CF2 * n1 + g) * h + m] : make_double2(0.0, 0.0);
+        if (sbase && mok) {
+          double2 t[CF1];
+#pragma unroll
+          for (int n1 = 0; n1 < CF1; ++n1) t[n1] = __ldg(&sbase[(CF2 * n1 + g) * h + m]);
+#pragma unroll
+          for (int n1 = 0; n1 < CF1; ++n1) x[n1] = c_mul(x[n1], c_conj(t[n1]));
+        }
+        dft<CF1>(x);
+#pragma unroll
+        for (int k1 = 1; k1 < CF1; ++k1) x[k1] = c_mul(x[k1], tc1[g * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < CF1; ++k1) cbuf[(k1 * (CF2 + 1) + g) * RS2_CWP + v] = x[k1];
+      }
+      __syncthreads();
+      if (g < CF1) {
+#pragma unroll
+        for (int n2 = 0; n2 < CF2; ++n2) x[n2] = cbuf[(g * (CF2 + 1) + n2) * RS2_CWP + v];
+      }
+      __syncthreads();
+      if (g < CF1) {
+        dft<CF2>(x);
+#pragma unroll
+        for (int k2 = 0; k2 < CF2; ++k2) cbuf[(g + CF1 * k2) * RS2_CWP + v] = x[k2];
+      }
+      __syncthreads();
+      if (g < CI2) {
+#pragma unroll
+        for (int m1 = 0; m1 < CI1; ++m1) {
+          const int i = CI2 * m1 + g;
+          const int f = (i <= NC2 / 2) ? i : i - NC2;
+          double2 z = make_double2(0.0, 0.0);
+          if (f <= KC && f >= -KC) {
+            const double2 y = cbuf[(f >= 0 ? f : f + NC) * RS2_CWP + v];
+            z = make_double2(y.x * (1.0 / NC), -y.y * (1.0 / NC));
+          }
+          x[m1] = z;
+        }
+      }
+      __syncthreads();
+      if (g < CI2) {
+        dft<CI1>(x);
+#pragma unroll
+        for (int k1 = 1; k1 < CI1; ++k1) x[k1] = c_mul(x[k1], tc2[g * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < CI1; ++k1) cbuf[(k1 * (CI2 + 1) + g) * RS2_CWP + v] = x[k1];
+      }
+      __syncthreads();
+      if (g < CI1 && mok) {
+#pragma unroll
+        for (int n2 = 0; n2 < CI2; ++n2) x[n2] = cbuf[(g * (CI2 + 1) + n2) * RS2_CWP + v];
+        dft<CI2>(x);
+#pragma unroll
+        for (int k2 = 0; k2 < CI2; ++k2) inter[(g + CI1 * k2) * IP + m] = c_conj(x[k2]);
+      }
+    }
+    __syncthreads();
+    // ---- rows n <= nth2/2: nph -> nph2, back to half storage of child c (+ add) ----
+    for (int r0 = warp * VW; r0 < nrow; r0 += 4 * VW) {
+      const int n = r0 + grp;
+      const bool vok = n < nrow && grp < VW;
+      if (vok && gr < RF2) {
+        const double2 *lo = inter + n * IP, *hi = inter + (n == 0 ? 0 : NC2 - n) * IP;
+#pragma unroll
+        for (int n1 = 0; n1 < RF1; ++n1) {
+          const int e = RF2 * n1 + gr;
+          x[n1] = e < h ? lo[e] : hi[e - h];
+        }
+        dft<RF1>(x);
+#pragma unroll
+        for (int k1 = 1; k1 < RF1; ++k1) x[k1] = c_mul(x[k1], tr1[gr * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < RF1; ++k1) rb[k1 * (RF2 + 1) + gr] = x[k1];
+      }
+      __syncwarp();
+      if (vok && gr < RF1) {
+#pragma unroll
+        for (int n2 = 0; n2 < RF2; ++n2) x[n2] = rb[gr * (RF2 + 1) + n2];
+      }
+      __syncwarp();
+      if (vok && gr < RF1) {
+        dft<RF2>(x);
+#pragma unroll
+        for (int k2 = 0; k2 < RF2; ++k2) rb[gr + RF1 * k2] = x[k2];
+      }
+      __syncwarp();
+      if (vok && gr < RI2) {
+#pragma unroll
+        for (int m1 = 0; m1 < RI1; ++m1) {
+          const int i = RI2 * m1 + gr;
+          const int f = (i <= NR2 / 2) ? i : i - NR2;
+          double2 z = make_double2(0.0, 0.0);
+          if (f <= KR && f >= -KR) {
+            const double2 y = rb[f >= 0 ? f : f + NR];
+            z = make_double2(y.x * (1.0 / NR), -y.y * (1.0 / NR));
+          }
+          x[m1] = z;
+        }
+      }
+      __syncwarp();
+      if (vok && gr < RI2) {
+        dft<RI1>(x);
+#pragma unroll
+        for (int k1 = 1; k1 < RI1; ++k1) x[k1] = c_mul(x[k1], tr2[gr * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < RI1; ++k1) rb[k1 * (RI2 + 1) + gr] = x[k1];
+      }
+      __syncwarp();
+      if (vok && gr < RI1) {
+#pragma unroll
+        for (int n2 = 0; n2 < RI2; ++n2) x[n2] = rb[gr * (RI2 + 1) + n2];
+        dft<RI2>(x);
+        const bool mirror = !(n == 0 || 2 * n == NC2);
+#pragma unroll
+        for (int k2 = 0; k2 < RI2; ++k2) {
+          const int t = gr + RI1 * k2;
+          if (t >= h2 && !mirror) continue;  // both halves are the same points
+          const int64_t o = (c * NC2 + (t < h2 ? n : NC2 - n)) * h2 + (t < h2 ? t : t - h2);
+          double2 val = c_conj(x[k2]);
+          if (add) val = c_add(val, add[o]);
+          out[o] = val;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int RF1, int RF2, int RI1, int RI2, int CF1, int CF2, int CI1, int CI2>
+static void launch_box2d_t(const double2 *in, int64_t nitem, const int32_t *par, const int8_t *oct,
+                           const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
+                           cudaStream_t s) {
+  constexpr int NR = RF1 * RF2, NR2 = RI1 * RI2, NC = CF1 * CF2, NC2 = CI1 * CI2;
+  constexpr int GM = Max2<Max2<RF1, RF2>::v, Max2<RI1, RI2>::v>::v;
+  constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;
+  constexpr int RBUF = Max2<Max2<RF1 * (RF2 + 1), RI1 * (RI2 + 1)>::v, Max2<NR, NR2>::v>::v;
+  constexpr int CBUF = Max2<Max2<CF1 * (CF2 + 1), CI1 * (CI2 + 1)>::v, Max2<NC, NC2>::v>::v;
+  const size_t smem = ((size_t)NR + NR2 + NC + NC2 + (size_t)NC2 * (NR / 2 + 1) + 4 * (32 / G) * RBUF +
+                       (size_t)CBUF * RS2_CWP) * sizeof(double2);
+  auto kern = box2_down_kernel<RF1, RF2, RI1, RI2, CF1, CF2, CI1, CI2>;
+  cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, nsm = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nitem, (int64_t)nsm * std::max(per, 1)));
+  kern<<<grid, 128, smem, s>>>(in, nitem, par, oct, shift, tw.d + tw.offset[NR], tw.d + tw.offset[NR2],
+                               tw.d + tw.offset[NC], tw.d + tw.offset[NC2], add, out);
+}
+
 template <int RF1, int RF2, int RI1, int RI2, int CF1, int CF2, int CI1, int CI2>
 static void launch_box2_t(const double2 *in, int64_t nitem, const int32_t *cbeg, int64_t cbase, const int8_t *oct,
                           const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
@@ -1230,6 +1425,25 @@ bool box2_up_applies(int nth, int nph, int nth2, int nph2) {
   if (!rs2_enabled() || nth != nph || nth2 != nph2) return false;
   const int key = nth * 1000 + nth2;
   return key == 16032 || key == 32064 || key == 24032;
+}
+
+bool box2_down_applies(int nth, int nph, int nth2, int nph2) {
+  if (!rs2_enabled() || nth != nph || nth2 != nph2) return false;
+  const int key = nth * 1000 + nth2;
+  return key == 32016 || key == 64032 || key == 32024;
+}
+
+// downward single pass: child c = R(conj(shift[oct[c]]) * in[par[c]]) (+ add[c]), c < nitem
+bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *par,
+                      const int8_t *oct, const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
+                      cudaStream_t s) {
+  if (!box2_down_applies(nth, nph, nth2, nph2)) return false;
+  switch (nth * 1000 + nth2) {
+    case 32016: launch_box2d_t<8, 4, 4, 4, 8, 4, 4, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
+    case 64032: launch_box2d_t<8, 8, 8, 4, 8, 8, 8, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
+    case 32024: launch_box2d_t<8, 4, 6, 4, 8, 4, 6, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
+    default: return false;
+  }
 }
 
 bool launch_box2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *cbeg,
