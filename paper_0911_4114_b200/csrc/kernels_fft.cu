@@ -1421,16 +1421,26 @@ static void launch_box2_t(const double2 *in, int64_t nitem, const int32_t *cbeg,
 
 // (nth, nph) -> (nth2, nph2) upward resamples done in one pass (square grids of the C2 microbench
 // B8 / B16 and the C4 translation-only levels); false: use the two-pass kernels
+static bool box2_big() {  // single pass for 64 <-> 128 grids (A/B switch HFMM_BOX2_BIG)
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("HFMM_BOX2_BIG");
+    v = e ? atoi(e) : 0;
+  }
+  return v != 0;
+}
+
 bool box2_up_applies(int nth, int nph, int nth2, int nph2) {
   if (!rs2_enabled() || nth != nph || nth2 != nph2) return false;
   const int key = nth * 1000 + nth2;
-  return key == 16032 || key == 32064 || key == 24032;
+  return key == 16032 || key == 32064 || key == 24032 || (key == 64128 && box2_big());
 }
+
 
 bool box2_down_applies(int nth, int nph, int nth2, int nph2) {
   if (!rs2_enabled() || nth != nph || nth2 != nph2) return false;
   const int key = nth * 1000 + nth2;
-  return key == 32016 || key == 64032 || key == 32024;
+  return key == 32016 || key == 64032 || key == 32024 || (key == 128064 && box2_big());
 }
 
 // downward single pass: child c = R(conj(shift[oct[c]]) * in[par[c]]) (+ add[c]), c < nitem
@@ -1442,6 +1452,7 @@ bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nt
     case 32016: launch_box2d_t<8, 4, 4, 4, 8, 4, 4, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
     case 64032: launch_box2d_t<8, 8, 8, 4, 8, 8, 8, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
     case 32024: launch_box2d_t<8, 4, 6, 4, 8, 4, 6, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
+    case 128064: launch_box2d_t<16, 8, 8, 8, 16, 8, 8, 8>(in, nitem, par, oct, shift, add, out, tw, s); return true;
     default: return false;
   }
 }
@@ -1454,6 +1465,7 @@ bool launch_box2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2
     case 16032: launch_box2_t<4, 4, 8, 4, 4, 4, 8, 4>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
     case 32064: launch_box2_t<8, 4, 8, 8, 8, 4, 8, 8>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
     case 24032: launch_box2_t<6, 4, 8, 4, 6, 4, 8, 4>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
+    case 64128: launch_box2_t<8, 8, 16, 8, 8, 8, 16, 8>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
     default: return false;
   }
 }
