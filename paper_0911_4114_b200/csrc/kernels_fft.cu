@@ -1430,17 +1430,31 @@ static bool box2_big() {  // single pass for 64 <-> 128 grids (A/B switch HFMM_B
   return v != 0;
 }
 
+// Grids with a single-pass kernel, keyed by (nth, nph, nth2, nph2); the template factors are
+// (rows nph -> nph2, columns nth -> nth2).  C2: B8 / B16 square grids; BASELINE matvec configs: the
+// translation-only levels of C3 / C5 (28 <-> 40 <-> 54x56) and C4 (24 <-> 32 <-> 42x48 <-> 60).
+static constexpr int64_t gkey(int a, int b, int c, int d) { return (((int64_t)a * 1000 + b) * 1000 + c) * 1000 + d; }
+
 bool box2_up_applies(int nth, int nph, int nth2, int nph2) {
-  if (!rs2_enabled() || nth != nph || nth2 != nph2) return false;
-  const int key = nth * 1000 + nth2;
-  return key == 16032 || key == 32064 || key == 24032 || (key == 64128 && box2_big());
+  if (!rs2_enabled()) return false;
+  switch (gkey(nth, nph, nth2, nph2)) {
+    case gkey(16, 16, 32, 32): case gkey(32, 32, 64, 64): case gkey(24, 24, 32, 32):
+    case gkey(32, 32, 42, 48): case gkey(42, 48, 60, 60): case gkey(28, 28, 40, 40): case gkey(40, 40, 54, 56):
+      return true;
+    case gkey(64, 64, 128, 128): return box2_big();
+    default: return false;
+  }
 }
 
-
 bool box2_down_applies(int nth, int nph, int nth2, int nph2) {
-  if (!rs2_enabled() || nth != nph || nth2 != nph2) return false;
-  const int key = nth * 1000 + nth2;
-  return key == 32016 || key == 64032 || key == 32024 || (key == 128064 && box2_big());
+  if (!rs2_enabled()) return false;
+  switch (gkey(nth, nph, nth2, nph2)) {
+    case gkey(32, 32, 16, 16): case gkey(64, 64, 32, 32): case gkey(32, 32, 24, 24):
+    case gkey(42, 48, 32, 32): case gkey(60, 60, 42, 48): case gkey(40, 40, 28, 28): case gkey(54, 56, 40, 40):
+      return true;
+    case gkey(128, 128, 64, 64): return box2_big();
+    default: return false;
+  }
 }
 
 // downward single pass: child c = R(conj(shift[oct[c]]) * in[par[c]]) (+ add[c]), c < nitem
@@ -1448,11 +1462,20 @@ bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nt
                       const int8_t *oct, const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
                       cudaStream_t s) {
   if (!box2_down_applies(nth, nph, nth2, nph2)) return false;
-  switch (nth * 1000 + nth2) {
-    case 32016: launch_box2d_t<8, 4, 4, 4, 8, 4, 4, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
-    case 64032: launch_box2d_t<8, 8, 8, 4, 8, 8, 8, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
-    case 32024: launch_box2d_t<8, 4, 6, 4, 8, 4, 6, 4>(in, nitem, par, oct, shift, add, out, tw, s); return true;
-    case 128064: launch_box2d_t<16, 8, 8, 8, 16, 8, 8, 8>(in, nitem, par, oct, shift, add, out, tw, s); return true;
+  switch (gkey(nth, nph, nth2, nph2)) {
+#define B2D(a, b, c, d, R1, R2, R3, R4, C1, C2, C3, C4)                                                      \
+  case gkey(a, b, c, d):                                                                                     \
+    launch_box2d_t<R1, R2, R3, R4, C1, C2, C3, C4>(in, nitem, par, oct, shift, add, out, tw, s);            \
+    return true;
+    B2D(32, 32, 16, 16, 8, 4, 4, 4, 8, 4, 4, 4)
+    B2D(64, 64, 32, 32, 8, 8, 8, 4, 8, 8, 8, 4)
+    B2D(32, 32, 24, 24, 8, 4, 6, 4, 8, 4, 6, 4)
+    B2D(128, 128, 64, 64, 16, 8, 8, 8, 16, 8, 8, 8)
+    B2D(42, 48, 32, 32, 8, 6, 8, 4, 7, 6, 8, 4)
+    B2D(60, 60, 42, 48, 10, 6, 8, 6, 10, 6, 7, 6)
+    B2D(40, 40, 28, 28, 8, 5, 7, 4, 8, 5, 7, 4)
+    B2D(54, 56, 40, 40, 8, 7, 8, 5, 9, 6, 8, 5)
+#undef B2D
     default: return false;
   }
 }
@@ -1461,11 +1484,20 @@ bool launch_box2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2
                     int64_t cbase, const int8_t *oct, const double2 *shift, double2 *out, const TwiddleSet &tw,
                     cudaStream_t s) {
   if (!box2_up_applies(nth, nph, nth2, nph2)) return false;
-  switch (nth * 1000 + nth2) {
-    case 16032: launch_box2_t<4, 4, 8, 4, 4, 4, 8, 4>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
-    case 32064: launch_box2_t<8, 4, 8, 8, 8, 4, 8, 8>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
-    case 24032: launch_box2_t<6, 4, 8, 4, 6, 4, 8, 4>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
-    case 64128: launch_box2_t<8, 8, 16, 8, 8, 8, 16, 8>(in, nitem, cbeg, cbase, oct, shift, out, tw, s); return true;
+  switch (gkey(nth, nph, nth2, nph2)) {
+#define B2U(a, b, c, d, R1, R2, R3, R4, C1, C2, C3, C4)                                                      \
+  case gkey(a, b, c, d):                                                                                     \
+    launch_box2_t<R1, R2, R3, R4, C1, C2, C3, C4>(in, nitem, cbeg, cbase, oct, shift, out, tw, s);          \
+    return true;
+    B2U(16, 16, 32, 32, 4, 4, 8, 4, 4, 4, 8, 4)
+    B2U(32, 32, 64, 64, 8, 4, 8, 8, 8, 4, 8, 8)
+    B2U(24, 24, 32, 32, 6, 4, 8, 4, 6, 4, 8, 4)
+    B2U(64, 64, 128, 128, 8, 8, 16, 8, 8, 8, 16, 8)
+    B2U(32, 32, 42, 48, 8, 4, 8, 6, 8, 4, 7, 6)
+    B2U(42, 48, 60, 60, 8, 6, 10, 6, 7, 6, 10, 6)
+    B2U(28, 28, 40, 40, 7, 4, 8, 5, 7, 4, 8, 5)
+    B2U(40, 40, 54, 56, 8, 5, 8, 7, 8, 5, 9, 6)
+#undef B2U
     default: return false;
   }
 }
