@@ -778,6 +778,11 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
         for (int c = 0; c < 4; ++c) sorted[4 * i + c] = it[k][4 * ord[i] + c];
       if (k == P2P_SYM)
         for (int64_t i = 0; i < m; ++i) sym_pairs += cost(i);
+      if (k == P2P_DIAG && HFMM_P2P_DSYM)  // diagonal tiles: n (n - 1) / 2 unordered pairs each
+        for (int64_t i = 0; i < m; ++i) {
+          const int64_t nt = it[k][4 * i + 1] - it[k][4 * i];
+          sym_pairs += nt * (nt - 1) / 2;
+        }
       p->p2p_items[k] = dupload(sorted);
       p->p2p_nitems[k] = m;
     }
@@ -894,7 +899,8 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, b
   {
     PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
     for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD})
-      launch_p2p_items(pu, p->p2p_items[k], p->p2p_nitems[k], k, p->uscale, p->dummy_t, p->dummy_s, p->y_near,
+      launch_p2p_items(pu, p->p2p_items[k], p->p2p_nitems[k], (k == P2P_DIAG && HFMM_P2P_DSYM) ? P2P_DSYM : k,
+                       p->uscale, p->dummy_t, p->dummy_s, p->y_near,
                        p->stream2);
   }
   if (prof) cudaEventRecord(p->sev[8], p->stream2);

@@ -118,10 +118,14 @@ constexpr int64_t P2P_TILE = (int64_t)HFMM_P2P_TPB * HFMM_P2P_T;  // targets per
 #define HFMM_TAB_STEPS 2048
 #endif
 constexpr int TAB_STEPS = HFMM_TAB_STEPS;  // e^{i h k} table size; h = 2 pi / TAB_STEPS
-enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2 };
+enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2, P2P_DSYM = 3 };
+#ifndef HFMM_P2P_DSYM
+#define HFMM_P2P_DSYM 1  // matvec diagonal tiles with the symmetric kernel (each unordered pair once)
+#endif
 // P2P work items, int64 [nitems][4] = (t0, t1, s0, s1): targets [t0, t1) (<= P2P_TILE), sources
 // [s0, s1).  P2P_SYM: disjoint ranges, rows and columns (each unordered pair once);
-// P2P_DIAG: rows only, self pair masked (sources contain the targets); P2P_ORD: rows only.
+// P2P_DIAG: rows only, self pair masked (sources contain the targets); P2P_ORD: rows only;
+// P2P_DSYM (launch kind of the matvec's diagonal tiles, s-range == t-range): symmetric, pairs once.
 // Adds scale * sum into y_near (zeroed beforehand); scale = kappa TAB_STEPS / (2 pi).
 // dummy_t / dummy_s (scaled units): far positions used to pad partial symmetric tiles.
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,

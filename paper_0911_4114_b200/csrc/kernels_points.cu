@@ -162,6 +162,11 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU
 // t - 1, so after 32 steps lane t holds the warp sum of source t (2 shuffles per step instead of
 // a 5-level butterfly per source); the 4 warps combine in shared memory, one atomic per source.
 // Each source loaded from shared memory serves PT targets of the lane.
+// DS (diagonal tile, targets == sources, <= P2P_TILE points): each unordered pair once -- 32-point
+// block pairs (target block tb = warp + 4 p, source block sb) with tb < sb in full, tb == sb for half
+// of the systolic rotation (steps 1..15 and lanes < 16 of step 16; step 0 is the excluded self pair,
+// P:90), tb > sb skipped (warp-uniform branches).
+template <bool DS>
 __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU pts,
                                                                         const int64_t *__restrict__ items,
                                                                         double scale, double3 dummy_t,
@@ -202,6 +207,7 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
     const int nblk = (cnt + 31) >> 5;
     for (int blk = 0; blk < nblk; ++blk) {
       const int base = blk << 5;
+      const int sb = (int)((c0 - s0) >> 5) + blk;  // source block (DS)
       double cr = 0.0, ci = 0.0;
 #pragma unroll 2
       for (int u = 0; u < 32; ++u) {
@@ -210,7 +216,17 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
         const double2 qs = sq[s];
 #pragma unroll
         for (int p = 0; p < PT; ++p) {
-          const double2 g = green_u(tx[p], ty[p], tz[p], xs, ys, zs, tab);
+          double w = 1.0;
+          if (DS) {
+            const int tb = warp + 4 * p;
+            if (tb > sb) continue;
+            if (tb == sb) {
+              if (u == 0 || u > 16) continue;
+              if (u == 16 && lane >= 16) w = 0.0;   // the other half of the antipodal step
+            }
+          }
+          double2 g = green_u(tx[p], ty[p], tz[p], xs, ys, zs, tab);
+          if (DS) g = make_double2(g.x * w, g.y * w);
           ar[p] = fma(g.x, qs.x, fma(-g.y, qs.y, ar[p]));
           ai[p] = fma(g.x, qs.y, fma(g.y, qs.x, ai[p]));
           cr = fma(g.x, tq[p].x, fma(-g.y, tq[p].y, cr));
@@ -240,10 +256,11 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
                       const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s) {
   if (nitems <= 0) return;
-  if (kind == P2P_SYM)
-    p2p_sym_kernel<<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale,
-                                                        make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
-                                                        make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near);
+  if (kind == P2P_SYM || kind == P2P_DSYM) {
+    auto kern = kind == P2P_SYM ? p2p_sym_kernel<false> : p2p_sym_kernel<true>;
+    kern<<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
+                                             make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near);
+  }
   else if (kind == P2P_DIAG)
     p2p_ord_kernel<true><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
   else
