@@ -44,6 +44,9 @@ constexpr int M2LG_KC = 32;       // directions per chunk (lanes)
 #ifndef HFMM_M2L_PF
 #define HFMM_M2L_PF 4
 #endif
+#ifndef HFMM_M2L_SPLIT
+#define HFMM_M2L_SPLIT 0  // parent-block kernel: real/imaginary halves of each MAC in separate accumulators
+#endif
 #ifndef HFMM_M2L_DPF
 #define HFMM_M2L_DPF 0  // parent-block kernel: prefetch the next neighbour parent's sources
 #endif
@@ -178,6 +181,11 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
     const int64_t g0 = range * groups_per_unit, g1 = min(ngroups, g0 + groups_per_unit);
     for (int64_t g = g0 + warp; g < g1; g += M2LG_WARPS) {
       double2 acc[8];
+#if HFMM_M2L_SPLIT
+      double2 acc2[8];  // second accumulator per target: independent FMA chains (ILP)
+#pragma unroll
+      for (int a = 0; a < 8; ++a) acc2[a] = make_double2(0.0, 0.0);
+#endif
 #pragma unroll
       for (int a = 0; a < 8; ++a) acc[a] = make_double2(0.0, 0.0);
       const uint32_t mask = __ldg(&gmask[g]);
@@ -212,7 +220,13 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
           for (int d = 0; d < 8; ++d) {
             const int ex = (d >> 2) + dx, ey = ((d >> 1) & 1) + dy, ez = (d & 1) + dz;
             if (ex < 0 || ex > 1 || ey < 0 || ey > 1 || ez < 0 || ez > 1) continue;
+#if HFMM_M2L_SPLIT
+            const double2 mm = m[(ex << 2) | (ey << 1) | ez];
+            acc[d] = make_double2(fma(t.x, mm.x, acc[d].x), fma(t.x, mm.y, acc[d].y));
+            acc2[d] = make_double2(fma(-t.y, mm.y, acc2[d].x), fma(t.y, mm.x, acc2[d].y));
+#else
             acc[d] = g_cfma(t, m[(ex << 2) | (ey << 1) | ez], acc[d]);
+#endif
           }
         }
 #if HFMM_M2L_DPF
@@ -226,6 +240,9 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
 #pragma unroll
       for (int d = 0; d < 8; ++d) {
         const int32_t b = gtarget[g * 8 + d];
+#if HFMM_M2L_SPLIT
+        acc[d] = make_double2(acc[d].x + acc2[d].x, acc[d].y + acc2[d].y);
+#endif
         if (b >= 0 && kval) I[(int64_t)b * K + k] = acc[d];
       }
     }
