@@ -402,6 +402,9 @@ void launch_l2t(PointsDev pts, const int64_t *first, const double *cx, const dou
 //        box's points (<= 32) and 32/P slices of the directions; slices reduced by shuffles.
 // ---------------------------------------------------------------------------------------------
 constexpr int SMALL_TPB = 128;
+#ifndef HFMM_L2T_V2
+#define HFMM_L2T_V2 1  // L2T with directions on lanes (0: point-on-lane kernel, A/B)
+#endif
 constexpr int SMALL_WARPS = SMALL_TPB / 32;
 
 __global__ void __launch_bounds__(SMALL_TPB) s2m_warp_kernel(PointsDev pts, const int64_t *__restrict__ first,
@@ -513,6 +516,69 @@ __global__ void __launch_bounds__(SMALL_TPB) l2t_warp_kernel(PointsDev pts, cons
   }
 }
 
+// L2T, directions on lanes (the S2M layout): lane holds directions (k0 + lane, k0 + 32 + lane)
+// with their L values and kappa s in registers, the box's points are broadcast from shared memory
+// 32 at a time, and each point's partial sum is reduced across the warp (5 xor-shuffle levels);
+// lane p keeps the running sum of point p of the current 32-point batch.  Two evaluations per
+// lane per point with no global load in the inner loop.
+__global__ void __launch_bounds__(SMALL_TPB) l2t_warp2_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                              const double *__restrict__ cx,
+                                                              const double *__restrict__ cy,
+                                                              const double *__restrict__ cz, int32_t box0,
+                                                              int32_t box1, const double *__restrict__ ks,
+                                                              int64_t K, const double2 *__restrict__ L, double w,
+                                                              const double *__restrict__ wk,
+                                                              double2 *__restrict__ y_far) {
+  __shared__ double2 tab[TAB];
+  __shared__ double wx[SMALL_WARPS][32], wy[SMALL_WARPS][32], wz[SMALL_WARPS][32];
+  fill_exp_table(tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * SMALL_WARPS;
+  const double ws = wk ? 1.0 : w;
+  for (int64_t b = box0 + (int64_t)blockIdx.x * SMALL_WARPS + warp; b < box1; b += nwarps) {
+    const int64_t s0 = first[b], s1 = first[b + 1];
+    const double c0x = cx[b], c0y = cy[b], c0z = cz[b];
+    const double2 *Lb = L + b * K;
+    for (int64_t j0 = s0; j0 < s1; j0 += 32) {  // batches of 32 points
+      const int cnt = (int)min((int64_t)32, s1 - j0);
+      __syncwarp();
+      if (lane < cnt) {  // c_a - x_i
+        wx[warp][lane] = c0x - pts.x[j0 + lane];
+        wy[warp][lane] = c0y - pts.y[j0 + lane];
+        wz[warp][lane] = c0z - pts.z[j0 + lane];
+      }
+      __syncwarp();
+      double yr = 0.0, yi = 0.0;  // lane p: point j0 + p
+      for (int64_t k0 = 0; k0 < K; k0 += 64) {
+        const int64_t ka = k0 + lane, kb = ka + 32;
+        const bool va = ka < K, vb = kb < K;
+        const double kxa = va ? ks[ka] : 0.0, kya = va ? ks[K + ka] : 0.0, kza = va ? ks[2 * K + ka] : 0.0;
+        const double kxb = vb ? ks[kb] : 0.0, kyb = vb ? ks[K + kb] : 0.0, kzb = vb ? ks[2 * K + kb] : 0.0;
+        double2 la = va ? Lb[ka] : make_double2(0.0, 0.0), lb = vb ? Lb[kb] : make_double2(0.0, 0.0);
+        if (wk) {  // per-point weights (ragged rows, R-15)
+          const double wa = va ? wk[ka] : 0.0, wb = vb ? wk[kb] : 0.0;
+          la = make_double2(wa * la.x, wa * la.y), lb = make_double2(wb * lb.x, wb * lb.y);
+        }
+        for (int p = 0; p < cnt; ++p) {
+          const double dx = wx[warp][p], dy = wy[warp][p], dz = wz[warp][p];
+          const double2 ea = cexpi_u(fma(kxa, dx, fma(kya, dy, kza * dz)), tab);
+          const double2 eb = cexpi_u(fma(kxb, dx, fma(kyb, dy, kzb * dz)), tab);
+          double pr = fma(ea.x, la.x, fma(-ea.y, la.y, fma(eb.x, lb.x, -eb.y * lb.y)));
+          double pi = fma(ea.x, la.y, fma(ea.y, la.x, fma(eb.x, lb.y, eb.y * lb.x)));
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            pr += __shfl_xor_sync(0xffffffffu, pr, off);
+            pi += __shfl_xor_sync(0xffffffffu, pi, off);
+          }
+          if (lane == p) yr += pr, yi += pi;
+        }
+      }
+      if (lane < cnt) y_far[j0 + lane] = make_double2(ws * yr, ws * yi);
+    }
+  }
+}
+
 static unsigned persistent_grid(int64_t nbox, const void *fn) {
   int per_sm = 0, dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -533,8 +599,13 @@ void launch_l2t_small(PointsDev pts, const int64_t *first, const double *cx, con
                       int32_t box0, int32_t box1, const double *ks, int64_t K, const double2 *L, double w,
                       const double *wk, double2 *y_far, cudaStream_t s) {
   if (box1 <= box0) return;
+#if HFMM_L2T_V2
+  l2t_warp2_kernel<<<persistent_grid(box1 - box0, (const void *)l2t_warp2_kernel), SMALL_TPB, 0, s>>>(
+      pts, first, cx, cy, cz, box0, box1, ks, K, L, w, wk, y_far);
+#else
   l2t_warp_kernel<<<persistent_grid(box1 - box0, (const void *)l2t_warp_kernel), SMALL_TPB, 0, s>>>(
       pts, first, cx, cy, cz, box0, box1, ks, K, L, w, wk, y_far);
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------
