@@ -182,6 +182,7 @@ class HFMM:
         if rc != 0:
             raise HFMMError(rc, self.lib.hfmm_last_error(None).decode())
         self.h = h
+        self.device = int(device)
         self.n = 0
         self.last_rc = 0
 
@@ -214,12 +215,32 @@ class HFMM:
     def precompute(self, kappa: float, eps: float, alpha: float = 0.8, tau: float = 0.0, flags: int = 0):
         return self._check(self.lib.hfmm_precompute(self.h, kappa, eps, alpha, tau, flags))
 
+    def _check_vec(self, t, name: str, cuda: bool):
+        """The library reads / writes exactly n complex128 values at the pointer: reject anything else
+        (wrong dtype, strided view, wrong length, other device) before the call."""
+        if hasattr(t, "data_ptr"):
+            import torch
+            ok = (t.dtype == torch.complex128 and t.is_contiguous() and tuple(t.shape) == (self.n,)
+                  and bool(t.is_cuda) == cuda and (not cuda or t.device.index == self.device))
+            what = f"{name}: dtype {t.dtype}, shape {tuple(t.shape)}, device {t.device}"
+        else:
+            ok = (isinstance(t, np.ndarray) and t.dtype == np.complex128 and t.flags.c_contiguous
+                  and t.shape == (self.n,) and not cuda)
+            what = f"{name}: {type(t).__name__} dtype {getattr(t, 'dtype', None)}, shape {getattr(t, 'shape', None)}"
+        if not ok:
+            where = f"cuda:{self.device}" if cuda else "host"
+            raise HFMMError(-1, f"{what}; need a contiguous complex128 vector of shape ({self.n},) on {where}")
+
     def _apply(self, fn, q, out=None, stream=None, local=False, serial=False):
         mem_local = (HFMM_Y_LOCAL if local else 0) | (HFMM_SERIAL if serial else 0)
+        if self.n <= 0:
+            raise HFMMError(-5, "matvec before build_tree")
         if hasattr(q, "is_cuda") and q.is_cuda:
             import torch
             if out is None:
                 out = torch.empty_like(q)
+            self._check_vec(q, "q", True)
+            self._check_vec(out, "out", True)
             s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
             if not s:
                 s = 1  # torch's default stream is the legacy default stream (cudaStreamLegacy)
@@ -229,12 +250,16 @@ class HFMM:
             import torch
             if out is None:
                 out = torch.empty_like(q)
+            self._check_vec(q, "q", False)
+            self._check_vec(out, "out", False)
             s = None if stream is None else C.c_void_p(stream or 1)  # 0 -> cudaStreamLegacy
             self._check(fn(self.h, q.data_ptr(), out.data_ptr(), HFMM_HOST | mem_local, s))
             return out
         q = np.ascontiguousarray(q, dtype=np.complex128)
         if out is None:
             out = np.empty_like(q)
+        self._check_vec(q, "q", False)
+        self._check_vec(out, "out", False)
         self._check(fn(self.h, q.ctypes.data, out.ctypes.data, HFMM_HOST | mem_local, None))
         return out
 

@@ -80,6 +80,7 @@ T *dupload(const std::vector<T> &h) {
 }
 
 TwiddleSet &global_twiddles(int device) {
+  std::lock_guard<std::recursive_mutex> lk(cache_mutex());
   static std::map<int, std::unique_ptr<TwiddleSet>> sets;
   auto it = sets.find(device);
   if (it != sets.end()) return *it->second;
@@ -144,6 +145,11 @@ struct hfmm_plan {
 
 static thread_local std::string g_create_err;
 
+std::recursive_mutex &hfmm::cache_mutex() {
+  static std::recursive_mutex m;
+  return m;
+}
+
 #define CK(call)                                                                     \
   do {                                                                               \
     cudaError_t e_ = (call);                                                         \
@@ -197,6 +203,8 @@ static void free_points(hfmm_plan *p) {
   p->have_tree = false;
 }
 
+extern "C" void hfmm_destroy(hfmm_plan *p);
+
 extern "C" int hfmm_create(hfmm_plan **out, int device) {
   if (!out) return HFMM_E_ARG;
   *out = nullptr;
@@ -211,31 +219,43 @@ extern "C" int hfmm_create(hfmm_plan **out, int device) {
     return HFMM_E_ARG;
   }
   auto *p = new hfmm_plan();
+  // on any CUDA failure below: message into g_create_err (what hfmm_last_error(NULL) returns),
+  // release what was created, no plan returned
+#define CKC(call)                                                                    \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      g_create_err = std::string("hfmm_create: ") + #call + ": " + cudaGetErrorString(e_); \
+      hfmm_destroy(p);                                                               \
+      return HFMM_E_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
   p->device = device;
   cudaSetDevice(device);
-  CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   {
     // The far-field chain (latency-bound resampling, M2L, S2M/L2T) runs at high priority so its
     // CTAs take SM slots as soon as CTAs of the FP64-bound near field (low priority) retire.
     int lo = 0, hi = 0;
-    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
 #if HFMM_STREAM_PRIORITY
-    CK(cudaStreamCreateWithPriority(&p->stream2, cudaStreamNonBlocking, lo));
-    CK(cudaStreamCreateWithPriority(&p->stream_hi, cudaStreamNonBlocking, hi));
+    CKC(cudaStreamCreateWithPriority(&p->stream2, cudaStreamNonBlocking, lo));
+    CKC(cudaStreamCreateWithPriority(&p->stream_hi, cudaStreamNonBlocking, hi));
 #else
-    CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&p->stream_hi, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&p->stream_hi, cudaStreamNonBlocking));
 #endif
   }
-  CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&p->ev_join_hi, cudaEventDisableTiming));
-  for (auto &e : p->sev) CK(cudaEventCreate(&e));
+  CKC(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&p->ev_join_hi, cudaEventDisableTiming));
+  for (auto &e : p->sev) CKC(cudaEventCreate(&e));
   const char *prof = std::getenv("HFMM_PROFILE_STAGES");
   p->profile = prof && prof[0] && prof[0] != '0';
   global_twiddles(device);
   *out = p;
   return HFMM_OK;
+#undef CKC
 }
 
 extern "C" int hfmm_set_dist(hfmm_plan *p, int rank, int nranks, const void *id) {
@@ -507,7 +527,12 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       double2 *T = nullptr;
       rc = level_tables(p, L, &T, &L.F);
       if (rc) return rc;
-      L.active = force || (L.F <= p->tau);
+      if (!T && force) {  // h_n overflow: no usable table even when every level is forced
+        p->err = "hfmm_precompute: transfer function overflows (h_n) at level " + std::to_string(l) +
+                 " -- cannot force it active";
+        return HFMM_E_SEARCH;
+      }
+      L.active = T && (force || (L.F <= p->tau));
       if (L.active) {
         L.T = T;
         break;
@@ -558,6 +583,11 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
         cudaFree(U.T);
         int rc = level_tables(p, U, &U.T, &U.F);
         if (rc) return rc;
+        if (!U.T) {
+          p->err = "hfmm_precompute: transfer function overflows (h_n) at level " + std::to_string(l) +
+                   " after the monotone-grid rebuild";
+          return HFMM_E_SEARCH;
+        }
       }
     }
   }
@@ -1195,6 +1225,7 @@ struct OpCache {
   }
 };
 OpCache &op_cache() {  // per device: the index arrays live in that device's memory
+  std::lock_guard<std::recursive_mutex> lk(cache_mutex());
   static std::map<int, OpCache> caches;
   int d = 0;
   cudaGetDevice(&d);
@@ -1259,7 +1290,10 @@ extern "C" int hfmm_m2m_op(int nparent, int nth, int nph, int nth2, int nph2, co
   cudaStream_t s = (cudaStream_t)stream;
   const TwiddleSet &tw = global_twiddles(cur_device());
   OpCache &c = op_cache();
-  c.ensure(nparent);
+  {
+    std::lock_guard<std::recursive_mutex> lk(cache_mutex());
+    c.ensure(nparent);
+  }
   double2 *tmp = (double2 *)work;
   bool own = false;
   if (!tmp) {
@@ -1286,7 +1320,10 @@ extern "C" int hfmm_l2l_op(int nparent, int nth, int nph, int nth2, int nph2, co
   cudaStream_t s = (cudaStream_t)stream;
   const TwiddleSet &tw = global_twiddles(cur_device());
   OpCache &c = op_cache();
-  c.ensure(nparent);
+  {
+    std::lock_guard<std::recursive_mutex> lk(cache_mutex());
+    c.ensure(nparent);
+  }
   double2 *tmp = (double2 *)work;
   bool own = false;
   if (!tmp) {

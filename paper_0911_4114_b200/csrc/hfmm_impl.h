@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <complex>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -12,6 +13,11 @@
 namespace hfmm {
 
 using cplx = std::complex<double>;
+
+// One lock for the process-wide per-device caches (twiddles, __constant__ uploads, operator index
+// arrays, device twiddle offsets): concurrent plans on several devices from several threads
+// (one thread per GPU) must not race on their std::map / std::set insertions.
+std::recursive_mutex &cache_mutex();
 
 // ---------------- host special functions (host_specfun.cpp) ---------------------------------
 // Spherical Bessel j_n (Miller, downward), y_n (upward), cylindrical J_n (Miller).

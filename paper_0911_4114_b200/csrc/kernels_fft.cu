@@ -933,11 +933,10 @@ static void launch_cols2_t(const double2 *in, int64_t nitem, int ncols, int rowl
 }
 
 static int rs2_enabled() {
-  static int enabled = -1;
-  if (enabled < 0) {
+  static const int enabled = [] {   // thread-safe one-time initialisation
     const char *e = getenv("HFMM_RS2");   // 0: tiled passes only (A/B)
-    enabled = e ? atoi(e) : 1;
-  }
+    return e ? atoi(e) : 1;
+  }();
   return enabled;
 }
 
@@ -1422,11 +1421,10 @@ static void launch_box2_t(const double2 *in, int64_t nitem, const int32_t *cbeg,
 // (nth, nph) -> (nth2, nph2) upward resamples done in one pass (square grids of the C2 microbench
 // B8 / B16 and the C4 translation-only levels); false: use the two-pass kernels
 static bool box2_big() {  // single pass for 64 <-> 128 grids (A/B switch HFMM_BOX2_BIG)
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char *e = getenv("HFMM_BOX2_BIG");
-    v = e ? atoi(e) : 0;
-  }
+    return e ? atoi(e) : 0;
+  }();
   return v != 0;
 }
 

@@ -266,6 +266,7 @@ struct M2LGroupPlan {
 #endif
 
 static void upload_slot_table() {
+  std::lock_guard<std::recursive_mutex> lk(cache_mutex());
   static std::set<int> done;
   int d = 0;
   cudaGetDevice(&d);
@@ -382,6 +383,7 @@ static bool dense_group(int na, const int32_t *tgt, const int32_t *row, const in
 }
 
 static void upload_sym_table() {  // __constant__ memory is per device: upload once per device
+  std::lock_guard<std::recursive_mutex> lk(cache_mutex());
   static std::set<int> done;
   int d = 0;
   cudaGetDevice(&d);

@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU
 // a 5-level butterfly per source); the 4 warps combine in shared memory, one atomic per source.
 // Each source loaded from shared memory serves PT targets of the lane.
 // DS (diagonal tile, targets == sources, <= P2P_TILE points): each unordered pair once -- 32-point
-// block pairs (target block tb = warp + 4 p, source block sb) with tb < sb in full, tb == sb for half
+// block pairs (target block tb = warp + (P2P_TPB / 32) p, source block sb) with tb < sb in full, tb == sb for half
 // of the systolic rotation (steps 1..15 and lanes < 16 of step 16; step 0 is the excluded self pair,
 // P:90), tb > sb skipped (warp-uniform branches).
 template <bool DS>
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
         for (int p = 0; p < PT; ++p) {
           double w = 1.0;
           if (DS) {
-            const int tb = warp + 4 * p;
+            const int tb = warp + (P2P_TPB / 32) * p;
             if (tb > sb) continue;
             if (tb == sb) {
               if (u == 0 || u > 16) continue;

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(RG_TPB) rect2rag_kernel(const double2 *__restr
 
 static const int32_t *twiddle_offsets_device(const TwiddleSet &tw) {
   // device copy of TwiddleSet::offset (lengths < kMaxFFT), one per TwiddleSet (one set per device)
+  std::lock_guard<std::recursive_mutex> lk(cache_mutex());
   static std::map<const TwiddleSet *, int32_t *> copies;
   auto it = copies.find(&tw);
   if (it != copies.end()) return it->second;
