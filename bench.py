@@ -50,9 +50,11 @@ def parse():
                     help="C2 operator microbench bandwidths B (comma list; '' to skip)")
     ap.add_argument("--ragged", type=int, default=0,
                     help="1: ragged quadrature on the active levels (HFMM_RAGGED, DESIGN.md R-15)")
-    ap.add_argument("--extra", default="C3,C5",
+    ap.add_argument("--extra", default="C3,C5,C3_acc,C5_acc",
                     help="other BASELINE matvec configs timed after the main one (comma list; '' to skip)")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--oracle-full", default=None,
+                    help="time ONE full-vector oracle matvec of this config on every host core, print it, exit")
     return ap.parse_args()
 
 
@@ -107,52 +109,82 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
-def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
-    """Time the CPU oracle (as it stands) on a bounded sample of one matvec and extrapolate.
+def host_info():
+    """Host cores and CPU model (the oracle baseline runs on this host)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
-    Sample: S2M, L2T and P2P on `budget_leaves` far-field leaves, M2M / L2L on 2 children per
-    level, M2L on 2 target boxes per level; each term is scaled by its unit count (points x
-    directions, pairs, children, interaction-list entries).  Returns (seconds per matvec,
-    description, cores)."""
-    from threadpoolctl import threadpool_limits
-    from oracle.plan import make_plan, choose_source_level, set_source_level
-    from oracle.fmm import OracleFMM
-    from oracle.tree import interaction_list, neighbours
-    with threadpool_limits(1):
+
+_ORACLE_CACHE = {}
+
+
+def oracle_setup(cfg, x, workers):
+    """The oracle's plan (with the library's default source-level policy, R-14) and tree: built
+    once per process, outside every timed sample."""
+    key = (cfg.name, workers)
+    if key not in _ORACLE_CACHE:
+        from oracle.plan import make_plan, choose_source_level, set_source_level
+        from oracle.fmm import OracleFMM
         plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha)
-        if plan.L_f is not None:   # the same source level as the library's default policy (R-14)
+        if plan.L_f is not None:
             set_source_level(plan, choose_source_level(x, cfg.lo, cfg.size, cfg.depth, plan.L_f))
-        f = OracleFMM(x, cfg.lo, cfg.size, plan)
-        rng = np.random.default_rng(seed)
-        total = 0.0
-        desc = []
+        _ORACLE_CACHE[key] = OracleFMM(x, cfg.lo, cfg.size, plan, workers=workers)
+    return _ORACLE_CACHE[key]
+
+
+def oracle_sample(cfg, x, q, budget_targets: int = 2000, seed: int = 0, workers: int = None):
+    """Time the CPU oracle (as it stands) on a bounded sample of one matvec, on `workers` threads
+    (default: every host core; BLAS held to one thread per worker).
+
+    Sample: P2P, S2M and L2T for `budget_targets` points of one randomly drawn far-field leaf
+    (S2M of the source-level boxes holding them), M2L on 2 target boxes per active level, M2M and
+    L2L on 2 children per level.  Every term is measured; the extrapolation to one matvec scales
+    each by its unit count (pairs, points, interaction-list entries, children) and is reported
+    separately.  Returns dict(sample_s = measured wall seconds of the sample, s_per_matvec =
+    extrapolated seconds per matvec, sample = description, cores = threads used)."""
+    from threadpoolctl import threadpool_limits
+    from oracle.tree import interaction_list, neighbours
+    workers = workers or os.cpu_count() or 1
+    f = oracle_setup(cfg, x, workers)
+    plan = f.plan
+    rng = np.random.default_rng(seed)
+    with threadpool_limits(1):
+        t_all = time.perf_counter()
         if plan.L_f is None:
-            t = rng.choice(len(x), size=min(len(x), 200), replace=False)
+            t = rng.choice(len(x), size=min(len(x), budget_targets), replace=False)
             t0 = time.perf_counter()
             f.p2p(q, t)
             dt = time.perf_counter() - t0
-            total = dt * len(x) / len(t)
-            return total, f"direct sum for {len(t)} sampled targets, x{len(x) / len(t):.0f}", 1
+            return {"sample_s": time.perf_counter() - t_all, "s_per_matvec": dt * len(x) / len(t),
+                    "sample": f"direct sum for {len(t)} sampled targets, x{len(x) / len(t):.0f}", "cores": workers}
         L, S = plan.L_f, plan.source_level
         lev = f.levels[L]
-        leaves = rng.choice(len(lev.boxes), size=min(budget_leaves, len(lev.boxes)), replace=False)
-        pts = np.concatenate([lev.members[b] for b in leaves])
-        # S2M on the source-level boxes inside the sampled far-field leaves
+        leaf = int(rng.integers(len(lev.boxes)))
+        mem = lev.members[leaf]
+        pts = np.sort(rng.choice(mem, size=min(budget_targets, len(mem)), replace=False))
+        # S2M on the source-level boxes holding the sampled points (scaled by points covered)
         levS = f.levels[S]
-        sbox = sorted({levS.index[tuple(c)] for c in np.minimum(np.floor((x[pts] - np.asarray(cfg.lo)) / levS.a)
-                                                               .astype(np.int64), 2 ** S - 1).tolist()})
+        bS = np.minimum(np.floor((x[pts] - np.asarray(cfg.lo)) / levS.a).astype(np.int64), 2 ** S - 1)
+        sbox = sorted({levS.index[tuple(c)] for c in bS.tolist()})
+        covered = sum(len(levS.members[b]) for b in sbox)
         t0 = time.perf_counter()
         f.s2m(q, boxes=sbox)
-        ts2m = (time.perf_counter() - t0) * len(x) / len(pts)
-        # P2P (pairs-weighted)
-        pairs_s = sum(len(lev.members[b]) * sum(len(lev.members[c]) for c in neighbours(lev, lev.boxes[b]))
-                      for b in leaves)
+        ts2m = (time.perf_counter() - t0) * len(x) / covered
+        # P2P (scaled by ordered pairs)
+        nsrc = sum(len(lev.members[c]) for c in neighbours(lev, lev.boxes[leaf]))
         pairs_all = sum(len(lev.members[b]) * sum(len(lev.members[c]) for c in neighbours(lev, lev.boxes[b]))
                         for b in range(len(lev.boxes)))
         t0 = time.perf_counter()
         f.p2p(q, pts)
-        tp2p = (time.perf_counter() - t0) * pairs_all / pairs_s
-        # L2T with a random local field
+        tp2p = (time.perf_counter() - t0) * pairs_all / (len(pts) * nsrc)
+        # L2T with a random local field (scaled by points)
         Kf = plan.levels[S].K
         Lf = {b: rng.standard_normal(Kf) + 1j * rng.standard_normal(Kf) for b in sbox}
         t0 = time.perf_counter()
@@ -170,6 +202,9 @@ def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
                 Mall = {b: rng.standard_normal(K) + 1j * rng.standard_normal(K) for b in range(nb)}
                 nnz_s = sum(len(interaction_list(levl, levl.boxes[a])) for a in sub)
                 nnz = sum(len(interaction_list(levl, levl.boxes[a])) for a in range(nb))
+                for a in sub:                      # tables are precompute (untimed in the GPU path too)
+                    for _, o in interaction_list(levl, levl.boxes[a]):
+                        f.table(l, o)
                 t0 = time.perf_counter()
                 f.m2l(Mall, l, targets=sub)
                 tmid += (time.perf_counter() - t0) * nnz / max(nnz_s, 1)
@@ -178,15 +213,39 @@ def oracle_sample(cfg, x, q, budget_leaves: int = 2, seed: int = 0):
                 f.m2m(M, l)
                 tmid += (time.perf_counter() - t0) * nb / len(sub)
                 Kp = plan.levels[l - 1].K
-                Lp = {p: rng.standard_normal(Kp) + 1j * rng.standard_normal(Kp) for p in range(len(f.levels[l - 1].boxes))}
+                pa = sorted({f.levels[l - 1].index[(c[0] // 2, c[1] // 2, c[2] // 2)] for c in (levl.boxes[b] for b in sub)})
+                Lp = {p: rng.standard_normal(Kp) + 1j * rng.standard_normal(Kp) for p in pa}
                 t0 = time.perf_counter()
                 f.l2l(Lp, M, l - 1)
                 tmid += (time.perf_counter() - t0) * nb / len(sub)
-        total = ts2m + tp2p + tl2t + tmid
-        desc = (f"oracle passes on {len(leaves)} of {len(lev.boxes)} far-field leaves ({len(pts)} points: S2M and "
-                f"L2T at source level {S}, P2P at L_f={L}), M2L on 2 boxes/level, M2M+L2L on 2 children/level; "
-                f"each term scaled by its unit count")
-        return total, desc, 1
+        sample_s = time.perf_counter() - t_all
+    desc = (f"oracle on {workers} threads: P2P, S2M and L2T for {len(pts)} points of 1 of {len(lev.boxes)} far-field "
+            f"leaves (S2M/L2T at source level {S}, P2P at L_f={L}), M2L on 2 boxes/level, M2M+L2L on 2 "
+            f"children/level; measured {sample_s:.2f} s, extrapolated to one matvec by unit counts")
+    return {"sample_s": sample_s, "s_per_matvec": ts2m + tp2p + tl2t + tmid, "sample": desc, "cores": workers,
+            "terms_s_per_matvec": {"s2m": ts2m, "p2p": tp2p, "l2t": tl2t, "m2m_m2l_l2l": tmid}}
+
+
+def golden_parity(name, y, info):
+    """y of a timed matvec vs the oracle's stored target-subset values (tests/golden/subset_<name>.json,
+    written by tools/gen_subset_refs.py from oracle/ only): relative L2 over the sampled targets, and
+    the error vs the stored direct sums.  Reads stored numbers only (no oracle code runs here)."""
+    path = os.path.join(ROOT, "tests", "golden", f"subset_{name}.json")
+    if not os.path.exists(path):
+        return {"available": False}
+    d = json.load(open(path))
+    if (d["L_f"], d["source_level"]) != (info["L_f"], info["source_level"]):
+        return {"available": False, "why": "plan differs from the stored reference's"}
+    t = np.array(d["targets"])
+    c = lambda v: np.array([complex(a, b) for a, b in v])
+    yo = c(d["y_near"]) + c(d["y_far"])
+    out = {"available": True, "targets": len(t), "rel_l2_vs_oracle": float(np.linalg.norm(y[t] - yo) / np.linalg.norm(yo)),
+           "bar": 1e-11, "max_F_active": max((v["F"] for v in d["levels"].values() if v["active"]), default=None)}
+    if d.get("y_direct"):
+        yd = c(d["y_direct"])
+        out["err_vs_direct"] = float(np.linalg.norm(y[t] - yd) / np.linalg.norm(yd))
+        out["eps"] = d["config"]["eps"]
+    return out
 
 
 def hbm_peak():
@@ -275,7 +334,7 @@ def bench_operators(bandwidths, reps: int = 5, fp64_peak_tflops: float = 37.2):
     return out
 
 
-def bench_matvec_config(cfg, warmup: int, steps: int):
+def bench_matvec_config(cfg, warmup: int, steps: int, tau: float = 0.0, golden: str = None):
     """One more BASELINE matvec config on this GPU (context for the main line): ms per matvec with
     q resident, L2 flushed between steps, CUDA events on the launching stream."""
     import torch
@@ -284,7 +343,7 @@ def bench_matvec_config(cfg, warmup: int, steps: int):
     x, q = points_and_charges(cfg)
     g = hf.HFMM(0)
     g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
-    g.precompute(cfg.kappa, cfg.eps, cfg.alpha)
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha, tau=tau)
     info = g.info()
     qd = torch.from_numpy(q).cuda()
     yd = torch.empty_like(qd)
@@ -303,43 +362,108 @@ def bench_matvec_config(cfg, warmup: int, steps: int):
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
     t = statistics.mean(ms)
-    out = {"n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps, "geometry": cfg.kind,
+    out = {"n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps, "geometry": cfg.kind, "tau": info["tau"],
            "L_f": info["L_f"], "source_level": info["source_level"], "ms_per_matvec": t, "matvec_per_s": 1e3 / t,
-           "mpoints_per_s": cfg.n / t / 1e3, "p2p_pairs": info["p2p_pairs"], "steps": steps}
+           "mpoints_per_s": cfg.n / t / 1e3, "p2p_pairs": info["p2p_pairs"], "steps": steps,
+           "parity": golden_parity(golden or cfg.name, yd.cpu().numpy(), info)}
     g.close()
     del qd, yd, flush
     torch.cuda.empty_cache()
     return out
 
 
+def oracle_full(name):
+    """One full-vector oracle matvec (every target) on every host core: the measured counterpart of
+    the sampled cpu_baseline (its extrapolation is printed beside it for the same config)."""
+    from threadpoolctl import threadpool_limits
+    from workloads import CONFIGS, points_and_charges
+    cfg = CONFIGS[name]
+    x, q = points_and_charges(cfg)
+    workers = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    f = oracle_setup(cfg, x, workers)
+    t_setup = time.perf_counter() - t0
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        y = f.matvec(q)
+        t_full = time.perf_counter() - t0
+    samp = oracle_sample(cfg, x, q, budget_targets=3000, workers=workers)
+    out = {"oracle_full_matvec": name, "n": cfg.n, "seconds": t_full, "setup_s": t_setup, "cores": workers,
+           "host": host_info(), "sampled_extrapolation_s": samp["s_per_matvec"], "sample": samp["sample"]}
+    path = os.path.join(ROOT, "tests", "golden", f"subset_{name}.json")
+    if os.path.exists(path):                  # consistency with the stored target-subset reference
+        d = json.load(open(path))
+        t = np.array(d["targets"])
+        yo = np.array([complex(a, b) for a, b in d["y_near"]]) + np.array([complex(a, b) for a, b in d["y_far"]])
+        out["rel_l2_vs_subset_reference"] = float(np.linalg.norm(y[t] - yo) / np.linalg.norm(yo))
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(cfg, world):
+    """The `config` object of both arms' JSON lines (identical keys, so the driver can pair them)."""
+    return {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps,
+            "seed": cfg.seed, "geometry": cfg.kind, "l2": "flushed (512 MB write) between steps",
+            "parallelism": f"octree level-2 subtrees x{world}"}
+
+
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the CPU oracle, each step a bounded sample, on rank 0 only."""
+    """--impl reference: the CPU oracle on every host core, each step a bounded measured sample
+    (ms_per_step = its measured wall time); value = matvec/s from the unit-count extrapolation,
+    which is reported separately (extrapolated_s_per_matvec).  Rank 0 only."""
     if rank != 0:
         return
     from workloads import points_and_charges
     x, q = points_and_charges(cfg)
-    for _ in range(args.warmup):
-        oracle_sample(cfg, x, q, budget_leaves=1)
-    secs = []
-    desc = ""
-    for k in range(args.steps):
-        s, desc, cores = oracle_sample(cfg, x, q, budget_leaves=1, seed=k)
-        secs.append(s)
-    t = statistics.mean(secs)
-    line = {"metric": "FMM matvecs/s", "value": 1.0 / t, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps,
-                       "seed": cfg.seed, "geometry": cfg.kind},
-            "impl": "reference",
-            "cpu_baseline": {"value": 1.0 / t, "unit": "matvec/s", "cores": 1, "kind": "oracle", "sample": desc},
-            "e2e": {"value": 1.0 / t, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    workers = os.cpu_count() or 1
+    oracle_setup(cfg, x, workers)                       # plan + tree: untimed setup
+    for k in range(args.warmup):
+        oracle_sample(cfg, x, q, budget_targets=REF_TARGETS, seed=1000 + k, workers=workers)
+    samples = [oracle_sample(cfg, x, q, budget_targets=REF_TARGETS, seed=k, workers=workers)
+               for k in range(args.steps)]
+    t_meas = statistics.mean(r["sample_s"] for r in samples)
+    t_mv = statistics.mean(r["s_per_matvec"] for r in samples)
+    line = {"metric": "FMM matvecs/s", "value": 1.0 / t_mv, "unit": "matvec/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_meas, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, world), "impl": "reference",
+            "extrapolated_s_per_matvec": t_mv,
+            "note": "ms_per_step is the measured wall time of one step's sample; value extrapolates the sample "
+                    "to one whole matvec by unit counts (extrapolated_s_per_matvec)",
+            "host": host_info(),
+            "cpu_baseline": {"value": 1.0 / t_mv, "unit": "matvec/s", "cores": workers, "kind": "oracle",
+                             "sample": samples[-1]["sample"]},
+            "e2e": {"value": 1.0 / t_mv, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+REF_TARGETS = 600      # points per reference-arm step (a few seconds of oracle work on 8 cores)
+
+
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` without a torchrun environment: re-exec this script as N ranks
+    (one process per GPU) on 127.0.0.1, exactly as the driver's own torchrun launch would."""
+    import socket
+    import torch
+    ngpu = torch.cuda.device_count()
+    if ngpu < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {ngpu} visible CUDA device(s)"}), flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 # ------------------------------------------------------------------------------------------
 def main():
     args = parse()
+    if args.oracle_full:
+        oracle_full(args.oracle_full)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -453,12 +577,12 @@ def main():
         "metric": "FMM matvecs/s", "value": 1e3 / ms, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps,
-                   "seed": cfg.seed, "geometry": cfg.kind, "L_f": L_f, "l2": "flushed (512 MB write) between steps",
-                   "parallelism": f"octree level-2 subtrees x{world}"},
+        "config": workload_config(cfg, world),
         "mpoints_per_s": cfg.n * 1e3 / ms / 1e6,
         "e2e": {"value": 1e3 / te.item(), "unit": "matvec/s", "h2d_bytes_per_step": cfg.n * 16,
-                "d2h_bytes_per_step": cfg.n * 16},
+                "d2h_bytes_per_step": cfg.n * 16,
+                "note": "hfmm_matvec with pinned host q / y: H2D, the matvec, the y gather across ranks "
+                        "(all-reduce) and the D2H inside the timed region"},
         "gpu_launches": launches,
         "roofline": {"kernel": "p2p", "bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved / peak_tflops, "traffic": traffic,
@@ -476,21 +600,34 @@ def main():
                      "flops_per_launch": p2p_flops,
                      "measured_dfma_peak_tflops": 34.2},
         "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
-        "plan": {"levels": [{k: lv[k] for k in ("level", "ell", "n_theta", "n_phi", "F", "active")}
+        "plan": {"L_f": L_f, "source_level": info["source_level"],
+                 "levels": [{k: lv[k] for k in ("level", "ell", "n_theta", "n_phi", "F", "active")}
                             for lv in info["levels"]], "p2p_pairs": pairs, "s2m_evals": info["s2m_evals"]},
         "setup_s": {"build_tree": t_tree, "precompute": t_pre},
         "clocks": clocks,
     }
+    if world == 1:
+        line["parity"] = golden_parity(cfg.name, yd.cpu().numpy(), info)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s, desc, cores = oracle_sample(cfg, x, q)
-        line["cpu_baseline"] = {"value": 1.0 / s, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": desc}
+        r = oracle_sample(cfg, x, q, budget_targets=3000)
+        line["cpu_baseline"] = {"value": 1.0 / r["s_per_matvec"], "unit": "matvec/s", "cores": r["cores"],
+                                "kind": "oracle", "sample": r["sample"], "sample_s": r["sample_s"],
+                                "extrapolated_s_per_matvec": r["s_per_matvec"], "terms_s_per_matvec": r["terms_s_per_matvec"],
+                                "host": host_info()}
     if world == 1 and (args.ops or args.extra):
         g.close()
         del qd, yd, flush, qh, yh
         torch.cuda.empty_cache()
     if world == 1 and args.extra:
-        line["other_configs"] = {name: bench_matvec_config(CONFIGS[name], args.warmup, max(3, args.steps // 2))
-                                 for name in args.extra.split(",") if name and name != cfg.name}
+        oc = {}
+        for name in args.extra.split(","):
+            base = name.split("_")[0]
+            if not name or name == cfg.name or base not in CONFIGS:
+                continue
+            # "<cfg>_acc": the accuracy-only admissibility tau = eps / 10
+            tau = CONFIGS[base].eps / 10 if name.endswith("_acc") else 0.0
+            oc[name] = bench_matvec_config(CONFIGS[base], args.warmup, max(3, args.steps // 2), tau=tau, golden=name)
+        line["other_configs"] = oc
     if world == 1 and args.ops:
         line["operators"] = bench_operators([int(b) for b in args.ops.split(",")], fp64_peak_tflops=peak_tflops)
     if rank == 0:

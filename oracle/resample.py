@@ -39,8 +39,11 @@ def band(N: int, Np: int) -> np.ndarray:
 def resample_matrix(N: int, Np: int) -> np.ndarray:
     """Dense R[p, j] = sum_{k in band} (1/N) e^{-2 pi i j k / N} e^{2 pi i k p / N'} (cached; read-only)."""
     k = band(N, Np)
-    fwd = np.exp(-2j * math.pi * np.outer(k, np.arange(N)) / N) / N          # [k, j]
-    inv = np.exp(2j * math.pi * np.outer(np.arange(Np), k) / Np)             # [p, k]
+    # e^{-2 pi i j k / N} is periodic in j k with period N: the integer product is reduced mod N
+    # exactly before it becomes a phase, so every entry is within an ulp or two (an unreduced
+    # phase of size ~pi N would carry ~u pi N / 2 of its own error)
+    fwd = np.exp(-2j * math.pi * (np.outer(k, np.arange(N)) % N) / N) / N     # [k, j]
+    inv = np.exp(2j * math.pi * (np.outer(np.arange(Np), k) % Np) / Np)       # [p, k]
     return inv @ fwd
 
 

@@ -1,0 +1,187 @@
+"""GPU parity on the BASELINE matvec paths (VERDICT r1 "next round" item 2).
+
+(a) c4_small: C4's plan (kappa = 32 pi, eps = 1e-8, depth 7, S2M/L2T at depth 7) on 2,000 sphere
+    points.  Its grids are exactly C4's (240 / 140 on the active levels, 60 / 42x48 / 32 / 24 on
+    the translation-only levels), so every kernel instantiation the C4 headline runs (the
+    60 <-> 140 <-> 240 register passes, the 24 <-> 32 <-> 42x48 <-> 60 single-pass kernels, M2L
+    on the 240 / 140 grids) is compared with the oracle stage by stage: M_l, I_l, L_l at every
+    level, y_near, y_far and y (relative L2 <= 1e-11), and y vs direct summation (<= eps).
+(b) every grid pair the C3 / C4 / C5 / C1HF plans instantiate, both directions, through the
+    operator entry points (resample, fused M2M, fused L2L) vs oracle.resample (1e-13).
+(c) full-size C3 / C4 / C5: the library matvec (default flags, the path bench.py times) at 1,000
+    sampled targets vs the oracle's target-subset references in tests/golden/subset_<cfg>.json
+    (written by tools/gen_subset_refs.py from oracle/ only): relative L2 <= 1e-11 for y, y_near
+    and y_far, and <= eps vs the stored direct sums; the integer plan equals the stored one.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from workloads import CONFIGS, small_config, points_and_charges
+from oracle.plan import make_plan
+from oracle.fmm import OracleFMM
+from oracle.direct import direct_sum
+from oracle.resample import resample_half_batch
+
+pytestmark = pytest.mark.gpu
+PARITY = 1e-11
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
+
+
+@pytest.fixture(scope="module")
+def hf():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_0911_4114_b200 as mod
+    from paper_0911_4114_b200.build import build
+    build(verbose=False)
+    return mod
+
+
+# ---- (a) C4's plan on a small point set ------------------------------------------------------
+C4_GRIDS = {2: (240, 240), 3: (140, 140), 4: (60, 60), 5: (42, 48), 6: (32, 32), 7: (24, 24)}
+
+
+@pytest.fixture(scope="module")
+def c4_small(hf):
+    cfg = small_config("c4_small", n=2000, kappa=32 * math.pi, depth=7, eps=1e-8, seed=41)
+    x, q = points_and_charges(cfg)
+    g = hf.HFMM(0)
+    g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha, flags=hf.HFMM_SOURCE_AT_DEPTH)
+    y = g.matvec(q)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=cfg.depth)
+    f = OracleFMM(x, cfg.lo, cfg.size, plan, workers=os.cpu_count() or 1)
+    M, I, Lloc = f.far_locals(q)
+    allt = np.arange(cfg.n)
+    yn, yf = f.p2p(q, allt), f.l2t(Lloc[plan.source_level], allt)
+    return cfg, x, q, plan, f, g, y, (M, I, Lloc, yn, yf)
+
+
+def test_c4_small_plan_is_c4s(c4_small):
+    cfg, x, q, plan, f, g, y, _ = c4_small
+    info = g.info()
+    assert plan.L_f == info["L_f"] == 3 and plan.source_level == info["source_level"] == 7
+    for lv in info["levels"]:
+        l = lv["level"]
+        if l <= 7:
+            assert (lv["n_theta"], lv["n_phi"]) == C4_GRIDS[l] == (plan.levels[l].n_theta, plan.levels[l].n_phi)
+            assert lv["ell"] == plan.levels[l].ell and lv["rep"] == plan.levels[l].rep
+            assert lv["alpha"] == plan.levels[l].alpha
+
+
+def test_c4_small_stages(c4_small):
+    cfg, x, q, plan, f, g, y, (M, I, Lloc, yn, yf) = c4_small
+    for l in range(2, plan.source_level + 1):
+        tab = g.debug(7, l)
+        lev = f.levels[l]
+        mp = np.array([lev.index[(int(r[0]), int(r[1]), int(r[2]))] for r in tab])
+        K = plan.levels[l].K
+        stages = [(0, M), (2, Lloc)] + ([(1, I)] if l <= plan.L_f else [])
+        for what, ref in stages:
+            got = g.debug(what, l).reshape(-1, K)
+            err = rel(got, np.stack([ref[l][mp[b]] for b in range(len(mp))]))
+            assert err <= PARITY, ("MIL"[what], l, err)
+    perm = g.debug(6)
+    assert rel(g.debug(4)[: cfg.n], yn[perm]) <= PARITY
+    assert rel(g.debug(5)[: cfg.n], yf[perm]) <= PARITY
+
+
+def test_c4_small_matvec(c4_small):
+    cfg, x, q, plan, f, g, y, (M, I, Lloc, yn, yf) = c4_small
+    assert rel(y, yn + yf) <= PARITY
+    assert rel(y, direct_sum(x, q, cfg.kappa)) <= cfg.eps
+
+
+# ---- (b) every grid pair of the BASELINE plans, through the operator entry points -----------
+CONFIG_PAIRS = sorted({
+    ((28, 28), (40, 40)), ((40, 40), (54, 56)), ((54, 56), (120, 120)),                  # C3
+    ((24, 24), (32, 32)), ((32, 32), (42, 48)), ((42, 48), (60, 60)), ((60, 60), (140, 140)),
+    ((140, 140), (240, 240)),                                                            # C4
+    ((120, 120), (216, 216)), ((216, 216), (432, 432)),                                  # C5
+    ((120, 120), (240, 240)), ((240, 240), (420, 420)),                                  # C1HF
+})
+
+
+@pytest.mark.parametrize("child,parent", CONFIG_PAIRS)
+def test_config_grid_pairs(hf, child, parent):
+    import torch
+    (nth, nph), (nth2, nph2) = child, parent
+    K, K2 = nth * nph // 2, nth2 * nph2 // 2
+    rng = np.random.default_rng(nth * 1000 + nth2)
+    npar = 3
+    C = rng.standard_normal((8 * npar, K)) + 1j * rng.standard_normal((8 * npar, K))
+    P = rng.standard_normal((npar, K2)) + 1j * rng.standard_normal((npar, K2))
+    S = np.exp(2j * math.pi * rng.uniform(size=(8, K2)))
+    Inc = rng.standard_normal((8 * npar, K)) + 1j * rng.standard_normal((8 * npar, K))
+    dC, dP, dS, dI = (torch.from_numpy(a).cuda() for a in (C, P, S, Inc))
+    tol = 1e-13
+    # interpolation and anterpolation
+    up = torch.empty((8 * npar, K2), dtype=torch.complex128, device="cuda")
+    hf.resample(dC, nth, nph, nth2, nph2, up)
+    ref_up = resample_half_batch(C.reshape(-1, nth, nph // 2), nph, nth2, nph2).reshape(8 * npar, -1)
+    assert rel(up.cpu().numpy(), ref_up) <= tol
+    dn = torch.empty((npar, K), dtype=torch.complex128, device="cuda")
+    hf.resample(dP, nth2, nph2, nth, nph, dn)
+    ref_dn = resample_half_batch(P.reshape(-1, nth2, nph2 // 2), nph2, nth, nph).reshape(npar, -1)
+    assert rel(dn.cpu().numpy(), ref_dn) <= tol
+    # fused M2M: parent p = sum_c S_c * R(child 8p + c)
+    par = torch.empty((npar, K2), dtype=torch.complex128, device="cuda")
+    hf.m2m_op(dC, dS, par, nth, nph, nth2, nph2)
+    ref_m2m = (S[None] * ref_up.reshape(npar, 8, K2)).sum(1)
+    assert rel(par.cpu().numpy(), ref_m2m) <= tol
+    # fused L2L: child c = R(conj(S_{c%8}) * parent c//8) + I_c
+    out = torch.empty((8 * npar, K), dtype=torch.complex128, device="cuda")
+    hf.l2l_op(dP, dS, dI, out, nth2, nph2, nth, nph)
+    prod = (np.conj(S)[None] * P[:, None, :]).reshape(-1, nth2, nph2 // 2)
+    ref_l2l = resample_half_batch(prod, nph2, nth, nph).reshape(8 * npar, -1) + Inc
+    assert rel(out.cpu().numpy(), ref_l2l) <= tol
+
+
+# ---- (c) full-size configs vs the oracle's target-subset references --------------------------
+def load_golden(name):
+    path = os.path.join(GOLDEN, f"subset_{name}.json")
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: run tools/gen_subset_refs.py {name}")
+    with open(path) as fh:
+        d = json.load(fh)
+    c = lambda v: np.array([complex(a, b) for a, b in v])
+    return d, np.array(d["targets"]), c(d["y_near"]), c(d["y_far"]), (c(d["y_direct"]) if d["y_direct"] else None)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_fullsize_subset_parity(hf, name):
+    import torch
+    d, t, yn_o, yf_o, yd = load_golden(name)
+    cfg = CONFIGS[name]
+    assert d["config"]["n"] == cfg.n and d["config"]["seed"] == cfg.seed
+    x, q = points_and_charges(cfg)
+    g = hf.HFMM(0)
+    g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha)
+    info = g.info()
+    assert (info["L_f"], info["source_level"]) == (d["L_f"], d["source_level"])
+    for lv in info["levels"]:
+        ref = d["levels"].get(str(lv["level"]))
+        if ref is not None:
+            assert (lv["ell"], lv["n_theta"], lv["n_phi"], lv["rep"]) == \
+                   (ref["ell"], ref["n_theta"], ref["n_phi"], ref["rep"]), lv["level"]
+    y = g.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    perm = g.debug(6)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    yn_g, yf_g = g.debug(4)[: cfg.n][inv[t]], g.debug(5)[: cfg.n][inv[t]]
+    p_y, p_n, p_f = rel(y[t], yn_o + yf_o), rel(yn_g, yn_o), rel(yf_g, yf_o)
+    print(f"{name}: parity y {p_y:.2e} y_near {p_n:.2e} y_far {p_f:.2e} (max F_l "
+          f"{max(v['F'] for v in d['levels'].values() if v['active']):.1e})")
+    assert p_y <= PARITY and p_n <= PARITY and p_f <= PARITY
+    if yd is not None:
+        assert rel(y[t], yd) <= cfg.eps
+    g.close()

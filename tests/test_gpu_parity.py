@@ -334,10 +334,9 @@ def test_resample_operator(hf, up, grids):
     hf.resample(inp, a[0], a[1], b[0], b[1], out)
     torch.cuda.synchronize()
     ref = resample_half_batch(F, a[1], b[0], b[1])
-    # the oracle's dense DFT matrices evaluate e^{-2 pi i j k / N} at arguments up to ~pi N, so
-    # their own entries carry ~u pi N / 2 relative error (2e-13 at N = 1080): tolerance grows with N
-    tol = max(1e-13, 1.1e-16 * 3.14159 * max(a + b) * 2)
-    assert rel(out.cpu().numpy(), ref) <= tol
+    # the oracle reduces j k mod N before forming each DFT phase (oracle/resample.py), so its
+    # entries are accurate to a few ulp at every N: one flat tolerance
+    assert rel(out.cpu().numpy(), ref) <= 1e-13
 
 
 # ---- the two M2L kernels (M2L): parent-block vs merged-list -------------------------

@@ -164,3 +164,20 @@ def test_multilevel_corner_pair():
     assert abs(errs[2]) < 1e-3
     for L in (3, 4, 5):
         assert abs(errs[L] - errs[2]) < 1e-12 / abs(x[0] - x[1]).max()
+
+
+def test_subset_mode_equals_full_matvec():
+    """Target-subset mode computes exactly the full matvec's y at the sampled
+    targets: same passes restricted to the targets' ancestors (translation-only levels included)."""
+    from workloads import small_config, points_and_charges
+    from oracle.plan import make_plan
+    from oracle.fmm import OracleFMM
+    cfg = small_config("subset", n=1500, kappa=16 * math.pi, depth=4, eps=1e-6, seed=31)
+    x, q = points_and_charges(cfg)
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=4)
+    assert plan.L_f == 2 and plan.source_level == 4
+    f = OracleFMM(x, cfg.lo, cfg.size, plan)
+    t = np.sort(np.random.default_rng(2).choice(cfg.n, 60, replace=False))
+    y_full = f.matvec(q)
+    y_sub = OracleFMM(x, cfg.lo, cfg.size, plan, workers=4).matvec_subset(q, t)
+    assert np.max(np.abs(y_sub - y_full[t])) <= 1e-14 * np.max(np.abs(y_full))
