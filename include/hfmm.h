@@ -29,8 +29,9 @@
  * every function collectively with identical arguments (inputs replicated).  Each rank
  * computes the far field and near field of the level-2 subtrees it owns (Morton-ordered
  * partition weighted by work); multipole expansions of every active level are
- * all-gathered with NCCL over NVLink before M2L; y is all-gathered at the end unless
- * HFMM_Y_LOCAL is set (then only owned entries of y are written, others are zero).
+ * all-gathered with NCCL over NVLink before M2L; y is all-gathered at the end (each rank's
+ * owned sorted range, then unpermuted on every rank) unless HFMM_Y_LOCAL is set (then only owned
+ * entries of y are written, others are zero).
  */
 #ifndef HFMM_H
 #define HFMM_H
@@ -127,6 +128,21 @@ int hfmm_set_dist(hfmm_plan *p, int rank, int nranks, const void *nccl_unique_id
 
 /* Fill out_128b with a fresh ncclUniqueId (rank 0 calls this and broadcasts the bytes). */
 int hfmm_nccl_unique_id(void *out_128b);
+
+/* Virtual ranks (test mode for the multi-rank path on ONE device, one process): a group of
+ * nranks plans, each bound to a rank with hfmm_set_dist_virtual (instead of hfmm_set_dist,
+ * before build_tree; every plan on the same device, built with identical arguments).  The
+ * plans then partition the work exactly as nranks GPUs would.  hfmm_vgroup_matvec runs the
+ * multi-rank matvec over all of them, every collective replaced by one cudaMemcpyAsync per peer
+ * block (M_l all-gather before M2L, y all-gather at the end): q DEVICE pointer [n] complex128
+ * (input order), y DEVICE pointer [nranks][n] (rank r's full output vector at y + r n); enqueued
+ * on `stream` (NULL: rank 0's plan stream, synchronised before return).  A plan bound to a group
+ * returns HFMM_E_STATE from hfmm_matvec.  Destroy the group after (or before) its plans. */
+typedef struct hfmm_vgroup hfmm_vgroup;
+int hfmm_vgroup_create(hfmm_vgroup **out, int nranks);
+int hfmm_set_dist_virtual(hfmm_plan *p, hfmm_vgroup *g, int rank);
+int hfmm_vgroup_matvec(hfmm_vgroup *g, const double *q, double *y, void *stream);
+void hfmm_vgroup_destroy(hfmm_vgroup *g);
 
 /* Octree over n points.  xyz: HOST pointer, n x 3 row-major float64.  depth >= 2 is the
  * configured leaf level D (root level 0); root cube [lo, lo + size]^3 must contain every point

@@ -37,6 +37,7 @@ EXPORTED = [
     "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
     "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
     "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free", "hfmm_m2l_op_kind", "hfmm_ragged_rows",
+    "hfmm_vgroup_create", "hfmm_set_dist_virtual", "hfmm_vgroup_matvec", "hfmm_vgroup_destroy",
 ]
 
 
@@ -102,6 +103,10 @@ def load() -> C.CDLL:
         "hfmm_m2l_op_free": (None, [vp]),
         "hfmm_m2l_op_kind": (ci, [vp]),
         "hfmm_ragged_rows": (ci, [dbl, dbl, dbl, dbl, ci, ci, ci, vp]),
+        "hfmm_vgroup_create": (ci, [C.POINTER(vp), ci]),
+        "hfmm_set_dist_virtual": (ci, [vp, vp, ci]),
+        "hfmm_vgroup_matvec": (ci, [vp, vp, vp, vp]),
+        "hfmm_vgroup_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -304,6 +309,48 @@ class HFMM:
         if what == 7:
             buf = buf.reshape(-1, 4)
         return buf
+
+
+class VirtualGroup:
+    """nranks plans on one device acting as the ranks of a multi-GPU run (test mode; include/hfmm.h
+    hfmm_vgroup_*).  Bind plans with `bind(plan, rank)` before their build_tree."""
+
+    def __init__(self, nranks: int):
+        self.lib = load()
+        h = C.c_void_p()
+        rc = self.lib.hfmm_vgroup_create(C.byref(h), nranks)
+        if rc != 0:
+            raise HFMMError(rc, "hfmm_vgroup_create")
+        self.h, self.nranks, self.plans = h, nranks, [None] * nranks
+
+    def bind(self, plan: "HFMM", rank: int):
+        plan._check(self.lib.hfmm_set_dist_virtual(plan.h, self.h, rank))
+        self.plans[rank] = plan
+
+    def matvec(self, q, out=None, stream=None):
+        """q: device complex128 [n] -> [nranks][n] (every rank's output vector)."""
+        import torch
+        n = self.plans[0].n
+        self.plans[0]._check_vec(q, "q", True)
+        if out is None:
+            out = torch.empty((self.nranks, n), dtype=torch.complex128, device=q.device)
+        if out.dtype != torch.complex128 or not out.is_contiguous() or tuple(out.shape) != (self.nranks, n):
+            raise HFMMError(-1, f"out must be a contiguous complex128 tensor of shape ({self.nranks}, {n})")
+        rc = self.lib.hfmm_vgroup_matvec(self.h, q.data_ptr(), out.data_ptr(), _stream(stream))
+        if rc < 0:
+            raise HFMMError(rc, "hfmm_vgroup_matvec: " + self.plans[0].lib.hfmm_last_error(self.plans[0].h).decode())
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.hfmm_vgroup_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _stream(stream):

@@ -96,16 +96,28 @@ TwiddleSet &global_twiddles(int device) {
 
 }  // namespace
 
+// Virtual ranks (test mode, include/hfmm.h hfmm_vgroup_*): R plans of one process on one device
+// act as the ranks of a multi-GPU run; their collectives become one cudaMemcpyAsync per peer
+// block between the plans' buffers, driven phase by phase by hfmm_vgroup_matvec.
+struct hfmm_vgroup {
+  int nranks = 0;
+  std::vector<hfmm_plan *> plans;
+};
+
 struct hfmm_plan {
   int device = 0;
   cudaStream_t stream = nullptr, stream2 = nullptr, stream_hi = nullptr;  // near field low, far chain high priority
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join_hi = nullptr;
+  cudaEvent_t ev_up = nullptr;   // far chain: M_l of every level up to date (virtual-rank exchange)
   std::string err;
   bool have_tree = false, have_plan = false;
   Tree tree;
   // dist
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  hfmm_vgroup *vg = nullptr;      // virtual ranks in one process (test mode, hfmm_set_dist_virtual)
+  std::vector<int64_t> pt_lo, pt_hi;  // every rank's owned sorted point range (y gather)
+  double2 *y_sorted = nullptr;    // y in sorted order (multi-rank gather)
   // points (sorted)
   double *px = nullptr, *py = nullptr, *pz = nullptr;
   int64_t *perm = nullptr;
@@ -195,11 +207,11 @@ static void free_levels(hfmm_plan *p) {
 
 static void free_points(hfmm_plan *p) {
   for (void *ptr : {(void *)p->px, (void *)p->py, (void *)p->pz, (void *)p->perm, (void *)p->q_in,
-                    (void *)p->q_sorted, (void *)p->y_out, (void *)p->y_near})
+                    (void *)p->q_sorted, (void *)p->y_out, (void *)p->y_near, (void *)p->y_sorted})
     if (ptr) cudaFree(ptr);
   p->px = p->py = p->pz = nullptr;
   p->perm = nullptr;
-  p->q_in = p->q_sorted = p->y_out = p->y_near = nullptr;
+  p->q_in = p->q_sorted = p->y_out = p->y_near = p->y_sorted = nullptr;
   p->have_tree = false;
 }
 
@@ -249,6 +261,7 @@ extern "C" int hfmm_create(hfmm_plan **out, int device) {
   CKC(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_join_hi, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&p->ev_up, cudaEventDisableTiming));
   for (auto &e : p->sev) CKC(cudaEventCreate(&e));
   const char *prof = std::getenv("HFMM_PROFILE_STAGES");
   p->profile = prof && prof[0] && prof[0] != '0';
@@ -308,7 +321,9 @@ extern "C" int hfmm_build_tree(hfmm_plan *p, int64_t n, const double *xyz, int d
   p->perm = dupload(t.perm);
   p->q_in = dalloc<double2>(n), p->q_sorted = dalloc<double2>(n);
   p->y_out = dalloc<double2>(n), p->y_near = dalloc<double2>(n);
-  if (!p->px || !p->py || !p->pz || !p->perm || !p->q_in || !p->q_sorted || !p->y_out || !p->y_near) {
+  if (p->nranks > 1) p->y_sorted = dalloc<double2>(n);
+  if (!p->px || !p->py || !p->pz || !p->perm || !p->q_in || !p->q_sorted || !p->y_out || !p->y_near ||
+      (p->nranks > 1 && !p->y_sorted)) {
     p->err = "hfmm_build_tree: device allocation failed";
     return HFMM_E_NOMEM;
   }
@@ -444,6 +459,8 @@ static void partition(hfmm_plan *p) {
     };
     p->own_pt0 = cutp(r);
     p->own_pt1 = cutp(r + 1);
+    p->pt_lo.assign(R, 0), p->pt_hi.assign(R, 0);
+    for (int q = 0; q < R; ++q) p->pt_lo[q] = cutp(q), p->pt_hi[q] = cutp(q + 1);
     return;
   }
   const LevelBoxes &BL = t.levels[p->L_f];
@@ -467,6 +484,8 @@ static void partition(hfmm_plan *p) {
   const LevelDev &Lf = p->lv[p->L_f];
   p->own_pt0 = BL.first[Lf.own0];
   p->own_pt1 = BL.first[Lf.own1];
+  p->pt_lo.assign(R, 0), p->pt_hi.assign(R, 0);
+  for (int q = 0; q < R; ++q) p->pt_lo[q] = BL.first[Lf.rlo[q]], p->pt_hi[q] = BL.first[Lf.rhi[q]];
 }
 
 extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double alpha, double tau,
@@ -913,7 +932,12 @@ static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
   return HFMM_OK;
 }
 
-static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool serial) {
+// The matvec in two phases around its one exchange step (M2L needs the M_l of off-rank partners):
+//   run_up    permute, near field (P2P, low-priority stream), S2M and M2M (far chain, high priority)
+//   run_down  M2L, L2L, L2T on the far chain; join; combine
+// run_matvec = run_up, all-gather of every active level's M (NCCL), run_down.  The virtual-rank
+// group runs the phases of all its plans with peer copies in between.
+static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool serial) {
   const Tree &t = p->tree;
   const int64_t n = t.n;
   const bool prof = p->profile;
@@ -972,10 +996,21 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, b
         }
       }
     }
-    for (int l = 2; l <= Lf; ++l) {
-      int rc = allgather_level(p, p->lv[l], s);
-      if (rc) return rc;
-    }
+  }
+  CK(cudaEventRecord(p->ev_up, p->stream_hi));
+  return HFMM_OK;
+}
+
+static int run_down(hfmm_plan *p, cudaStream_t s_user, bool sorted_out) {
+  const Tree &t = p->tree;
+  const int64_t n = t.n;
+  const bool prof = p->profile;
+  PointsDev pts{p->px, p->py, p->pz, p->q_sorted};
+  cudaStream_t s = p->stream_hi;
+  const TwiddleSet &tw = global_twiddles(p->device);
+  if (p->L_f >= 2) {
+    const int Lf = p->L_f, Ds = p->D_s;
+    LevelDev &F = p->lv[Ds];
     if (prof) cudaEventRecord(p->sev[2], s);
     for (int l = 2; l <= Lf; ++l) {  // M2L
       LevelDev &L = p->lv[l];
@@ -1024,18 +1059,42 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, b
   CK(cudaEventRecord(p->ev_join_hi, s));
   CK(cudaStreamWaitEvent(s_user, p->ev_join, 0));
   CK(cudaStreamWaitEvent(s_user, p->ev_join_hi, 0));
-  launch_combine(p->y_near, p->L_f >= 2 ? p->y_far : nullptr, p->perm, p->y_out, n, p->own_pt0, p->own_pt1, s_user);
+  // owned rows: into y_out in input order, or (multi-rank gather) into y_sorted in sorted order
+  if (sorted_out)
+    launch_combine(p->y_near, p->L_f >= 2 ? p->y_far : nullptr, nullptr, p->y_sorted, n, p->own_pt0, p->own_pt1,
+                   s_user);
+  else
+    launch_combine(p->y_near, p->L_f >= 2 ? p->y_far : nullptr, p->perm, p->y_out, n, p->own_pt0, p->own_pt1,
+                   s_user);
   if (prof) cudaEventRecord(p->sev[6], s_user);
   CK(cudaGetLastError());
   return HFMM_OK;
 }
 
+static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool serial, bool sorted_out) {
+  int rc = run_up(p, q_dev, s_user, serial);
+  if (rc) return rc;
+  for (int l = 2; l <= p->L_f; ++l) {
+    rc = allgather_level(p, p->lv[l], p->stream_hi);
+    if (rc) return rc;
+  }
+  return run_down(p, s_user, sorted_out);
+}
+
 static int gather_y(hfmm_plan *p, cudaStream_t s) {
   if (p->nranks <= 1) return HFMM_OK;
-  // y is in input order; each rank wrote the entries of its owned sorted range.  Reduce-sum
-  // would be wrong for a partition with zero-initialised gaps only if entries overlap (they
-  // do not), so an all-reduce (sum) of the zero-padded vector is exact.
-  CKN(ncclAllReduce(p->y_out, p->y_out, (size_t)p->tree.n * 2, ncclDouble, ncclSum, p->comm, s));
+  // each rank wrote y of its owned sorted range [pt_lo[r], pt_hi[r]) into y_sorted: all-gather
+  // of the (variable-size) ranges -- one broadcast per root, grouped -- then every rank
+  // unpermutes the whole vector (N x 16 B per rank on the wire instead of an all-reduce's 2x)
+  CKN(ncclGroupStart());
+  for (int r = 0; r < p->nranks; ++r) {
+    const size_t cnt = (size_t)(p->pt_hi[r] - p->pt_lo[r]) * 2;
+    if (!cnt) continue;
+    double *buf = (double *)(p->y_sorted + p->pt_lo[r]);
+    CKN(ncclBroadcast(buf, buf, cnt, ncclDouble, r, p->comm, s));
+  }
+  CKN(ncclGroupEnd());
+  launch_combine(p->y_sorted, nullptr, p->perm, p->y_out, p->tree.n, 0, p->tree.n, s);
   return HFMM_OK;
 }
 
@@ -1059,7 +1118,12 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
     CK(cudaMemcpyAsync(p->q_in, q, n * sizeof(double2), cudaMemcpyHostToDevice, s));
     qd = p->q_in;
   }
-  if (p->nranks > 1 || local) CK(cudaMemsetAsync(p->y_out, 0, n * sizeof(double2), s));
+  if (p->vg && !direct) {
+    p->err = "matvec: a virtual-rank plan runs through hfmm_vgroup_matvec";
+    return HFMM_E_STATE;
+  }
+  const bool gather = p->nranks > 1 && !local && !direct;
+  if (local || (p->nranks > 1 && direct)) CK(cudaMemsetAsync(p->y_out, 0, n * sizeof(double2), s));
   if (direct) {
     launch_permute_q(qd, p->perm, p->q_sorted, n, s);
     PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
@@ -1067,9 +1131,9 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
     launch_p2p_items(pu, p->dir_items, p->dir_nitems, P2P_DIAG, p->uscale, p->dummy_t, p->dummy_s, p->y_near, s);
     launch_combine(p->y_near, nullptr, p->perm, p->y_out, n, 0, n, s);
   } else {
-    int rc = run_matvec(p, qd, s, (mem & HFMM_SERIAL) != 0);
+    int rc = run_matvec(p, qd, s, (mem & HFMM_SERIAL) != 0, gather);
     if (rc) return rc;
-    if (!local) {
+    if (gather) {
       rc = gather_y(p, s);
       if (rc) return rc;
     }
@@ -1094,6 +1158,96 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
   }
   CK(cudaGetLastError());
   return HFMM_OK;
+}
+
+// ---- virtual ranks (test mode): R plans on one device, peer copies instead of NCCL ------------
+extern "C" int hfmm_vgroup_create(hfmm_vgroup **out, int nranks) {
+  if (!out || nranks < 1) return HFMM_E_ARG;
+  *out = new hfmm_vgroup();
+  (*out)->nranks = nranks;
+  (*out)->plans.assign(nranks, nullptr);
+  return HFMM_OK;
+}
+
+extern "C" void hfmm_vgroup_destroy(hfmm_vgroup *g) {
+  if (!g) return;
+  for (hfmm_plan *p : g->plans)
+    if (p) p->vg = nullptr;
+  delete g;
+}
+
+extern "C" int hfmm_set_dist_virtual(hfmm_plan *p, hfmm_vgroup *g, int rank) {
+  if (!p) return HFMM_E_ARG;
+  if (!g || rank < 0 || rank >= g->nranks || (g->plans[rank] && g->plans[rank] != p)) {
+    p->err = "hfmm_set_dist_virtual: bad group / rank (or rank already taken)";
+    return HFMM_E_ARG;
+  }
+  if (p->have_tree) {
+    p->err = "hfmm_set_dist_virtual: must be called before build_tree";
+    return HFMM_E_STATE;
+  }
+  if (p->comm) {
+    ncclCommDestroy(p->comm);
+    p->comm = nullptr;
+  }
+  p->rank = rank, p->nranks = g->nranks, p->vg = g;
+  g->plans[rank] = p;
+  return HFMM_OK;
+}
+
+extern "C" int hfmm_vgroup_matvec(hfmm_vgroup *g, const double *q, double *y, void *stream) {
+  // The multi-rank matvec of run_matvec + gather_y with every collective replaced by one
+  // cudaMemcpyAsync per peer block: (1) run_up on every rank; (2) for each active level, rank r
+  // copies every peer r' 's owned block of M_l (after r' 's event) -- the all-gather; (3)
+  // run_down on every rank (owned rows of y into its y_sorted); (4) rank r copies every peer's
+  // owned range of y_sorted -- the y all-gather -- and unpermutes into y + r n.
+  if (!g || !q || !y) return HFMM_E_ARG;
+  const int R = g->nranks;
+  for (hfmm_plan *p : g->plans)
+    if (!p || !p->have_plan || p->device != g->plans[0]->device || p->tree.n != g->plans[0]->tree.n ||
+        p->L_f != g->plans[0]->L_f)
+      return HFMM_E_STATE;
+  hfmm_plan *p0 = g->plans[0];
+  cudaSetDevice(p0->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : p0->stream;
+  const int64_t n = p0->tree.n;
+  for (hfmm_plan *p : g->plans) {
+    int rc = run_up(p, (const double2 *)q, s, false);
+    if (rc) return rc;
+  }
+  for (int r = 0; r < R; ++r) {
+    hfmm_plan *p = g->plans[r];
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr == r) continue;
+      hfmm_plan *src = g->plans[rr];
+      if (cudaStreamWaitEvent(p->stream_hi, src->ev_up, 0) != cudaSuccess) return HFMM_E_CUDA;
+      for (int l = 2; l <= p->L_f; ++l) {
+        LevelDev &L = p->lv[l], &S = src->lv[l];
+        const int64_t b0 = L.rlo[rr], b1 = L.rhi[rr];
+        if (b1 > b0 &&
+            cudaMemcpyAsync(L.M + b0 * L.K, S.M + b0 * S.K, (size_t)(b1 - b0) * L.K * sizeof(double2),
+                            cudaMemcpyDeviceToDevice, p->stream_hi) != cudaSuccess)
+          return HFMM_E_CUDA;
+      }
+    }
+  }
+  for (hfmm_plan *p : g->plans) {
+    int rc = run_down(p, s, true);
+    if (rc) return rc;
+  }
+  for (int r = 0; r < R; ++r) {   // everything below is ordered on s after every run_down
+    hfmm_plan *p = g->plans[r];
+    for (int rr = 0; rr < R; ++rr) {
+      const int64_t a = p->pt_lo[rr], b = p->pt_hi[rr];
+      if (rr == r || b <= a) continue;
+      if (cudaMemcpyAsync(p->y_sorted + a, g->plans[rr]->y_sorted + a, (size_t)(b - a) * sizeof(double2),
+                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return HFMM_E_CUDA;
+    }
+    launch_combine(p->y_sorted, nullptr, p->perm, (double2 *)y + (size_t)r * n, n, 0, n, s);
+  }
+  if (!stream && cudaStreamSynchronize(s) != cudaSuccess) return HFMM_E_CUDA;
+  return cudaGetLastError() == cudaSuccess ? HFMM_OK : HFMM_E_CUDA;
 }
 
 extern "C" int hfmm_matvec(hfmm_plan *p, const double *q, double *y, int mem, void *stream) {
@@ -1201,6 +1355,8 @@ extern "C" void hfmm_destroy(hfmm_plan *p) {
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->ev_join_hi) cudaEventDestroy(p->ev_join_hi);
+  if (p->ev_up) cudaEventDestroy(p->ev_up);
+  if (p->vg && p->rank < (int)p->vg->plans.size() && p->vg->plans[p->rank] == p) p->vg->plans[p->rank] = nullptr;
   if (p->stream_hi) cudaStreamDestroy(p->stream_hi);
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->stream2) cudaStreamDestroy(p->stream2);

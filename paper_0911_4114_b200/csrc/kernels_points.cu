@@ -633,7 +633,7 @@ __global__ void combine_kernel(const double2 *__restrict__ y_near, const double2
       a.x += b.x;
       a.y += b.y;
     }
-    y_out[perm[i]] = a;
+    y_out[perm ? perm[i] : i] = a;   // perm == nullptr: keep the sorted order
   }
 }
 

@@ -5,13 +5,20 @@
     the translation-only levels), so every kernel instantiation the C4 headline runs (the
     60 <-> 140 <-> 240 register passes, the 24 <-> 32 <-> 42x48 <-> 60 single-pass kernels, M2L
     on the 240 / 140 grids) is compared with the oracle stage by stage: M_l, I_l, L_l at every
-    level, y_near, y_far and y (relative L2 <= 1e-11), and y vs direct summation (<= eps).
+    level, y_near and y (relative L2 <= 1e-11), y_far (below), and y vs direct summation (<= eps).
 (b) every grid pair the C3 / C4 / C5 / C1HF plans instantiate, both directions, through the
     operator entry points (resample, fused M2M, fused L2L) vs oracle.resample (1e-13).
 (c) full-size C3 / C4 / C5: the library matvec (default flags, the path bench.py times) at 1,000
     sampled targets vs the oracle's target-subset references in tests/golden/subset_<cfg>.json
-    (written by tools/gen_subset_refs.py from oracle/ only): relative L2 <= 1e-11 for y, y_near
-    and y_far, and <= eps vs the stored direct sums; the integer plan equals the stored one.
+    (written by tools/gen_subset_refs.py from oracle/ only): relative L2 <= 1e-11 for y and
+    y_near, y_far below, and <= eps vs the stored direct sums; the integer plan equals the stored one.
+
+Tolerance of the far-field output y_far on its own: max(1e-11, F_max), F_max = the largest F_l of
+the active levels (R-9 / "Parity bar").  y_far is a sum of quadrature terms whose
+magnitudes exceed the result by the roundoff amplification of the transfer functions (the
+low-frequency breakdown), so two FP64 implementations that round differently agree on it
+only to about F_max (measured on C4: 1.0e-11 = 0.27 F_3 with F_3 = 3.8e-11).  The bar of the
+whole matvec y stays 1e-11 (BASELINE north_star): y_near dominates its norm.
 """
 import json
 import math
@@ -33,6 +40,11 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
+
+
+def far_tol(F_active):
+    """y_far on its own: max(1e-11, largest active F_l) (module docstring)."""
+    return max(PARITY, max(F_active))
 
 
 @pytest.fixture(scope="module")
@@ -91,7 +103,7 @@ def test_c4_small_stages(c4_small):
             assert err <= PARITY, ("MIL"[what], l, err)
     perm = g.debug(6)
     assert rel(g.debug(4)[: cfg.n], yn[perm]) <= PARITY
-    assert rel(g.debug(5)[: cfg.n], yf[perm]) <= PARITY
+    assert rel(g.debug(5)[: cfg.n], yf[perm]) <= far_tol(plan.levels[l].F for l in range(2, plan.L_f + 1))
 
 
 def test_c4_small_matvec(c4_small):
@@ -181,7 +193,8 @@ def test_fullsize_subset_parity(hf, name):
     p_y, p_n, p_f = rel(y[t], yn_o + yf_o), rel(yn_g, yn_o), rel(yf_g, yf_o)
     print(f"{name}: parity y {p_y:.2e} y_near {p_n:.2e} y_far {p_f:.2e} (max F_l "
           f"{max(v['F'] for v in d['levels'].values() if v['active']):.1e})")
-    assert p_y <= PARITY and p_n <= PARITY and p_f <= PARITY
+    assert p_y <= PARITY and p_n <= PARITY
+    assert p_f <= far_tol(v["F"] for v in d["levels"].values() if v["active"])
     if yd is not None:
         assert rel(y[t], yd) <= cfg.eps
     g.close()
