@@ -19,6 +19,13 @@ Representations
   "half": array [N_theta][N_phi/2] (theta over [0, 2pi), phi over [0, pi)) --
           Alg. 1's output domain, used by the FMM passes (reading R-7).
 Every resample here is an explicit dense matrix built from the definition.
+
+P:749      "A slightly more efficient algorithm uses the symmetry eqn:FourierSphereSym rather than
+           eqn:NumSphereSym": resample_coeff_sym does the same operator in
+           the phi-coefficient domain -- phi-DFT of the rows n <= N_theta/2, the theta sequence of
+           each phi-frequency m extended by f~_{n,m} = (-1)^m f~_{-n,m} (eqn:FourierSphereSym,
+           P:277-280, i.e. c_m(theta_{N_theta - n}) = (-1)^m c_m(theta_n)), resampled in theta,
+           inverse phi-DFT of the rows n' <= N'_theta/2.
 """
 from __future__ import annotations
 
@@ -194,3 +201,31 @@ def resample_half_batch(F: np.ndarray, nph: int, nth_p: int, nph_p: int) -> np.n
     return np.where(lowp[None, :, None],
                     rows2[:, srcp, : nph_p // 2],
                     rows2[:, srcp, nph_p // 2:])
+
+
+def resample_coeff_sym(F: np.ndarray, nph: int, nth_p: int, nph_p: int) -> np.ndarray:
+    """NEXT 4 (eqn:FourierSphereSym P:277-280): half-stored [B][N_theta][N_phi/2] ->
+    [B][N'_theta][N'_phi/2], the same operator as resample_half_batch, computed in the
+    phi-coefficient domain (module docstring).  Dense DFT matrices, literal steps."""
+    F = np.asarray(F, dtype=np.complex128)
+    B, nth, h = F.shape
+    assert h == nph // 2
+    n_up = np.arange(nth // 2 + 1)
+    rows = np.concatenate([F[:, n_up, :], F[:, (nth - n_up) % nth, :]], axis=2)      # full rows n <= N_theta/2
+    m = band(nph, nph_p)                                                            # kept phi band
+    fwd = np.exp(-2j * math.pi * (np.outer(np.arange(nph), m) % nph) / nph) / nph    # [j, m]
+    C = rows @ fwd                                                                  # c_m(theta_n), n <= N_theta/2
+    # theta sequence of every m over n < N_theta: c_m(theta_{N_theta - n}) = (-1)^m c_m(theta_n)
+    n_all = np.arange(nth)
+    lower = n_all <= nth // 2
+    src = np.where(lower, n_all, nth - n_all)
+    sign = np.where(lower[:, None], 1.0, ((-1.0) ** np.abs(m))[None, :])            # [n, m]
+    Cfull = C[:, src, :] * sign[None]                                               # [B, nth, m]
+    Cp = np.einsum("pn,bnm->bpm", resample_matrix(nth, nth_p), Cfull)               # [B, nth', m]
+    n_up2 = np.arange(nth_p // 2 + 1)
+    inv = np.exp(2j * math.pi * (np.outer(m, np.arange(nph_p)) % nph_p) / nph_p)     # [m, t]
+    rows2 = Cp[:, n_up2, :] @ inv                                                   # full rows n' <= N'_theta/2
+    n_allp = np.arange(nth_p)
+    lowp = n_allp <= nth_p // 2
+    srcp = np.where(lowp, n_allp, nth_p - n_allp)
+    return np.where(lowp[None, :, None], rows2[:, srcp, : nph_p // 2], rows2[:, srcp, nph_p // 2:])

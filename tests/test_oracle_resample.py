@@ -103,3 +103,52 @@ def test_interpolate_data_profile_golden():
     assert steps["A_theta"] == (int(vals["cols"]), nthp)
     assert steps["W2"] == [calN] * int(vals["rows_out"])
     assert steps["A_phi"] == out_lens and len(out) == int(vals["rows_out"])
+
+
+# ---- NEXT 4: coefficient-domain symmetric resampling (eqn:FourierSphereSym P:277-280) ----
+def full_doubled_grid(nth, nph, coeffs):
+    """f(theta_n, phi_m) on the whole doubled grid n < N_theta, m < N_phi (no half storage)."""
+    th = 2 * math.pi * np.arange(nth) / nth
+    ph = 2 * math.pi * np.arange(nph) / nph
+    TH, PH = np.meshgrid(th, ph, indexing="ij")
+    s = shat(TH, PH)
+    f = np.zeros(TH.shape, dtype=complex)
+    for (i, j, k), c in coeffs.items():
+        f += c * s[..., 0] ** i * s[..., 1] ** j * s[..., 2] ** k
+    return f
+
+
+@pytest.mark.parametrize("nth,nph", [(16, 16), (14, 20), (24, 12)])
+def test_fourier_sphere_symmetry_holds(nth, nph):
+    """eqn:FourierSphereSym: the 2-D Fourier coefficients of a function of s sampled on
+    the doubled sphere satisfy f~_{n,m} = (-1)^m f~_{-n,m} (to rounding), for every (n, m)."""
+    f = full_doubled_grid(nth, nph, COEFFS)
+    Ft = np.fft.fft2(f) / (nth * nph)                        # f~[n, m], n mod N_theta, m mod N_phi
+    n = np.arange(nth)[:, None]
+    m = np.arange(nph)[None, :]
+    msigned = np.where(m <= nph // 2, m, m - nph)
+    lhs = Ft
+    rhs = ((-1.0) ** np.abs(msigned)) * Ft[(-n) % nth, m]
+    assert np.max(np.abs(lhs - rhs)) < 1e-14 * np.max(np.abs(Ft)) * 10
+    # and it is not vacuous: both parities carry weight
+    assert np.max(np.abs(Ft[:, 1::2])) > 1e-3 and np.max(np.abs(Ft[:, 0::2])) > 1e-3
+
+
+@pytest.mark.parametrize("src,dst", [((16, 16), (32, 32)), ((32, 32), (16, 16)), ((24, 24), (32, 32)),
+                                     ((32, 32), (42, 48)), ((42, 48), (60, 60)), ((60, 60), (42, 48)),
+                                     ((54, 56), (40, 40)), ((18, 20), (30, 28))])
+def test_coeff_sym_equals_five_step(src, dst):
+    """NEXT 4 is the same operator as the 5-step procedure: random data."""
+    from oracle.resample import resample_coeff_sym
+    rng = np.random.default_rng(src[0] + 100 * dst[0])
+    F = rng.standard_normal((3, src[0], src[1] // 2)) + 1j * rng.standard_normal((3, src[0], src[1] // 2))
+    a = resample_coeff_sym(F, src[1], dst[0], dst[1])
+    b = resample_half_batch(F, src[1], dst[0], dst[1])
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(b))
+
+
+def test_coeff_sym_exact_on_bandlimited():
+    from oracle.resample import resample_coeff_sym
+    f = sphere_poly(12, 12, COEFFS)
+    g = resample_coeff_sym(f[None], 12, 20, 24)[0]
+    assert np.max(np.abs(g - sphere_poly(20, 24, COEFFS))) < 1e-13
