@@ -117,6 +117,8 @@ typedef struct {
   int64_t owned_points;    /* points whose y this rank computes                              */
   int source_level;        /* D_s: level of S2M / L2T (R-14), -1 if no far field             */
   int launches;            /* libhfmm kernel launches per matvec (this rank)                 */
+  int next4_passes;        /* M2M / L2L level passes run by the NEXT 4 coefficient-domain
+                              symmetric kernels (HFMM_NEXT4=1 in the environment), else 0     */
 } hfmm_info;
 
 /* Create a plan on CUDA device `device` (-1: the current device).  *out receives the plan. */
@@ -138,6 +140,14 @@ int hfmm_nccl_unique_id(void *out_128b);
  * (input order), y DEVICE pointer [nranks][n] (rank r's full output vector at y + r n); enqueued
  * on `stream` (NULL: rank 0's plan stream, synchronised before return).  A plan bound to a group
  * returns HFMM_E_STATE from hfmm_matvec.  Destroy the group after (or before) its plans. */
+/* NEXT 4 (coefficient-domain symmetric resampling, eqn:FourierSphereSym P:277-280):
+ * process-wide switch for the single-pass M2M / L2L / resample kernels of the grid pairs it is
+ * instantiated for (C2 B8-B32, the translation-only levels of C3 / C4 / C5); other pairs keep the
+ * 5-step kernels.  Initial value from HFMM_NEXT4 in the environment (default 0).  Set it before
+ * hfmm_precompute (hfmm_info.next4_passes / launches are counted there).  Returns the previous
+ * value. */
+int hfmm_set_next4(int on);
+
 typedef struct hfmm_vgroup hfmm_vgroup;
 int hfmm_vgroup_create(hfmm_vgroup **out, int nranks);
 int hfmm_set_dist_virtual(hfmm_plan *p, hfmm_vgroup *g, int rank);

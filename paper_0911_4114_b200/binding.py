@@ -38,6 +38,7 @@ EXPORTED = [
     "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
     "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free", "hfmm_m2l_op_kind", "hfmm_ragged_rows",
     "hfmm_vgroup_create", "hfmm_set_dist_virtual", "hfmm_vgroup_matvec", "hfmm_vgroup_destroy",
+    "hfmm_set_next4",
 ]
 
 
@@ -55,7 +56,7 @@ class Info(C.Structure):
                 ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("p2p_sym_pairs", C.c_int64),
                 ("s2m_evals", C.c_int64),
                 ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64),
-                ("source_level", C.c_int), ("launches", C.c_int)]
+                ("source_level", C.c_int), ("launches", C.c_int), ("next4_passes", C.c_int)]
 
 
 class HFMMError(RuntimeError):
@@ -107,6 +108,7 @@ def load() -> C.CDLL:
         "hfmm_set_dist_virtual": (ci, [vp, vp, ci]),
         "hfmm_vgroup_matvec": (ci, [vp, vp, vp, vp]),
         "hfmm_vgroup_destroy": (None, [vp]),
+        "hfmm_set_next4": (ci, [ci]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -136,6 +138,12 @@ def level_quadrature(kappa: float, a: float, eps_level: float, alpha: float = 0.
     if rc < 0:
         raise HFMMError(rc, "hfmm_level_quadrature failed")
     return ell.value, nth.value, nph.value, list(rag[: nth.value // 2 + 1])
+
+
+def set_next4(on: bool) -> bool:
+    """NEXT 4 coefficient-domain symmetric resampling on / off (process-wide; include/hfmm.h
+    hfmm_set_next4).  Returns the previous setting."""
+    return bool(load().hfmm_set_next4(1 if on else 0))
 
 
 def rep_grid(kappa: float, a: float, eps: float):
@@ -289,7 +297,8 @@ class HFMM:
                     eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
                     p2p_sym_pairs=inf.p2p_sym_pairs,
                     s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points,
-                    source_level=(None if inf.source_level < 0 else inf.source_level), launches=inf.launches)
+                    source_level=(None if inf.source_level < 0 else inf.source_level), launches=inf.launches,
+                    next4_passes=inf.next4_passes)
 
     def stage_times(self):
         out = (C.c_double * 8)()

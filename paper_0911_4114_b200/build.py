@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhfmm.so")
-SOURCES = ["hfmm.cu", "kernels_points.cu", "kernels_fft.cu", "kernels_m2l.cu", "kernels_ragged.cu", "kernels_misc.cu",
+SOURCES = ["hfmm.cu", "kernels_points.cu", "kernels_fft.cu", "kernels_m2l.cu", "kernels_ragged.cu", "kernels_misc.cu", "kernels_sym.cu",
            "host_plan.cpp", "host_specfun.cpp", "host_tree.cpp"]
 
 
@@ -40,7 +40,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "hfmm_impl.h"),
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "hfmm_impl.h"), os.path.join(CSRC, "fft_regs.cuh"),
                                                       os.path.join(ROOT, "include", "hfmm.h")]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 

@@ -888,20 +888,25 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
   in.source_level = p->D_s;
   {  // kernel launches of one matvec (run_matvec): permute, P2P kinds, far chain, combine
-    int nl = 2;
+    int nl = 2, n4 = 0;
     for (int k = 0; k < 3; ++k) nl += p->p2p_nitems[k] > 0 ? 1 : 0;
     if (p->L_f >= 2) {
       for (int l = p->D_s; l > 2; --l) {          // M2M: rows + cols pass per level (or one pass)
         const LevelDev &C = p->lv[l], &P = p->lv[l - 1];
-        nl += (!C.ragged && !P.ragged && box2_up_applies(C.nth, C.nph, P.nth, P.nph)) ? 1 : 2;
+        const bool sym = !C.ragged && !P.ragged && sym2_up_applies(C.nth, C.nph, P.nth, P.nph);
+        n4 += sym ? 1 : 0;
+        nl += (sym || (!C.ragged && !P.ragged && box2_up_applies(C.nth, C.nph, P.nth, P.nph))) ? 1 : 2;
       }
       for (int l = 2; l < p->D_s; ++l) {          // L2L: cols + rows pass per level (or one pass)
         const LevelDev &P = p->lv[l], &C = p->lv[l + 1];
-        nl += (!C.ragged && !P.ragged && box2_down_applies(P.nth, P.nph, C.nth, C.nph)) ? 1 : 2;
+        const bool sym = !C.ragged && !P.ragged && sym2_down_applies(P.nth, P.nph, C.nth, C.nph);
+        n4 += sym ? 1 : 0;
+        nl += (sym || (!C.ragged && !P.ragged && box2_down_applies(P.nth, P.nph, C.nth, C.nph))) ? 1 : 2;
       }
       nl += 2 + (p->L_f - 1);                      // S2M, L2T, M2L per active level
     }
     in.launches = nl;
+    in.next4_passes = n4;
   }
   in.owned_points = p->own_pt1 - p->own_pt0;
   p->have_plan = true;

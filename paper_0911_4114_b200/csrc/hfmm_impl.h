@@ -188,6 +188,18 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
 // (cbeg == nullptr: one box per item, no shift).  Returns false when not applicable.
 bool box2_up_applies(int nth, int nph, int nth2, int nph2);
 bool box2_down_applies(int nth, int nph, int nth2, int nph2);
+// NEXT 4 coefficient-domain symmetric resampling (kernels_sym.cu; opt-in HFMM_NEXT4=1): same
+// arguments and result as launch_box2_up / launch_box2_down; false when not enabled or the grid
+// pair has no instantiation.
+bool next4_enabled();
+bool sym2_up_applies(int nth, int nph, int nth2, int nph2);
+bool sym2_down_applies(int nth, int nph, int nth2, int nph2);
+bool launch_sym2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *cbeg,
+                    int64_t cbase, const int8_t *oct, const double2 *shift, double2 *out, const TwiddleSet &tw,
+                    cudaStream_t s);
+bool launch_sym2_down(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *par,
+                      const int8_t *oct, const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
+                      cudaStream_t s);
 bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *par,
                       const int8_t *oct, const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
                       cudaStream_t s);

@@ -1249,6 +1249,7 @@ bool box2_down_applies(int nth, int nph, int nth2, int nph2) {
 bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *par,
                       const int8_t *oct, const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
                       cudaStream_t s) {
+  if (launch_sym2_down(in, nitem, nth, nph, nth2, nph2, par, oct, shift, add, out, tw, s)) return true;
   if (!box2_down_applies(nth, nph, nth2, nph2)) return false;
   switch (gkey(nth, nph, nth2, nph2)) {
 #define B2D(a, b, c, d, R1, R2, R3, R4, C1, C2, C3, C4)                                                      \
@@ -1271,6 +1272,7 @@ bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nt
 bool launch_box2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *cbeg,
                     int64_t cbase, const int8_t *oct, const double2 *shift, double2 *out, const TwiddleSet &tw,
                     cudaStream_t s) {
+  if (launch_sym2_up(in, nitem, nth, nph, nth2, nph2, cbeg, cbase, oct, shift, out, tw, s)) return true;
   if (!box2_up_applies(nth, nph, nth2, nph2)) return false;
   switch (gkey(nth, nph, nth2, nph2)) {
 #define B2U(a, b, c, d, R1, R2, R3, R4, C1, C2, C3, C4)                                                      \
