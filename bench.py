@@ -248,6 +248,30 @@ def golden_parity(name, y, info):
     return out
 
 
+def c1_breakdown():
+    """P:833 low-frequency breakdown demonstration on C1 (SURVEY D-1): the policy run (no admissible
+    level: the direct sum) vs every level forced active (HFMM_FORCE_ALL_LEVELS), errors vs the GPU
+    direct sum (hfmm_direct) next to each level's roundoff amplification F_l."""
+    import torch
+    import paper_0911_4114_b200 as hf
+    from workloads import CONFIGS, points_and_charges
+    cfg = CONFIGS["C1"]
+    x, q = points_and_charges(cfg)
+    qd = torch.from_numpy(q).cuda()
+    out = {"eps": cfg.eps}
+    for name, flags in (("policy", 0), ("forced", hf.HFMM_FORCE_ALL_LEVELS)):
+        g = hf.HFMM(0)
+        g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+        g.precompute(cfg.kappa, cfg.eps, cfg.alpha, flags=flags)
+        y = g.matvec(qd)
+        yd = g.direct(qd)
+        info = g.info()
+        out[name] = {"L_f": info["L_f"], "F": {lv["level"]: lv["F"] for lv in info["levels"] if lv["active"]},
+                     "err_vs_direct": float(torch.linalg.norm(y - yd) / torch.linalg.norm(yd))}
+        g.close()
+    return out
+
+
 def hbm_peak():
     """Measured HBM copy bandwidth (GB/s) from MEASURED_PEAKS.json, else the guide's fallback."""
     try:
@@ -628,6 +652,8 @@ def main():
             tau = CONFIGS[base].eps / 10 if name.endswith("_acc") else 0.0
             oc[name] = bench_matvec_config(CONFIGS[base], args.warmup, max(3, args.steps // 2), tau=tau, golden=name)
         line["other_configs"] = oc
+    if world == 1 and args.extra:
+        line["C1_breakdown"] = c1_breakdown()
     if world == 1 and args.ops:
         line["operators"] = bench_operators([int(b) for b in args.ops.split(",")], fp64_peak_tflops=peak_tflops)
     if rank == 0:

@@ -117,6 +117,8 @@ typedef struct {
   int64_t owned_points;    /* points whose y this rank computes                              */
   int source_level;        /* D_s: level of S2M / L2T (R-14), -1 if no far field             */
   int launches;            /* libhfmm kernel launches per matvec (this rank)                 */
+  int p2p_tile;            /* targets per P2P work item (128 threads x 3 or 4 targets each: 4
+                              unless the items would fill fewer than ~10 waves of the GPU)     */
   int next4_passes;        /* M2M / L2L level passes run by the NEXT 4 coefficient-domain
                               symmetric kernels (HFMM_NEXT4=1 in the environment), else 0     */
 } hfmm_info;

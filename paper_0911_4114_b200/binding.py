@@ -56,7 +56,7 @@ class Info(C.Structure):
                 ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("p2p_sym_pairs", C.c_int64),
                 ("s2m_evals", C.c_int64),
                 ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64),
-                ("source_level", C.c_int), ("launches", C.c_int), ("next4_passes", C.c_int)]
+                ("source_level", C.c_int), ("launches", C.c_int), ("p2p_tile", C.c_int), ("next4_passes", C.c_int)]
 
 
 class HFMMError(RuntimeError):
@@ -298,7 +298,7 @@ class HFMM:
                     p2p_sym_pairs=inf.p2p_sym_pairs,
                     s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points,
                     source_level=(None if inf.source_level < 0 else inf.source_level), launches=inf.launches,
-                    next4_passes=inf.next4_passes)
+                    p2p_tile=inf.p2p_tile, next4_passes=inf.next4_passes)
 
     def stage_times(self):
         out = (C.c_double * 8)()

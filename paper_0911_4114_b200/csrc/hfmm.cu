@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX: named host ranges per pass (no-op without a tool)
 #include "hfmm_impl.h"
 #include "../../include/hfmm.h"
 
@@ -144,6 +145,7 @@ struct hfmm_plan {
   int64_t dir_nitems = 0;
   double *ux = nullptr, *uy = nullptr, *uz = nullptr;
   double uscale = 0;               // kappa TAB_STEPS / (2 pi)
+  int p2p_pt = 4;                  // targets per thread of the P2P kernels (tile = 128 x p2p_pt)
   int64_t p2p_sym_pairs = 0;
   double dummy_t[3] = {0, 0, 0}, dummy_s[3] = {0, 0, 0};
   double2 *tmp = nullptr;
@@ -766,11 +768,12 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       ux[i] = t.xs[i] * p->uscale, uy[i] = t.ys[i] * p->uscale, uz[i] = t.zs[i] * p->uscale;
     p->ux = dupload(ux), p->uy = dupload(uy), p->uz = dupload(uz);
     // Owned target ranges: owned near-level boxes (far field), or the rank's point range of the
-    // root (no far field).  Every target tile (<= P2P_TILE points of one box) gets
+    // root (no far field).  Every target tile (<= `tile` points of one box) gets
     //   DIAG (tile, tile);  SYM (tile, later tile of the same box);
     //   SYM (tile, owned neighbour box beta > alpha);  ORD (tile, neighbour range owned elsewhere).
     std::vector<int64_t> it[3];
     int64_t pairs = 0, sym_pairs = 0;
+    int64_t tile = (int64_t)P2P_TPB_HOST * 4;   // targets per item: 128 threads x PT targets
     auto add = [&](int kind, int64_t t0, int64_t t1, int64_t s0, int64_t s1) {
       if (t1 <= t0 || s1 <= s0) return;
       it[kind].insert(it[kind].end(), {t0, t1, s0, s1});
@@ -778,14 +781,17 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     auto own_box = [&](int64_t A0, int64_t A1, const std::vector<std::pair<int64_t, int64_t>> &others_owned,
                        const std::vector<std::pair<int64_t, int64_t>> &others_foreign) {
       // targets [A0, A1) of one owned box; others_* = neighbour ranges (sym: only beta > alpha)
-      for (int64_t t0 = A0; t0 < A1; t0 += P2P_TILE) {
-        const int64_t t1 = std::min(t0 + P2P_TILE, A1);
+      for (int64_t t0 = A0; t0 < A1; t0 += tile) {
+        const int64_t t1 = std::min(t0 + tile, A1);
         add(P2P_DIAG, t0, t1, t0, t1);
-        for (int64_t u0 = t1; u0 < A1; u0 += P2P_TILE) add(P2P_SYM, t0, t1, u0, std::min(u0 + P2P_TILE, A1));
+        for (int64_t u0 = t1; u0 < A1; u0 += tile) add(P2P_SYM, t0, t1, u0, std::min(u0 + tile, A1));
         for (auto &r : others_owned) add(P2P_SYM, t0, t1, r.first, r.second);
         for (auto &r : others_foreign) add(P2P_ORD, t0, t1, r.first, r.second);
       }
     };
+    auto build_items = [&]() {
+    for (auto &v : it) v.clear();
+    pairs = 0;
     if (p->L_f >= 2) {
       const int64_t lo = p->lv[p->L_f].own0, hi = p->lv[p->L_f].own1;
       for (int64_t b = lo; b < hi; ++b) {
@@ -815,6 +821,23 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       own_box(A0, A1, {}, fo);
       pairs = (A1 - A0) * (n - 1);
     }
+    };
+    // Per-plan tile (load balance): 4 targets per thread (512-point tiles, 3 CTAs / SM) unless
+    // that leaves fewer than ~10 waves of items over the GPU, then 3 per thread (384-point tiles,
+    // 4 CTAs / SM): the tail of a short grid costs more than the slightly lower per-item rate
+    // (C3: 11% faster; C4 / C5 keep 512, same-box A/B profiles/r01/p2p_occupancy_ab_r26.txt)
+    p->p2p_pt = 4;
+    build_items();
+    {
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+      const int64_t nit = (int64_t)(it[0].size() + it[1].size() + it[2].size()) / 4;
+      if (nit < 10 * 3 * (int64_t)nsm) {
+        p->p2p_pt = 3;
+        tile = (int64_t)P2P_TPB_HOST * 3;
+        build_items();
+      }
+    }
     // longest items first (LPT order against the tail of the grid)
     for (int k = 0; k < 3; ++k) {
       const int64_t m = (int64_t)it[k].size() / 4;
@@ -838,7 +861,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     // hfmm_direct: every target tile against all points (self pair masked)
     {
       std::vector<int64_t> d;
-      for (int64_t t0 = 0; t0 < t.n; t0 += P2P_TILE) d.insert(d.end(), {t0, std::min(t0 + P2P_TILE, t.n), 0, t.n});
+      for (int64_t t0 = 0; t0 < t.n; t0 += tile) d.insert(d.end(), {t0, std::min(t0 + tile, t.n), 0, t.n});
       p->dir_items = dupload(d);
       p->dir_nitems = (int64_t)d.size() / 4;
     }
@@ -906,6 +929,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       nl += 2 + (p->L_f - 1);                      // S2M, L2T, M2L per active level
     }
     in.launches = nl;
+    in.p2p_tile = P2P_TPB_HOST * p->p2p_pt;
     in.next4_passes = n4;
   }
   in.owned_points = p->own_pt1 - p->own_pt0;
@@ -923,8 +947,15 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
 }
 
 // ---- the matvec ------------------------------------------------------------------------------
+// NVTX range for the launches of one pass (scoped; visible to ncu --nvtx / nsys)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
   if (p->nranks <= 1) return HFMM_OK;
+  NvtxRange nv("hfmm:allgather M_l");
   // all-gather of M_l over variable-size Morton ranges: one broadcast per root, grouped
   CKN(ncclGroupStart());
   for (int r = 0; r < p->nranks; ++r) {
@@ -943,6 +974,7 @@ static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
 // run_matvec = run_up, all-gather of every active level's M (NCCL), run_down.  The virtual-rank
 // group runs the phases of all its plans with peer copies in between.
 static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool serial) {
+  NvtxRange nv_up("hfmm:up (permute, P2P, S2M, M2M)");
   const Tree &t = p->tree;
   const int64_t n = t.n;
   const bool prof = p->profile;
@@ -956,11 +988,11 @@ static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool 
   if (prof) cudaEventRecord(p->sev[7], p->stream2);
   CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), p->stream2));
   {
+    NvtxRange nv("hfmm:P2P");
     PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
     for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD})
       launch_p2p_items(pu, p->p2p_items[k], p->p2p_nitems[k], (k == P2P_DIAG && HFMM_P2P_DSYM) ? P2P_DSYM : k,
-                       p->uscale, p->dummy_t, p->dummy_s, p->y_near,
-                       p->stream2);
+                       p->uscale, p->dummy_t, p->dummy_s, p->y_near, p->stream2, p->p2p_pt);
   }
   if (prof) cudaEventRecord(p->sev[8], p->stream2);
   CK(cudaEventRecord(p->ev_join, p->stream2));
@@ -1007,6 +1039,7 @@ static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool 
 }
 
 static int run_down(hfmm_plan *p, cudaStream_t s_user, bool sorted_out) {
+  NvtxRange nv_down("hfmm:down (M2L, L2L, L2T, combine)");
   const Tree &t = p->tree;
   const int64_t n = t.n;
   const bool prof = p->profile;
@@ -1018,6 +1051,7 @@ static int run_down(hfmm_plan *p, cudaStream_t s_user, bool sorted_out) {
     LevelDev &F = p->lv[Ds];
     if (prof) cudaEventRecord(p->sev[2], s);
     for (int l = 2; l <= Lf; ++l) {  // M2L
+      NvtxRange nv("hfmm:M2L");
       LevelDev &L = p->lv[l];
       m2l_group_apply(L.m2lg, L.T, L.perm, L.M, L.I, s);
     }
@@ -1088,6 +1122,7 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, b
 
 static int gather_y(hfmm_plan *p, cudaStream_t s) {
   if (p->nranks <= 1) return HFMM_OK;
+  NvtxRange nv("hfmm:allgather y");
   // each rank wrote y of its owned sorted range [pt_lo[r], pt_hi[r]) into y_sorted: all-gather
   // of the (variable-size) ranges -- one broadcast per root, grouped -- then every rank
   // unpermutes the whole vector (N x 16 B per rank on the wire instead of an all-reduce's 2x)
@@ -1133,7 +1168,8 @@ static int matvec_common(hfmm_plan *p, const double *q, double *y, int mem, void
     launch_permute_q(qd, p->perm, p->q_sorted, n, s);
     PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
     CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), s));
-    launch_p2p_items(pu, p->dir_items, p->dir_nitems, P2P_DIAG, p->uscale, p->dummy_t, p->dummy_s, p->y_near, s);
+    launch_p2p_items(pu, p->dir_items, p->dir_nitems, P2P_DIAG, p->uscale, p->dummy_t, p->dummy_s, p->y_near, s,
+                     p->p2p_pt);
     launch_combine(p->y_near, nullptr, p->perm, p->y_out, n, 0, n, s);
   } else {
     int rc = run_matvec(p, qd, s, (mem & HFMM_SERIAL) != 0, gather);

@@ -109,17 +109,13 @@ struct PointsU {
   const double2 *q;
 };
 #ifndef HFMM_P2P_MINB
-#define HFMM_P2P_MINB 2  // resident CTAs per SM requested from ptxas (register budget)
-#endif
-#ifndef HFMM_P2P_T
-#define HFMM_P2P_T 4     // targets per thread in the P2P kernels (A/B: 2 -> 4 saves ~3%)
+#define HFMM_P2P_MINB 2  // resident CTAs per SM requested from ptxas for 4 targets / thread
 #endif
 #ifndef HFMM_P2P_TPB
 #define HFMM_P2P_TPB 128  // threads per P2P CTA
 #endif
-constexpr int P2P_T = HFMM_P2P_T;
 constexpr int P2P_THREADS = HFMM_P2P_TPB;
-constexpr int64_t P2P_TILE = (int64_t)HFMM_P2P_TPB * HFMM_P2P_T;  // targets per P2P work item
+constexpr int P2P_TPB_HOST = HFMM_P2P_TPB;  // work-item tile = P2P_TPB_HOST x targets per thread (3 or 4)
 #ifndef HFMM_TAB_STEPS
 #define HFMM_TAB_STEPS 2048
 #endif
@@ -128,14 +124,14 @@ enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2, P2P_DSYM = 3 };
 #ifndef HFMM_P2P_DSYM
 #define HFMM_P2P_DSYM 1  // matvec diagonal tiles with the symmetric kernel (each unordered pair once)
 #endif
-// P2P work items, int64 [nitems][4] = (t0, t1, s0, s1): targets [t0, t1) (<= P2P_TILE), sources
+// P2P work items, int64 [nitems][4] = (t0, t1, s0, s1): targets [t0, t1) (<= 128 x 3 or 4), sources
 // [s0, s1).  P2P_SYM: disjoint ranges, rows and columns (each unordered pair once);
 // P2P_DIAG: rows only, self pair masked (sources contain the targets); P2P_ORD: rows only;
 // P2P_DSYM (launch kind of the matvec's diagonal tiles, s-range == t-range): symmetric, pairs once.
 // Adds scale * sum into y_near (zeroed beforehand); scale = kappa TAB_STEPS / (2 pi).
 // dummy_t / dummy_s (scaled units): far positions used to pad partial symmetric tiles.
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
-                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s);
+                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt);
 
 // S2M: M[b][k] = sum_j q_j e^{i kappa s_k.(x_j - c_b)}; ks = kappa s / h (table steps)
 void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const double *cy,

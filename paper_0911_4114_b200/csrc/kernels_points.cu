@@ -92,7 +92,8 @@ __device__ __forceinline__ double rsqrt_fast(double r2) {
 //             registers) and G q_i to y_j (columns: systolic warp reduction, below)
 // ---------------------------------------------------------------------------------------------
 constexpr int P2P_TPB = P2P_THREADS;
-constexpr int PT = P2P_T;  // targets per thread (tile = PT * P2P_TPB)
+// PT = targets per thread (tile = PT * P2P_TPB), MINB = resident CTAs per SM asked of ptxas;
+// instantiated as (4, HFMM_P2P_MINB) and (3, 4) -- the plan picks one per matvec (hfmm.cu)
 
 __device__ __forceinline__ double2 green_u(double tx, double ty, double tz, double xs, double ys, double zs,
                                            const double2 *tab) {
@@ -103,8 +104,8 @@ __device__ __forceinline__ double2 green_u(double tx, double ty, double tz, doub
   return make_double2(e.x * ri, e.y * ri);
 }
 
-template <bool DIAG>
-__global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU pts,
+template <bool DIAG, int PT, int MINB>
+__global__ void __launch_bounds__(P2P_TPB, MINB) p2p_ord_kernel(PointsU pts,
                                                                         const int64_t *__restrict__ items,
                                                                         double scale, double2 *__restrict__ y_near) {
   __shared__ double2 tab[TAB];
@@ -162,12 +163,12 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_ord_kernel(PointsU
 // t - 1, so after 32 steps lane t holds the warp sum of source t (2 shuffles per step instead of
 // a 5-level butterfly per source); the 4 warps combine in shared memory, one atomic per source.
 // Each source loaded from shared memory serves PT targets of the lane.
-// DS (diagonal tile, targets == sources, <= P2P_TILE points): each unordered pair once -- 32-point
+// DS (diagonal tile, targets == sources, <= PT x P2P_TPB points): each unordered pair once -- 32-point
 // block pairs (target block tb = warp + (P2P_TPB / 32) p, source block sb) with tb < sb in full, tb == sb for half
 // of the systolic rotation (steps 1..15 and lanes < 16 of step 16; step 0 is the excluded self pair,
 // P:90), tb > sb skipped (warp-uniform branches).
-template <bool DS>
-__global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU pts,
+template <bool DS, int PT, int MINB>
+__global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
                                                                         const int64_t *__restrict__ items,
                                                                         double scale, double3 dummy_t,
                                                                         double3 dummy_s,
@@ -253,18 +254,27 @@ __global__ void __launch_bounds__(P2P_TPB, HFMM_P2P_MINB) p2p_sym_kernel(PointsU
   }
 }
 
-void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
-                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s) {
-  if (nitems <= 0) return;
+template <int PT, int MINB>
+static void launch_p2p_items_t(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
+                               const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s) {
   if (kind == P2P_SYM || kind == P2P_DSYM) {
-    auto kern = kind == P2P_SYM ? p2p_sym_kernel<false> : p2p_sym_kernel<true>;
+    auto kern = kind == P2P_SYM ? p2p_sym_kernel<false, PT, MINB> : p2p_sym_kernel<true, PT, MINB>;
     kern<<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
                                              make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near);
   }
   else if (kind == P2P_DIAG)
-    p2p_ord_kernel<true><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
+    p2p_ord_kernel<true, PT, MINB><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
   else
-    p2p_ord_kernel<false><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
+    p2p_ord_kernel<false, PT, MINB><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
+}
+
+void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
+                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt) {
+  if (nitems <= 0) return;
+  if (pt == 3)
+    launch_p2p_items_t<3, 4>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, s);
+  else
+    launch_p2p_items_t<4, HFMM_P2P_MINB>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, s);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -290,6 +290,13 @@ def test_forced_breakdown_levels_run(hf):
     assert info["levels"][1]["F"] > 1e3          # lambda/4 boxes: roundoff amplification >> 1
     y = g.matvec(q)
     assert np.all(np.isfinite(y))
+    # the breakdown is real: the forced run's error vs the direct sum is far above eps and of the
+    # order of the amplification F_l; the policy run (no admissible level) is exact
+    err = rel(y, direct_sum(x, q, cfg.kappa))
+    F = [lv["F"] for lv in info["levels"] if lv["active"]]
+    print(f"C1 forced: F_l = {F}, error vs direct {err:.2e} (eps {cfg.eps})")
+    assert err > 10 * cfg.eps
+    assert err < 10 * max(F)
 
 
 def test_edge_cases(hf):
