@@ -150,6 +150,13 @@ int hfmm_nccl_unique_id(void *out_128b);
  * value. */
 int hfmm_set_next4(int on);
 
+/* Fused two-pass upward resampler (interpolation / M2M on the large grids: C2 B32 / B64): rows and
+ * columns as dependent tasks of one persistent kernel with the intermediate in an L2-sized ring
+ * (csrc/kernels_fused.cu).  Process-wide switch, default on (HFMM_FUSED=0 in the environment turns
+ * it off at load); off = the two-pass kernels with a global intermediate.  Returns the previous
+ * value. */
+int hfmm_set_fused(int on);
+
 typedef struct hfmm_vgroup hfmm_vgroup;
 int hfmm_vgroup_create(hfmm_vgroup **out, int nranks);
 int hfmm_set_dist_virtual(hfmm_plan *p, hfmm_vgroup *g, int rank);

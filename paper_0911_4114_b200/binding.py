@@ -38,7 +38,7 @@ EXPORTED = [
     "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
     "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free", "hfmm_m2l_op_kind", "hfmm_ragged_rows",
     "hfmm_vgroup_create", "hfmm_set_dist_virtual", "hfmm_vgroup_matvec", "hfmm_vgroup_destroy",
-    "hfmm_set_next4",
+    "hfmm_set_next4", "hfmm_set_fused",
 ]
 
 
@@ -109,6 +109,7 @@ def load() -> C.CDLL:
         "hfmm_vgroup_matvec": (ci, [vp, vp, vp, vp]),
         "hfmm_vgroup_destroy": (None, [vp]),
         "hfmm_set_next4": (ci, [ci]),
+        "hfmm_set_fused": (ci, [ci]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -144,6 +145,11 @@ def set_next4(on: bool) -> bool:
     """NEXT 4 coefficient-domain symmetric resampling on / off (process-wide; include/hfmm.h
     hfmm_set_next4).  Returns the previous setting."""
     return bool(load().hfmm_set_next4(1 if on else 0))
+
+
+def set_fused(on: bool) -> bool:
+    """Fused two-pass upward resampler on / off (process-wide; include/hfmm.h hfmm_set_fused)."""
+    return bool(load().hfmm_set_fused(1 if on else 0))
 
 
 def rep_grid(kappa: float, a: float, eps: float):

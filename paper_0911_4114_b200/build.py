@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhfmm.so")
-SOURCES = ["hfmm.cu", "kernels_points.cu", "kernels_fft.cu", "kernels_m2l.cu", "kernels_ragged.cu", "kernels_misc.cu", "kernels_sym.cu",
+SOURCES = ["hfmm.cu", "kernels_points.cu", "kernels_fft.cu", "kernels_m2l.cu", "kernels_ragged.cu", "kernels_misc.cu", "kernels_sym.cu", "kernels_fused.cu",
            "host_plan.cpp", "host_specfun.cpp", "host_tree.cpp"]
 
 

@@ -151,6 +151,7 @@ struct hfmm_plan {
   double2 *tmp = nullptr;
   size_t tmp_elems = 0;
   double2 *scr1 = nullptr, *scr2 = nullptr;  // rectangular copies around ragged levels (R-15)
+  int *fu_cnt = nullptr;           // task counters of the fused upward resampler (2 max_boxes + 1)
   hfmm_info info{};
   double stage_ms[8] = {0};
   bool profile = false;
@@ -194,8 +195,9 @@ static void free_levels(hfmm_plan *p) {
   p->lv.clear();
   for (void *ptr : {(void *)p->scr1, (void *)p->scr2, (void *)p->first_near, (void *)p->first_src, (void *)p->tile_leaf, (void *)p->tile_begin, (void *)p->tmp,
                     (void *)p->y_far, (void *)p->p2p_items[0], (void *)p->p2p_items[1], (void *)p->p2p_items[2],
-                    (void *)p->dir_items, (void *)p->ux, (void *)p->uy, (void *)p->uz})
+                    (void *)p->dir_items, (void *)p->ux, (void *)p->uy, (void *)p->uz, (void *)p->fu_cnt})
     if (ptr) cudaFree(ptr);
+  p->fu_cnt = nullptr;
   p->first_near = nullptr, p->first_src = nullptr, p->tile_leaf = nullptr;
   p->tile_begin = nullptr, p->tmp = nullptr, p->y_far = nullptr;
   p->scr1 = p->scr2 = nullptr;
@@ -736,6 +738,11 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       }
     }
   }
+  {
+    int64_t maxb = 1;
+    for (int l = 2; l <= std::max(p->L_f, p->D_s); ++l) maxb = std::max<int64_t>(maxb, p->lv[l].nbox);
+    p->fu_cnt = dalloc<int>((size_t)(2 * maxb + 1));
+  }
   if (tmp_need) {
     p->tmp = dalloc<double2>(tmp_need);
     p->tmp_elems = tmp_need;
@@ -1018,9 +1025,11 @@ static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool 
           src = p->scr1;
         }
         if (!C.ragged && !P.ragged &&
-            launch_box2_up(src, P.own1 - P.own0, C.nth, C.nph, P.nth, P.nph, P.cbeg + P.own0, C.own0, C.oct, P.shift,
-                           P.M + P.own0 * P.K, tw, s))
-          continue;  // single pass (small square grids)
+            (launch_fused_up(src, P.own1 - P.own0, C.nth, C.nph, P.nth, P.nph, P.cbeg + P.own0, C.own0, C.oct,
+                             P.shift, P.M + P.own0 * P.K, p->tmp, p->tmp_elems, p->fu_cnt, tw, s) ||
+             launch_box2_up(src, P.own1 - P.own0, C.nth, C.nph, P.nth, P.nph, P.cbeg + P.own0, C.own0, C.oct, P.shift,
+                            P.M + P.own0 * P.K, tw, s)))
+          continue;  // single pass: fused two-pass (large grids) or one CTA per item (small grids)
         launch_rows_up(src, nc, C.nth, C.nph, P.nph, p->tmp, tw, s);
         if (P.ragged) {  // per-child parent fields, then step 5 + shift + sum on the ragged parent grid
           launch_cols_up(p->tmp, C.nth, P.nph, P.nth, nullptr, 0, nullptr, nc, nullptr, p->scr2, tw, s);
@@ -1446,7 +1455,8 @@ bool up_or_down(int nth, int nph, int nth2, int nph2, bool *up) {
 extern "C" int64_t hfmm_resample_workspace(int nbatch, int n_theta, int n_phi, int n_theta2, int n_phi2) {
   bool up;
   if (!up_or_down(n_theta, n_phi, n_theta2, n_phi2, &up)) return -1;
-  if (up) return (int64_t)nbatch * (n_theta / 2 + 1) * n_phi2 * 16;
+  // UP: the rows-pass intermediate (or the fused kernel's ring) + its 2 nbatch + 1 task counters
+  if (up) return (int64_t)nbatch * (n_theta / 2 + 1) * n_phi2 * 16 + ((int64_t)(2 * nbatch + 1) * 4 + 15) / 16 * 16;
   return (int64_t)nbatch * n_theta2 * (n_phi / 2) * 16;
 }
 
@@ -1463,8 +1473,11 @@ extern "C" int hfmm_resample(int nbatch, int nth, int nph, int nth2, int nph2, c
     own = true;
   }
   if (up) {
-    if (!launch_box2_up((const double2 *)in, nbatch, nth, nph, nth2, nph2, nullptr, 0, nullptr, nullptr,
-                        (double2 *)out, tw, s)) {
+    const size_t ring = (size_t)nbatch * (nth / 2 + 1) * nph2;   // complex values before the counters
+    if (launch_fused_up((const double2 *)in, nbatch, nth, nph, nth2, nph2, nullptr, 0, nullptr, nullptr,
+                        (double2 *)out, tmp, ring, (int *)(tmp + ring), tw, s)) {
+    } else if (!launch_box2_up((const double2 *)in, nbatch, nth, nph, nth2, nph2, nullptr, 0, nullptr, nullptr,
+                               (double2 *)out, tw, s)) {
       launch_rows_up((const double2 *)in, nbatch, nth, nph, nph2, tmp, tw, s);
       launch_cols_up(tmp, nth, nph2, nth2, nullptr, 0, nullptr, nbatch, nullptr, (double2 *)out, tw, s);
     }
@@ -1497,8 +1510,11 @@ extern "C" int hfmm_m2m_op(int nparent, int nth, int nph, int nth2, int nph2, co
     if (cudaMalloc(&tmp, hfmm_resample_workspace(nparent * 8, nth, nph, nth2, nph2)) != cudaSuccess) return HFMM_E_NOMEM;
     own = true;
   }
-  if (!launch_box2_up((const double2 *)child, nparent, nth, nph, nth2, nph2, c.cbeg, 0, c.oct, (const double2 *)shift,
-                      (double2 *)parent, tw, s)) {
+  const size_t ring = (size_t)nparent * 8 * (nth / 2 + 1) * nph2;
+  if (launch_fused_up((const double2 *)child, nparent, nth, nph, nth2, nph2, c.cbeg, 0, c.oct, (const double2 *)shift,
+                      (double2 *)parent, tmp, ring, (int *)(tmp + ring), tw, s)) {
+  } else if (!launch_box2_up((const double2 *)child, nparent, nth, nph, nth2, nph2, c.cbeg, 0, c.oct,
+                             (const double2 *)shift, (double2 *)parent, tw, s)) {
     launch_rows_up((const double2 *)child, (int64_t)nparent * 8, nth, nph, nph2, tmp, tw, s);
     launch_cols_up(tmp, nth, nph2, nth2, c.cbeg, 0, c.oct, nparent, (const double2 *)shift, (double2 *)parent, tw, s);
   }

@@ -184,6 +184,14 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
 // (cbeg == nullptr: one box per item, no shift).  Returns false when not applicable.
 bool box2_up_applies(int nth, int nph, int nth2, int nph2);
 bool box2_down_applies(int nth, int nph, int nth2, int nph2);
+// Fused two-pass upward resampler (kernels_fused.cu): rows and columns of every item as dependent
+// tasks of one persistent kernel, the intermediate in an L2-sized ring (ring = workspace of
+// ring_elems complex values, cnt = 2 nitem + 1 ints).  False when not instantiated / disabled
+// (HFMM_FUSED=0) or the workspace is too small.
+bool fused_enabled();
+bool launch_fused_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2, int nph2, const int32_t *cbeg,
+                     int64_t cbase, const int8_t *oct, const double2 *shift, double2 *out, double2 *ring,
+                     size_t ring_elems, int *cnt, const TwiddleSet &tw, cudaStream_t s);
 // NEXT 4 coefficient-domain symmetric resampling (kernels_sym.cu; opt-in HFMM_NEXT4=1): same
 // arguments and result as launch_box2_up / launch_box2_down; false when not enabled or the grid
 // pair has no instantiation.

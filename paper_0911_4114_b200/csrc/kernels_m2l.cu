@@ -249,6 +249,90 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
   }
 }
 
+// Two sibling groups per warp (GPW = 2): the tables depend only on the offset 2D + delta, so one
+// shared-memory table load serves the MACs of both groups (half the table traffic per MAC, twice
+// the accumulators in registers); neighbour parents of either group's mask, a missing parent's
+// sources are zeros.  M2LB2_WARPS warps x 2 groups per CTA.
+#ifndef HFMM_M2L_GPW
+#define HFMM_M2L_GPW 2
+#endif
+constexpr int M2LB2_WARPS = 8;
+
+__global__ void __launch_bounds__(32 * M2LB2_WARPS, 1) m2l_dense2_kernel(
+    int64_t K, int64_t ngroups, int64_t groups_per_unit, int64_t nunits, const int32_t *__restrict__ gtarget,
+    const int32_t *__restrict__ gsrc, const uint32_t *__restrict__ gmask, const double2 *__restrict__ T,
+    const int32_t *__restrict__ perm, const double2 *__restrict__ M, double2 *__restrict__ I) {
+  extern __shared__ double2 Ts[];  // [343][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (K + M2LG_KC - 1) / M2LG_KC;
+  const int64_t ranges = (nunits + nchunks - 1) / nchunks;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t chunk = u / ranges, range = u % ranges;
+    const int64_t k0 = chunk * M2LG_KC;
+    const int64_t k = k0 + lane;
+    const bool kval = k < K;
+    __syncthreads();  // previous unit done with Ts
+    fill_tables_cube(Ts, T, perm, K, k0);
+    __syncthreads();
+    const int64_t g0 = range * groups_per_unit, g1 = min(ngroups, g0 + groups_per_unit);
+    for (int64_t ga = g0 + 2 * warp; ga < g1; ga += 2 * M2LB2_WARPS) {
+      const int64_t gb = ga + 1;
+      const bool hb = gb < g1;
+      double2 acc[2][8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) acc[0][a] = acc[1][a] = make_double2(0.0, 0.0);
+      const uint32_t mka = __ldg(&gmask[ga]), mkb = hb ? __ldg(&gmask[gb]) : 0u;
+      const uint32_t mask = mka | mkb;
+      auto load8 = [&](int64_t g, bool has, int D, double2 *m) {
+        if (!has) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) m[e] = make_double2(0.0, 0.0);
+          return;
+        }
+        const int4 *sp = reinterpret_cast<const int4 *>(gsrc + (g * 27 + D) * 8);
+        const int4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+        const int32_t sid[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          m[e] = (sid[e] >= 0 && kval) ? __ldg(&M[(int64_t)sid[e] * K + k]) : make_double2(0.0, 0.0);
+      };
+      int D = mask ? __ffs(mask) - 1 : 27;
+      double2 m[2][8];
+      if (D < 27) load8(ga, (mka >> D) & 1u, D, m[0]), load8(gb, (mkb >> D) & 1u, D, m[1]);
+      while (D < 27) {
+        const uint32_t rest = mask & ~((2u << D) - 1u);
+        const int Dn = rest ? __ffs(rest) - 1 : 27;
+        const int Dx = D / 9 - 1, Dy = (D / 3) % 3 - 1, Dz = D % 3 - 1;
+        const double2 *Tb = Ts + ((2 * Dx + 2) * 49 + (2 * Dy + 2) * 7 + (2 * Dz + 2)) * M2LG_KC + lane;
+#pragma unroll
+        for (int dl = 0; dl < 27; ++dl) {
+          const int dx = dl / 9 - 1, dy = (dl / 3) % 3 - 1, dz = dl % 3 - 1;
+          const double2 t = Tb[((dx + 1) * 49 + (dy + 1) * 7 + (dz + 1)) * M2LG_KC];
+#pragma unroll
+          for (int d = 0; d < 8; ++d) {
+            const int ex = (d >> 2) + dx, ey = ((d >> 1) & 1) + dy, ez = (d & 1) + dz;
+            if (ex < 0 || ex > 1 || ey < 0 || ey > 1 || ez < 0 || ez > 1) continue;
+            const int e = (ex << 2) | (ey << 1) | ez;
+            acc[0][d] = g_cfma(t, m[0][e], acc[0][d]);
+            acc[1][d] = g_cfma(t, m[1][e], acc[1][d]);
+          }
+        }
+        if (Dn < 27) load8(ga, (mka >> Dn) & 1u, Dn, m[0]), load8(gb, (mkb >> Dn) & 1u, Dn, m[1]);
+        D = Dn;
+      }
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        const int32_t ba = gtarget[ga * 8 + d];
+        if (ba >= 0 && kval) I[(int64_t)ba * K + k] = acc[0][d];
+        if (hb) {
+          const int32_t bb = gtarget[gb * 8 + d];
+          if (bb >= 0 && kval) I[(int64_t)bb * K + k] = acc[1][d];
+        }
+      }
+    }
+  }
+}
+
 // ---- host plan -----------------------------------------------------------------------------------
 struct M2LGroupPlan {
   int64_t nbox = 0, K = 0, ngroups = 0, nentries = 0;
@@ -503,8 +587,15 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
     upload_slot_table();
     const size_t smem_b = (size_t)M2LB_SLOTS * M2LG_KC * sizeof(double2);
     cudaFuncSetAttribute(m2l_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
-    m2l_dense_kernel<<<grid, 32 * M2LG_WARPS, smem_b, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget, pl->dsrc,
-                                                         pl->dmask, T, perm, M, I);
+    if (HFMM_M2L_GPW == 2) {
+      cudaFuncSetAttribute(m2l_dense2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
+      // same units (groups_per_unit = per_warp x 16): 8 warps x 2 groups each cover them
+      m2l_dense2_kernel<<<grid, 32 * M2LB2_WARPS, smem_b, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget,
+                                                               pl->dsrc, pl->dmask, T, perm, M, I);
+    } else {
+      m2l_dense_kernel<<<grid, 32 * M2LG_WARPS, smem_b, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget, pl->dsrc,
+                                                           pl->dmask, T, perm, M, I);
+    }
   } else {
     m2l_group_kernel<<<grid, 32 * M2LG_WARPS, smem, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->gtarget,
                                                          pl->gsrc_row, pl->src_box, pl->tid8, T, perm, M, I);
