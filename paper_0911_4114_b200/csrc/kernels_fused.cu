@@ -6,7 +6,7 @@
 // algorithmic bytes on the C2 B64 interpolation (profiles/r01).  Here ONE persistent kernel runs
 // both passes as dependent tasks taken in a fixed order from a global counter:
 //     round r:  the row task of every child of item r       (child -> ring slot r mod D)
-//               the column strips of item r - L            (ring slot -> parent, shift, child sum)
+//               the column task of item r - L              (ring slot -> parent, shift, child sum)
 // A column task of item i waits for the row tasks of item i (per-item counter), a row task that
 // reuses ring slot s waits until every column task of the item that last used it is done; both
 // wait only on tasks with smaller positions in the order, which were handed out earlier to
@@ -27,6 +27,9 @@
 namespace hfmm {
 
 constexpr int FU_CW = 8, FU_CWP = 9;   // columns per strip, exchange pitch (the cols2 layout)
+#ifndef HFMM_FUSED_MINB
+#define HFMM_FUSED_MINB 3                 // CTAs per SM asked of ptxas (the two-pass kernels run 3)
+#endif
 
 __device__ __forceinline__ void fu_cp_async16(double2 *smem, const double2 *gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -59,7 +62,7 @@ struct FuCfg {
 };
 
 template <int RF1, int RF2, int RI1, int RI2, int CF1, int CF2, int CI1, int CI2>
-__global__ void __launch_bounds__(128) fused_up_kernel(const double2 *__restrict__ in, int64_t nitem,
+__global__ void __launch_bounds__(128, HFMM_FUSED_MINB) fused_up_kernel(const double2 *__restrict__ in, int64_t nitem,
                                                       const int32_t *__restrict__ cbeg, int64_t cbase, int CH,
                                                       const int8_t *__restrict__ oct,
                                                       const double2 *__restrict__ shift,
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(128) fused_up_kernel(const double2 *__restrict
   const int grp = lane / G, gr = lane - grp * G;
   double2 *rb = rbuf + (warp * VW + grp) * RBUF;
   const int v = threadIdx.x & (FU_CW - 1), g = threadIdx.x >> 3;
-  const int64_t RT = CH + NSTRIP;                 // tasks per round
+  const int64_t RT = CH + 1;                      // tasks per round: the row tasks, one column task
   const int64_t ntasks = (nitem + L) * RT;
   for (;;) {
     __syncthreads();                              // previous task done with shared memory / s_task
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(128) fused_up_kernel(const double2 *__restrict
       if (c >= c1) continue;
       if (item >= D) {                            // slot reuse: the item D before must be consumed
         if (threadIdx.x == 0)
-          while (fu_ld_acquire(&cols_done[item - D]) < NSTRIP) __nanosleep(64);
+          while (fu_ld_acquire(&cols_done[item - D]) < 1) __nanosleep(64);
         __syncthreads();
       }
       double2 *dst = ring + ((item % D) * CH + idx) * C::child_elems;
@@ -174,29 +177,37 @@ __global__ void __launch_bounds__(128) fused_up_kernel(const double2 *__restrict
       __syncthreads();
       if (threadIdx.x == 0) atomicAdd(&rows_done[item], 1);   // ... before the count
     } else {
-      // ---------------- column task: strip of item `round - L` (ring -> parent) ----------------
+      // ------- column task: every strip of item `round - L` (ring -> parent), the next step's
+      //         strip fetched with cp.async while the current one is transformed (cols2 pipeline)
       const int64_t item = round - L;
       if (item < 0 || item >= nitem) continue;
-      const int strip = (int)(idx - CH);
       const int64_t c0 = cbeg ? cbeg[item] : item, c1 = cbeg ? cbeg[item + 1] : item + 1;
+      const int nch = (int)(c1 - c0);
       if (threadIdx.x == 0)
-        while (fu_ld_acquire(&rows_done[item]) < (int)(c1 - c0)) __nanosleep(64);
+        while (fu_ld_acquire(&rows_done[item]) < nch) __nanosleep(64);
       __syncthreads();
-      const int m = strip * FU_CW + v;
-      const bool mok = m < h2;
-      double2 *ob = out + item * (int64_t)NC2 * h2 + m;
-      for (int64_t c = c0; c < c1; ++c) {
-        const double2 *cb = ring + ((item % D) * CH + (c - c0)) * C::child_elems;
-        double2 x[16];
-        __syncthreads();                          // stg / cbuf free
+      const double2 *slot = ring + (item % D) * CH * C::child_elems;
+      auto issue = [&](int st) {   // step st = strip * nch + child
+        const int strip = st / nch, cj = st - strip * nch;
+        const double2 *cb = slot + cj * C::child_elems;
         for (int e = threadIdx.x; e < NC * FU_CW; e += blockDim.x) {   // theta-periodic strip (L2 only)
           const int n = e >> 3, vv = e & (FU_CW - 1), mm = strip * FU_CW + vv;
           if (mm >= h2) continue;
           const double2 *sp = (2 * n <= NC) ? &cb[(int64_t)n * NR2 + mm] : &cb[(int64_t)(NC - n) * NR2 + mm + h2];
           fu_cp_async16(&stg[n * FU_CWP + vv], sp);
         }
+      };
+      const int nsteps = NSTRIP * nch;
+      issue(0);
+      for (int st = 0; st < nsteps; ++st) {
+        const int strip = st / nch, cj = st - strip * nch;
+        const int64_t c = c0 + cj;
+        const int m = strip * FU_CW + v;
+        const bool mok = m < h2;
+        double2 *ob = out + item * (int64_t)NC2 * h2 + m;
+        double2 x[16];
         fu_cp_async_wait_all();
-        __syncthreads();
+        __syncthreads();                          // stg holds step st; cbuf free
         if (g < CF2) {
 #pragma unroll
           for (int n1 = 0; n1 < CF1; ++n1) x[n1] = mok ? stg[(CF2 * n1 + g) * FU_CWP + v] : make_double2(0.0, 0.0);
@@ -206,7 +217,8 @@ __global__ void __launch_bounds__(128) fused_up_kernel(const double2 *__restrict
 #pragma unroll
           for (int k1 = 0; k1 < CF1; ++k1) cbuf[(k1 * (CF2 + 1) + g) * FU_CWP + v] = x[k1];
         }
-        __syncthreads();
+        __syncthreads();                          // stg consumed: fetch the next step's strip
+        if (st + 1 < nsteps) issue(st + 1);
         if (g < CF1) {
 #pragma unroll
           for (int n2 = 0; n2 < CF2; ++n2) x[n2] = cbuf[(g * (CF2 + 1) + n2) * FU_CWP + v];
@@ -254,7 +266,7 @@ __global__ void __launch_bounds__(128) fused_up_kernel(const double2 *__restrict
 #pragma unroll
             for (int k2 = 0; k2 < CI2; ++k2) x[k2] = c_mul(x[k2], tt[k2]);
           }
-          if (c != c0) {
+          if (cj != 0) {
             double2 tt[CI2];
 #pragma unroll
             for (int k2 = 0; k2 < CI2; ++k2) tt[k2] = ob[(int64_t)(g + CI1 * k2) * h2];

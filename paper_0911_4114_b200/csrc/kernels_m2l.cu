@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
 // the accumulators in registers); neighbour parents of either group's mask, a missing parent's
 // sources are zeros.  M2LB2_WARPS warps x 2 groups per CTA.
 #ifndef HFMM_M2L_GPW
-#define HFMM_M2L_GPW 2
+#define HFMM_M2L_GPW 1   // 2: m2l_dense2_kernel (A/B: B64 52 vs 42 ms, kept off)
 #endif
 constexpr int M2LB2_WARPS = 8;
 
