@@ -50,7 +50,7 @@ def parse():
                     help="C2 operator microbench bandwidths B (comma list; '' to skip)")
     ap.add_argument("--ragged", type=int, default=0,
                     help="1: ragged quadrature on the active levels (HFMM_RAGGED, DESIGN.md R-15)")
-    ap.add_argument("--extra", default="C3,C5,C3_acc,C5_acc",
+    ap.add_argument("--extra", default="C3,C5,C3_acc,C5_acc,C1HF",
                     help="other BASELINE matvec configs timed after the main one (comma list; '' to skip)")
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--oracle-full", default=None,

@@ -152,9 +152,9 @@ int hfmm_set_next4(int on);
 
 /* Fused two-pass upward resampler (interpolation / M2M on the large grids: C2 B32 / B64): rows and
  * columns as dependent tasks of one persistent kernel with the intermediate in an L2-sized ring
- * (csrc/kernels_fused.cu).  Process-wide switch, default on (HFMM_FUSED=0 in the environment turns
- * it off at load); off = the two-pass kernels with a global intermediate.  Returns the previous
- * value. */
+ * (csrc/kernels_fused.cu).  Process-wide switch, default OFF (slower in the same-box A/B,
+ * profiles/r02/fused_ab_r2.txt); HFMM_FUSED=1 in the environment turns it on at load; off = the
+ * two-pass kernels with a global intermediate.  Returns the previous value. */
 int hfmm_set_fused(int on);
 
 typedef struct hfmm_vgroup hfmm_vgroup;

@@ -284,10 +284,14 @@ __global__ void __launch_bounds__(128, HFMM_FUSED_MINB) fused_up_kernel(const do
 }
 
 // ---- launch ---------------------------------------------------------------------------------------
-// Process-wide switch: HFMM_FUSED in the environment at load time (default 1), or hfmm_set_fused().
+// Process-wide switch: HFMM_FUSED in the environment at load time (default 0), or hfmm_set_fused().
+// Off by default: the same-box A/B lost (profiles/r02/fused_ab_r2.txt: B64 interp 27.5 / 21.7 ms
+// at 3 / 2 CTAs per SM vs 17.1 ms two-pass; fused M2M far slower -- one column task per parent
+// serialises 8 children x 16 strips behind the dependency waits).  The two-pass kernels run at
+// ~4.5 TB/s average on their 1.8x traffic; the task-queue kernel is latency-bound instead.
 static std::atomic<int> g_fused{[] {
   const char *e = getenv("HFMM_FUSED");
-  return e ? atoi(e) : 1;
+  return e ? atoi(e) : 0;
 }()};
 
 bool fused_enabled() { return g_fused.load(std::memory_order_relaxed) != 0; }

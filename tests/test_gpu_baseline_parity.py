@@ -222,3 +222,28 @@ def test_fullsize_subset_accuracy_policy(hf, name):
     assert p_y <= far_tol([Fmax])
     assert rel(y[t], yd) <= cfg.eps
     g.close()
+
+
+def test_c1hf_full_vector(hf):
+    """C1-HF (SURVEY D-1: the C1 points at kappa = 64 pi, depth 4 -- every level 2..4 admissible, every
+    kernel active): the whole output vector vs the oracle reference (tests/golden/subset_C1HF.json,
+    all 2,000 targets) and vs the direct sums (<= eps)."""
+    import torch
+    d, t, yn_o, yf_o, yd = load_golden("C1HF")
+    cfg = CONFIGS["C1HF"]
+    assert len(t) == cfg.n
+    x, q = points_and_charges(cfg)
+    g = hf.HFMM(0)
+    g.build_tree(x, cfg.depth, cfg.lo, cfg.size)
+    g.precompute(cfg.kappa, cfg.eps, cfg.alpha)
+    info = g.info()
+    assert (info["L_f"], info["source_level"]) == (d["L_f"], d["source_level"]) == (4, 4)
+    y = g.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    perm = g.debug(6)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    assert rel(y[t], yn_o + yf_o) <= PARITY
+    assert rel(g.debug(4)[: cfg.n][inv[t]], yn_o) <= PARITY
+    assert rel(g.debug(5)[: cfg.n][inv[t]], yf_o) <= far_tol(v["F"] for v in d["levels"].values() if v["active"])
+    assert rel(y[t], yd) <= cfg.eps
+    g.close()

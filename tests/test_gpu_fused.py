@@ -1,5 +1,6 @@
-"""GPU parity of the fused two-pass upward resampler (csrc/kernels_fused.cu; default on for the large
-square grids 64 -> 128 and 128 -> 256 of the C2 microbench).
+"""GPU parity of the fused two-pass upward resampler (csrc/kernels_fused.cu; opt-in experiment for
+the large square grids 64 -> 128 and 128 -> 256 of the C2 microbench, off by default after a
+negative same-box A/B, profiles/r02/fused_ab_r2.txt).
 
 It runs the same row / column arithmetic as the two-pass kernels, operation for operation, with
 the intermediate in an L2-sized ring of D items instead of a global buffer, as dependent tasks of
@@ -46,13 +47,13 @@ def test_fused_interp(hf, n, n2, nbox):
     child = crandn(gen, nbox, K)
     out_f = torch.empty(nbox, K2, dtype=torch.complex128, device="cuda")
     out_2 = torch.empty_like(out_f)
-    assert hf.set_fused(True) in (True, False)
-    hf.resample(child, n, n, n2, n2, out_f)
-    hf.set_fused(False)
+    prev = hf.set_fused(True)
     try:
+        hf.resample(child, n, n, n2, n2, out_f)
+        hf.set_fused(False)
         hf.resample(child, n, n, n2, n2, out_2)
     finally:
-        hf.set_fused(True)
+        hf.set_fused(prev)
     torch.cuda.synchronize()
     assert torch.equal(out_f, out_2)
     s = np.array([0, 1, nbox // 3, nbox // 2 + 7, nbox - 1])
@@ -71,13 +72,13 @@ def test_fused_m2m(hf, n, n2, npar):
                         2 * math.pi * torch.rand(8, K2, dtype=torch.float64, device="cuda", generator=gen))
     par_f = torch.empty(npar, K2, dtype=torch.complex128, device="cuda")
     par_2 = torch.empty_like(par_f)
-    hf.set_fused(True)
-    hf.m2m_op(child, shift, par_f, n, n, n2, n2)
-    hf.set_fused(False)
+    prev = hf.set_fused(True)
     try:
+        hf.m2m_op(child, shift, par_f, n, n, n2, n2)
+        hf.set_fused(False)
         hf.m2m_op(child, shift, par_2, n, n, n2, n2)
     finally:
-        hf.set_fused(True)
+        hf.set_fused(prev)
     torch.cuda.synchronize()
     assert torch.equal(par_f, par_2)
     sh = shift.cpu().numpy()
