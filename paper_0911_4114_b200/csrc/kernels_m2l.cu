@@ -333,6 +333,123 @@ __global__ void __launch_bounds__(32 * M2LB2_WARPS, 1) m2l_dense2_kernel(
   }
 }
 
+// Parent-block kernel with the next neighbour parent's sources prefetched (m2l_dense_pf_kernel,
+// HFMM_M2L_PF16): chunks of 16 directions; a warp runs two sibling groups, lanes 0-15 one and
+// 16-31 the other, over the same 16 directions, so every table read is a 2-way broadcast (half the
+// shared-memory wavefronts per MAC of the 32-direction kernel, half its table footprint: 88 KB); the
+// 8 source values of the next neighbour parent are fetched with cp.async into a per-warp double
+// buffer in shared memory while the current parent's MACs run (the 32-direction kernel exposes that
+// L2 latency: long-scoreboard stalls, profiles/r01), without holding them in registers.
+#ifndef HFMM_M2L_PF16
+#define HFMM_M2L_PF16 1
+#endif
+constexpr int M2LP_KC = 16, M2LP_WARPS = 16;
+
+__device__ __forceinline__ void m2l_cp_async16(double2 *smem, const double2 *gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;   // src-size 0: zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+
+__device__ __forceinline__ void fill_tables_cube16(double2 *Ts, const double2 *__restrict__ T,
+                                                   const int32_t *__restrict__ perm, int64_t K, int64_t k0) {
+  for (int i = threadIdx.x; i < M2LB_SLOTS * M2LP_KC; i += blockDim.x) {
+    const int sl = i / M2LP_KC, kk = i % M2LP_KC;
+    const int o = c_slot_id[sl];
+    const int64_t kg = k0 + kk;
+    double2 v = make_double2(0.0, 0.0);
+    if (o >= 0 && kg < K) {
+      if (perm) {
+        const int32_t code = c_sym_of[o];
+        v = T[(int64_t)(code >> 4) * K + perm[(int64_t)(code & 15) * K + kg]];
+      } else {
+        v = T[(int64_t)o * K + kg];
+      }
+    }
+    Ts[i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(32 * M2LP_WARPS, 1) m2l_dense_pf_kernel(
+    int64_t K, int64_t ngroups, int64_t groups_per_unit, int64_t nunits, const int32_t *__restrict__ gtarget,
+    const int32_t *__restrict__ gsrc, const uint32_t *__restrict__ gmask, const double2 *__restrict__ T,
+    const int32_t *__restrict__ perm, const double2 *__restrict__ M, double2 *__restrict__ I) {
+  extern __shared__ double2 Ts[];                          // [343][16] tables, then [warps][2][8][32] buffers
+  double2 *bufs = Ts + M2LB_SLOTS * M2LP_KC;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane >> 4;
+  double2 *wb = bufs + warp * (2 * 8 * 32);
+  const int64_t nchunks = (K + M2LP_KC - 1) / M2LP_KC;
+  const int64_t ranges = (nunits + nchunks - 1) / nchunks;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t chunk = u / ranges, range = u % ranges;
+    const int64_t k0 = chunk * M2LP_KC;
+    const int64_t k = k0 + (lane & 15);
+    const bool kval = k < K;
+    __syncthreads();  // previous unit done with Ts
+    fill_tables_cube16(Ts, T, perm, K, k0);
+    __syncthreads();
+    const int64_t g0 = range * groups_per_unit, g1 = min(ngroups, g0 + groups_per_unit);
+    for (int64_t gp = g0 + 2 * warp; gp < g1; gp += 2 * M2LP_WARPS) {
+      const int64_t g = gp + half;                         // this half-warp's group
+      const bool hg = g < g1;
+      double2 acc[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) acc[a] = make_double2(0.0, 0.0);
+      const uint32_t mk = hg ? __ldg(&gmask[g]) : 0u;
+      const uint32_t mask = mk | __shfl_xor_sync(0xffffffffu, mk, 16);   // union over the two groups
+      auto issue = [&](int D, int stage) {                 // 8 source values of parent slot D
+        const bool has = (mk >> D) & 1u;
+        const int32_t *sp = gsrc + (g * 27 + D) * 8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int32_t sid = has ? __ldg(&sp[e]) : -1;
+          const bool ok = sid >= 0 && kval;
+          m2l_cp_async16(&wb[(stage * 8 + e) * 32 + lane], ok ? &M[(int64_t)sid * K + k] : M, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+      };
+      int D = mask ? __ffs(mask) - 1 : 27;
+      int stage = 0;
+      if (D < 27) issue(D, 0);
+      while (D < 27) {
+        const uint32_t rest = mask & ~((2u << D) - 1u);
+        const int Dn = rest ? __ffs(rest) - 1 : 27;
+        if (Dn < 27) {
+          issue(Dn, stage ^ 1);
+          asm volatile("cp.async.wait_group 1;\n" ::);   // the current stage has landed
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        double2 m[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m[e] = wb[(stage * 8 + e) * 32 + lane];
+        const int Dx = D / 9 - 1, Dy = (D / 3) % 3 - 1, Dz = D % 3 - 1;
+        const double2 *Tb = Ts + ((2 * Dx + 2) * 49 + (2 * Dy + 2) * 7 + (2 * Dz + 2)) * M2LP_KC + (lane & 15);
+#pragma unroll
+        for (int dl = 0; dl < 27; ++dl) {
+          const int dx = dl / 9 - 1, dy = (dl / 3) % 3 - 1, dz = dl % 3 - 1;
+          const double2 t = Tb[((dx + 1) * 49 + (dy + 1) * 7 + (dz + 1)) * M2LP_KC];
+#pragma unroll
+          for (int d = 0; d < 8; ++d) {
+            const int ex = (d >> 2) + dx, ey = ((d >> 1) & 1) + dy, ez = (d & 1) + dz;
+            if (ex < 0 || ex > 1 || ey < 0 || ey > 1 || ez < 0 || ez > 1) continue;
+            acc[d] = g_cfma(t, m[(ex << 2) | (ey << 1) | ez], acc[d]);
+          }
+        }
+        stage ^= 1;
+        D = Dn;
+      }
+      if (hg) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          const int32_t b = gtarget[g * 8 + d];
+          if (b >= 0 && kval) I[(int64_t)b * K + k] = acc[d];
+        }
+      }
+    }
+  }
+}
+
 // ---- host plan -----------------------------------------------------------------------------------
 struct M2LGroupPlan {
   int64_t nbox = 0, K = 0, ngroups = 0, nentries = 0;
@@ -587,7 +704,18 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
     upload_slot_table();
     const size_t smem_b = (size_t)M2LB_SLOTS * M2LG_KC * sizeof(double2);
     cudaFuncSetAttribute(m2l_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
-    if (HFMM_M2L_GPW == 2) {
+    if (HFMM_M2L_PF16) {
+      const size_t smem_p = ((size_t)M2LB_SLOTS * M2LP_KC + (size_t)M2LP_WARPS * 2 * 8 * 32) * sizeof(double2);
+      cudaFuncSetAttribute(m2l_dense_pf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+      // units over 16-direction chunks: 16 warps x 2 groups cover groups_per_unit = per_warp x 32
+      const int64_t nch16 = (pl->K + M2LP_KC - 1) / M2LP_KC;
+      const int64_t gpu16 = per_warp * 2 * M2LP_WARPS;
+      const int64_t ranges16 = (pl->ngroups + gpu16 - 1) / gpu16;
+      const int64_t nunits16 = nch16 * ranges16;
+      const unsigned grid16 = (unsigned)std::min<int64_t>(nunits16, nsm);
+      m2l_dense_pf_kernel<<<grid16, 32 * M2LP_WARPS, smem_p, s>>>(pl->K, pl->ngroups, gpu16, nunits16, pl->dtarget,
+                                                                  pl->dsrc, pl->dmask, T, perm, M, I);
+    } else if (HFMM_M2L_GPW == 2) {
       cudaFuncSetAttribute(m2l_dense2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
       // same units (groups_per_unit = per_warp x 16): 8 warps x 2 groups each cover them
       m2l_dense2_kernel<<<grid, 32 * M2LB2_WARPS, smem_b, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget,
