@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(32 * M2LB2_WARPS, 1) m2l_dense2_kernel(
 // buffer in shared memory while the current parent's MACs run (the 32-direction kernel exposes that
 // L2 latency: long-scoreboard stalls, profiles/r01), without holding them in registers.
 #ifndef HFMM_M2L_PF16
-#define HFMM_M2L_PF16 1
+#define HFMM_M2L_PF16 0   // A/B (profiles/r02/m2l_pf16_ab.txt): B64 44.7 vs 41.9 ms for the 32-direction kernel
 #endif
 constexpr int M2LP_KC = 16, M2LP_WARPS = 16;
 
