@@ -25,6 +25,7 @@ HFMM_ALPHA_FIXED = 0x4
 HFMM_SOURCE_AT_LF = 0x8
 HFMM_SOURCE_AT_DEPTH = 0x10
 HFMM_RAGGED = 0x20
+HFMM_DETERMINISTIC = 0x40
 HFMM_HOST = 0
 HFMM_DEVICE = 1
 HFMM_Y_LOCAL = 2

@@ -152,6 +152,10 @@ struct hfmm_plan {
   size_t tmp_elems = 0;
   double2 *scr1 = nullptr, *scr2 = nullptr;  // rectangular copies around ragged levels (R-15)
   int *fu_cnt = nullptr;           // task counters of the fused upward resampler (2 max_boxes + 1)
+  // deterministic P2P (HFMM_DETERMINISTIC): per-item partial slots, partials, per-point CSR
+  int64_t *p2p_slot[3] = {nullptr, nullptr, nullptr};
+  double2 *p2p_part = nullptr;
+  int64_t *p2p_rp = nullptr, *p2p_idx = nullptr;
   hfmm_info info{};
   double stage_ms[8] = {0};
   bool profile = false;
@@ -195,9 +199,13 @@ static void free_levels(hfmm_plan *p) {
   p->lv.clear();
   for (void *ptr : {(void *)p->scr1, (void *)p->scr2, (void *)p->first_near, (void *)p->first_src, (void *)p->tile_leaf, (void *)p->tile_begin, (void *)p->tmp,
                     (void *)p->y_far, (void *)p->p2p_items[0], (void *)p->p2p_items[1], (void *)p->p2p_items[2],
-                    (void *)p->dir_items, (void *)p->ux, (void *)p->uy, (void *)p->uz, (void *)p->fu_cnt})
+                    (void *)p->dir_items, (void *)p->ux, (void *)p->uy, (void *)p->uz, (void *)p->fu_cnt,
+                    (void *)p->p2p_slot[0], (void *)p->p2p_slot[1], (void *)p->p2p_slot[2], (void *)p->p2p_part,
+                    (void *)p->p2p_rp, (void *)p->p2p_idx})
     if (ptr) cudaFree(ptr);
   p->fu_cnt = nullptr;
+  for (auto &q : p->p2p_slot) q = nullptr;
+  p->p2p_part = nullptr, p->p2p_rp = p->p2p_idx = nullptr;
   p->first_near = nullptr, p->first_src = nullptr, p->tile_leaf = nullptr;
   p->tile_begin = nullptr, p->tmp = nullptr, p->y_far = nullptr;
   p->scr1 = p->scr2 = nullptr;
@@ -846,6 +854,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       }
     }
     // longest items first (LPT order against the tail of the grid)
+    std::vector<int64_t> sorted_items[3];
     for (int k = 0; k < 3; ++k) {
       const int64_t m = (int64_t)it[k].size() / 4;
       std::vector<int64_t> ord(m);
@@ -863,7 +872,56 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
           sym_pairs += nt * (nt - 1) / 2;
         }
       p->p2p_items[k] = dupload(sorted);
+      sorted_items[k] = std::move(sorted);
       p->p2p_nitems[k] = m;
+    }
+    // deterministic accumulation (HFMM_DETERMINISTIC): every item writes its row (and, for the
+    // symmetric kernels, column) partial sums into its own slots; point i then sums its partials
+    // in a fixed order (kinds in launch order, items in launch order, rows before columns)
+    if (flags & HFMM_DETERMINISTIC) {
+      std::vector<int64_t> slot[3];
+      int64_t off = 0;
+      for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD}) {
+        const bool cols = k == P2P_SYM || (k == P2P_DIAG && HFMM_P2P_DSYM);
+        const std::vector<int64_t> &v = sorted_items[k];
+        const int64_t m = (int64_t)v.size() / 4;
+        slot[k].assign(2 * m, -1);
+        for (int64_t i = 0; i < m; ++i) {
+          slot[k][2 * i] = off, off += v[4 * i + 1] - v[4 * i];
+          if (cols) slot[k][2 * i + 1] = off, off += v[4 * i + 3] - v[4 * i + 2];
+        }
+      }
+      std::vector<int64_t> rp(t.n + 1, 0), idx((size_t)off);
+      for (int pass = 0; pass < 2; ++pass) {   // count, then fill
+        std::vector<int64_t> fill;
+        if (pass == 1) {
+          for (int64_t i = 0; i < t.n; ++i) rp[i + 1] += rp[i];
+          fill.assign(rp.begin(), rp.end() - 1);
+        }
+        for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD}) {
+          const std::vector<int64_t> &v = sorted_items[k];
+          const int64_t m = (int64_t)v.size() / 4;
+          for (int64_t i = 0; i < m; ++i) {
+            for (int64_t q = v[4 * i]; q < v[4 * i + 1]; ++q) {
+              if (pass == 0) ++rp[q + 1];
+              else idx[(size_t)fill[q]++] = slot[k][2 * i] + (q - v[4 * i]);
+            }
+            if (slot[k][2 * i + 1] >= 0)
+              for (int64_t q = v[4 * i + 2]; q < v[4 * i + 3]; ++q) {
+                if (pass == 0) ++rp[q + 1];
+                else idx[(size_t)fill[q]++] = slot[k][2 * i + 1] + (q - v[4 * i + 2]);
+              }
+          }
+        }
+      }
+      for (int k = 0; k < 3; ++k) p->p2p_slot[k] = dupload(slot[k]);
+      p->p2p_part = dalloc<double2>((size_t)std::max<int64_t>(off, 1));
+      p->p2p_rp = dupload(rp);
+      p->p2p_idx = dupload(idx);
+      if (!p->p2p_part || !p->p2p_rp || (off && !p->p2p_idx)) {
+        p->err = "hfmm_precompute: allocation failed (deterministic P2P partials)";
+        return HFMM_E_NOMEM;
+      }
     }
     // hfmm_direct: every target tile against all points (self pair masked)
     {
@@ -918,7 +976,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
   in.source_level = p->D_s;
   {  // kernel launches of one matvec (run_matvec): permute, P2P kinds, far chain, combine
-    int nl = 2, n4 = 0;
+    int nl = 2 + ((flags & HFMM_DETERMINISTIC) ? 1 : 0), n4 = 0;   // + the partial-sum reduction
     for (int k = 0; k < 3; ++k) nl += p->p2p_nitems[k] > 0 ? 1 : 0;
     if (p->L_f >= 2) {
       for (int l = p->D_s; l > 2; --l) {          // M2M: rows + cols pass per level (or one pass)
@@ -993,13 +1051,16 @@ static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool 
   CK(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0));
   cudaStream_t s = p->stream_hi;
   if (prof) cudaEventRecord(p->sev[7], p->stream2);
-  CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), p->stream2));
+  const bool det = p->p2p_part != nullptr;
+  if (!det) CK(cudaMemsetAsync(p->y_near, 0, n * sizeof(double2), p->stream2));
   {
     NvtxRange nv("hfmm:P2P");
     PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
     for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD})
       launch_p2p_items(pu, p->p2p_items[k], p->p2p_nitems[k], (k == P2P_DIAG && HFMM_P2P_DSYM) ? P2P_DSYM : k,
-                       p->uscale, p->dummy_t, p->dummy_s, p->y_near, p->stream2, p->p2p_pt);
+                       p->uscale, p->dummy_t, p->dummy_s, p->y_near, p->stream2, p->p2p_pt,
+                       det ? p->p2p_part : nullptr, det ? p->p2p_slot[k] : nullptr);
+    if (det) launch_p2p_reduce(p->p2p_part, p->p2p_rp, p->p2p_idx, n, p->y_near, p->stream2);
   }
   if (prof) cudaEventRecord(p->sev[8], p->stream2);
   CK(cudaEventRecord(p->ev_join, p->stream2));

@@ -131,7 +131,11 @@ enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2, P2P_DSYM = 3 };
 // Adds scale * sum into y_near (zeroed beforehand); scale = kappa TAB_STEPS / (2 pi).
 // dummy_t / dummy_s (scaled units): far positions used to pad partial symmetric tiles.
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
-                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt);
+                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt,
+                      double2 *part = nullptr, const int64_t *slot = nullptr);
+// deterministic P2P accumulation: y_near[i] = sum of part[idx[e]], e in [row_ptr[i], row_ptr[i + 1])
+void launch_p2p_reduce(const double2 *part, const int64_t *row_ptr, const int64_t *idx, int64_t n, double2 *y_near,
+                       cudaStream_t s);
 
 // S2M: M[b][k] = sum_j q_j e^{i kappa s_k.(x_j - c_b)}; ks = kappa s / h (table steps)
 void launch_s2m(PointsDev pts, const int64_t *first, const double *cx, const double *cy,

@@ -104,10 +104,15 @@ __device__ __forceinline__ double2 green_u(double tx, double ty, double tz, doub
   return make_double2(e.x * ri, e.y * ri);
 }
 
+// Outputs: y_near += (atomics, default), or -- deterministic mode (part != nullptr) -- the item's
+// row / column partial sums written to part[slot[2 item] + row], part[slot[2 item + 1] + column],
+// summed per point in a fixed order afterwards (p2p_reduce_kernel): bitwise reproducible.
 template <bool DIAG, int PT, int MINB>
 __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_ord_kernel(PointsU pts,
                                                                         const int64_t *__restrict__ items,
-                                                                        double scale, double2 *__restrict__ y_near) {
+                                                                        double scale, double2 *__restrict__ y_near,
+                                                                        double2 *__restrict__ part,
+                                                                        const int64_t *__restrict__ slot) {
   __shared__ double2 tab[TAB];
   __shared__ double sx[P2P_TPB], sy[P2P_TPB], sz[P2P_TPB];
   __shared__ double2 sq[P2P_TPB];
@@ -154,7 +159,9 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_ord_kernel(PointsU pts,
 #pragma unroll
   for (int p = 0; p < PT; ++p) {
     const int64_t i = it[0] + threadIdx.x + p * P2P_TPB;
-    if (i < t1) atomicAdd(&y_near[i].x, scale * ar[p]), atomicAdd(&y_near[i].y, scale * ai[p]);
+    if (i >= t1) continue;
+    if (part) part[slot[2 * (int64_t)blockIdx.x] + (i - it[0])] = make_double2(scale * ar[p], scale * ai[p]);
+    else atomicAdd(&y_near[i].x, scale * ar[p]), atomicAdd(&y_near[i].y, scale * ai[p]);
   }
 }
 
@@ -172,7 +179,9 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
                                                                         const int64_t *__restrict__ items,
                                                                         double scale, double3 dummy_t,
                                                                         double3 dummy_s,
-                                                                        double2 *__restrict__ y_near) {
+                                                                        double2 *__restrict__ y_near,
+                                                                        double2 *__restrict__ part,
+                                                                        const int64_t *__restrict__ slot) {
   __shared__ double2 tab[TAB];
   __shared__ double sx[P2P_TPB], sy[P2P_TPB], sz[P2P_TPB];
   __shared__ double2 sq[P2P_TPB];
@@ -243,38 +252,66 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
       double2 sum = col[0][threadIdx.x];
 #pragma unroll
       for (int w = 1; w < P2P_TPB / 32; ++w) sum.x += col[w][threadIdx.x].x, sum.y += col[w][threadIdx.x].y;
-      atomicAdd(&y_near[c0 + threadIdx.x].x, scale * sum.x);
-      atomicAdd(&y_near[c0 + threadIdx.x].y, scale * sum.y);
+      if (part) {
+        part[slot[2 * (int64_t)blockIdx.x + 1] + (c0 - s0) + threadIdx.x] = make_double2(scale * sum.x, scale * sum.y);
+      } else {
+        atomicAdd(&y_near[c0 + threadIdx.x].x, scale * sum.x);
+        atomicAdd(&y_near[c0 + threadIdx.x].y, scale * sum.y);
+      }
     }
   }
 #pragma unroll
   for (int p = 0; p < PT; ++p) {
     const int64_t i = it[0] + threadIdx.x + p * P2P_TPB;
-    if (i < t1) atomicAdd(&y_near[i].x, scale * ar[p]), atomicAdd(&y_near[i].y, scale * ai[p]);
+    if (i >= t1) continue;
+    if (part) part[slot[2 * (int64_t)blockIdx.x] + (i - it[0])] = make_double2(scale * ar[p], scale * ai[p]);
+    else atomicAdd(&y_near[i].x, scale * ar[p]), atomicAdd(&y_near[i].y, scale * ai[p]);
   }
+}
+
+// Deterministic mode: y_near[i] = sum over the partials of point i in the order of its list.
+__global__ void p2p_reduce_kernel(const double2 *__restrict__ part, const int64_t *__restrict__ row_ptr,
+                                  const int64_t *__restrict__ idx, int64_t n, double2 *__restrict__ y_near) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      const double2 v = part[idx[e]];
+      acc.x += v.x, acc.y += v.y;
+    }
+    y_near[i] = acc;
+  }
+}
+
+void launch_p2p_reduce(const double2 *part, const int64_t *row_ptr, const int64_t *idx, int64_t n, double2 *y_near,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  p2p_reduce_kernel<<<blocks, 256, 0, s>>>(part, row_ptr, idx, n, y_near);
 }
 
 template <int PT, int MINB>
 static void launch_p2p_items_t(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
-                               const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s) {
+                               const double dummy_t[3], const double dummy_s[3], double2 *y_near, double2 *part,
+                               const int64_t *slot, cudaStream_t s) {
   if (kind == P2P_SYM || kind == P2P_DSYM) {
     auto kern = kind == P2P_SYM ? p2p_sym_kernel<false, PT, MINB> : p2p_sym_kernel<true, PT, MINB>;
     kern<<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
-                                             make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near);
+                                             make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near, part, slot);
   }
   else if (kind == P2P_DIAG)
-    p2p_ord_kernel<true, PT, MINB><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
+    p2p_ord_kernel<true, PT, MINB><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near, part, slot);
   else
-    p2p_ord_kernel<false, PT, MINB><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near);
+    p2p_ord_kernel<false, PT, MINB><<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, y_near, part, slot);
 }
 
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
-                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt) {
+                      const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt,
+                      double2 *part, const int64_t *slot) {
   if (nitems <= 0) return;
   if (pt == 3)
-    launch_p2p_items_t<3, 4>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, s);
+    launch_p2p_items_t<3, 4>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
   else
-    launch_p2p_items_t<4, HFMM_P2P_MINB>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, s);
+    launch_p2p_items_t<4, HFMM_P2P_MINB>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -367,3 +367,28 @@ def test_m2l_kernels_agree(hf, kind, monkeypatch):
     plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=g.info()["source_level"])
     y_or = OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q)
     assert rel(y, y_or) <= PARITY
+
+
+@pytest.mark.parametrize("case", ["small", "deep", "cube"])
+def test_deterministic_near_field(hf, case):
+    """HFMM_DETERMINISTIC: the P2P items write partial sums to their own slots and every point sums
+    them in a fixed order -- repeated matvecs are bitwise equal, and equal to the atomic default
+    up to summation order (1e-14) and to the oracle (1e-11)."""
+    import torch
+    cfgs = {"small": (small_config("det_s", n=777, kappa=32 * math.pi, depth=3, eps=1e-6, seed=21), 0),
+            "deep": (small_config("det_d", n=3000, kappa=16 * math.pi, depth=5, eps=1e-6, seed=5),
+                     hf.HFMM_SOURCE_AT_DEPTH),
+            "cube": (small_config("det_c", kind="cube", n=1001, kappa=24 * math.pi, depth=3, eps=1e-6, seed=5), 0)}
+    cfg, flags = cfgs[case]
+    x, q = points_and_charges(cfg)
+    g = gpu_plan(hf, cfg, x, flags=flags)
+    gd = gpu_plan(hf, cfg, x, flags=flags | hf.HFMM_DETERMINISTIC)
+    qd = torch.from_numpy(q).cuda()
+    y1, y2 = gd.matvec(qd), gd.matvec(qd)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert gd.info()["launches"] == g.info()["launches"] + 1
+    y0 = g.matvec(qd)
+    assert rel(y1.cpu().numpy(), y0.cpu().numpy()) <= 1e-14
+    plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=g.info()["source_level"])
+    assert rel(y1.cpu().numpy(), OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q)) <= PARITY
