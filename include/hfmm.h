@@ -67,10 +67,13 @@ extern "C" {
                                       levels); default: source level D_s by the policy below */
 #define HFMM_RAGGED 0x20u          /* ragged quadrature on the active levels (R-15, Alg. 3 per row;
                                       SURVEY 8f NEXT 2); default: rectangular N_phi (R-4)    */
-#define HFMM_DETERMINISTIC 0x40u   /* bitwise-reproducible near field: every P2P work item writes its
-                                      row / column partial sums to its own slots (no atomics) and
-                                      each point sums its partials in a fixed order; ~1 GB of
-                                      partials for C4 */
+#define HFMM_DETERMINISTIC 0x40u   /* bitwise-reproducible near field (the DEFAULT; kept as an explicit
+                                      request): every P2P work item writes its row / column partial
+                                      sums to its own slots (no atomics) and each point sums its
+                                      partials in a fixed order -- C4: +0.2% time, ~1.5 GB of
+                                      partials and indices (C5: ~20 GB)                        */
+#define HFMM_ATOMIC_NEAR 0x80u     /* opt out of the above: P2P partial sums added with atomics
+                                      (no partial buffers; repeat runs agree to ~1e-16 only)   */
 #define HFMM_SOURCE_AT_DEPTH 0x10u /* S2M / L2T at the configured depth D.  Default policy
                                       (R-14): the deepest level <= D whose occupied
                                       boxes hold >= 8 points on average; levels L_f < l <= D_s

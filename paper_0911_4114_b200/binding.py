@@ -26,6 +26,7 @@ HFMM_SOURCE_AT_LF = 0x8
 HFMM_SOURCE_AT_DEPTH = 0x10
 HFMM_RAGGED = 0x20
 HFMM_DETERMINISTIC = 0x40
+HFMM_ATOMIC_NEAR = 0x80
 HFMM_HOST = 0
 HFMM_DEVICE = 1
 HFMM_Y_LOCAL = 2

@@ -875,10 +875,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       sorted_items[k] = std::move(sorted);
       p->p2p_nitems[k] = m;
     }
-    // deterministic accumulation (HFMM_DETERMINISTIC): every item writes its row (and, for the
+    // deterministic accumulation (default; HFMM_ATOMIC_NEAR opts out): every item writes its row (and, for the
     // symmetric kernels, column) partial sums into its own slots; point i then sums its partials
     // in a fixed order (kinds in launch order, items in launch order, rows before columns)
-    if (flags & HFMM_DETERMINISTIC) {
+    if (!(flags & HFMM_ATOMIC_NEAR)) {   // default (HFMM_DETERMINISTIC); +0.2% on C4, bitwise repeatable
       std::vector<int64_t> slot[3];
       int64_t off = 0;
       for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD}) {
@@ -976,7 +976,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
   in.source_level = p->D_s;
   {  // kernel launches of one matvec (run_matvec): permute, P2P kinds, far chain, combine
-    int nl = 2 + ((flags & HFMM_DETERMINISTIC) ? 1 : 0), n4 = 0;   // + the partial-sum reduction
+    int nl = 2 + ((flags & HFMM_ATOMIC_NEAR) ? 0 : 1), n4 = 0;   // + the partial-sum reduction
     for (int k = 0; k < 3; ++k) nl += p->p2p_nitems[k] > 0 ? 1 : 0;
     if (p->L_f >= 2) {
       for (int l = p->D_s; l > 2; --l) {          // M2M: rows + cols pass per level (or one pass)
