@@ -72,9 +72,17 @@ __device__ __forceinline__ double2 cexpi_prod(double a, double b, const double2 
 }
 
 // 1/sqrt(r2) for r2 > 0: hardware approximation of the high word, one cubic Newton step.
+// HFMM_P2P_RSQ32 (A/B): seed from the FP32 MUFU.RSQ of the rounded r2 instead of MUFU.RSQ64H.
+#ifndef HFMM_P2P_RSQ32
+#define HFMM_P2P_RSQ32 0
+#endif
 __device__ __forceinline__ double rsqrt_fast(double r2) {
   double y;
+#if HFMM_P2P_RSQ32
+  y = (double)rsqrtf(__double2float_rn(r2));
+#else
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+#endif
   const double e = fma(-r2, y * y, 1.0);
   return fma(y * e, fma(e, 0.375, 0.5), y);
 }

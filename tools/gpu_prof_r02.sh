@@ -7,10 +7,11 @@ mkdir -p gpurun_out
 python bench.py --steps 5 --warmup 3 --ops "" --extra "" > gpurun_out/r02_bench_plain.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_launches_c4.csv \
   python bench.py --steps 2 --warmup 3 --ops "" --extra "" --no-cpu-baseline > gpurun_out/r02_ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"p2p_sym_kernel<0" -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:p2p_sym_kernel -s 6 -c 1 \
   -o gpurun_out/r02_p2p_sym python bench.py --steps 1 --warmup 3 --ops "" --extra "" --no-cpu-baseline > gpurun_out/r02_ncu_p2p.log 2>&1
 ncu -i gpurun_out/r02_p2p_sym.ncu-rep --page raw --csv > gpurun_out/r02_p2p_sym_raw.csv 2>/dev/null
 ncu -i gpurun_out/r02_p2p_sym.ncu-rep --page details --csv > gpurun_out/r02_p2p_sym_details.csv 2>/dev/null
+ncu -i gpurun_out/r02_p2p_sym.ncu-rep --page source --csv --print-source sass > gpurun_out/r02_p2p_sym_source_sass.csv 2>/dev/null
 OPS='import sys; sys.path.insert(0, "."); import bench; print(bench.bench_operators([64], reps=1))'
 python -c "$OPS" > gpurun_out/r02_ops_plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"m2l_dense|rows2_kernel|cols2_kernel" -s 3 -c 5 \
