@@ -72,7 +72,9 @@ __device__ __forceinline__ double2 cexpi_prod(double a, double b, const double2 
 }
 
 // 1/sqrt(r2) for r2 > 0: hardware approximation of the high word, one cubic Newton step.
-// HFMM_P2P_RSQ32 (A/B): seed from the FP32 MUFU.RSQ of the rounded r2 instead of MUFU.RSQ64H.
+// HFMM_P2P_RSQ32 (A/B): seed from the FP32 MUFU.RSQ of the rounded r2 instead of MUFU.RSQ64H --
+// slower (C4 70.2 vs 68.2 ms: the two F2F conversions cost more than the 64-bit MUFU seed;
+// profiles/r02/p2p_rsq32_ab.txt).
 #ifndef HFMM_P2P_RSQ32
 #define HFMM_P2P_RSQ32 0
 #endif

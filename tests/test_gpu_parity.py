@@ -323,6 +323,18 @@ def test_edge_cases(hf):
     g.build_tree(x, 2, (-1, -1, -1), 2.0)
     with pytest.raises(hf.HFMMError):
         g.precompute(-1.0, 1e-6)
+    # the binding rejects vectors the library would read / write out of bounds
+    import torch
+    g.precompute(7.0, 1e-6)
+    qd = torch.tensor([1 + 0j, 2 + 0j], dtype=torch.complex128, device="cuda")
+    for bad in (qd.to(torch.complex64), torch.zeros(3, dtype=torch.complex128, device="cuda"),
+                torch.zeros(4, dtype=torch.complex128, device="cuda")[::2], np.zeros(2, dtype=np.complex64),
+                np.zeros(3, dtype=np.complex128)):
+        with pytest.raises(hf.HFMMError):
+            g.matvec(bad)
+    with pytest.raises(hf.HFMMError):
+        g.matvec(qd, out=torch.empty(2, dtype=torch.complex128))          # host out for a device q
+    assert np.allclose(g.matvec(qd).cpu().numpy(), [2 * e, e], rtol=1e-14)
 
 
 @pytest.mark.parametrize("up", [True, False])
