@@ -47,6 +47,9 @@ constexpr int M2LG_KC = 32;       // directions per chunk (lanes)
 #ifndef HFMM_M2L_SPLIT
 #define HFMM_M2L_SPLIT 0  // parent-block kernel: real/imaginary halves of each MAC in separate accumulators
 #endif
+#ifndef HFMM_M2L_L1PF
+#define HFMM_M2L_L1PF 0  // parent-block kernel: prefetch the next neighbour parent's sources into L1
+#endif
 #ifndef HFMM_M2L_DPF
 #define HFMM_M2L_DPF 0  // parent-block kernel: prefetch the next neighbour parent's sources
 #endif
@@ -205,6 +208,16 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
       while (D < 27) {
         const uint32_t rest = mask & ~((2u << D) - 1u);
         const int Dn = rest ? __ffs(rest) - 1 : 27;
+#if HFMM_M2L_L1PF
+        if (Dn < 27 && kval) {  // the next parent's sources into L1 while this parent's MACs run
+          const int4 *sp = reinterpret_cast<const int4 *>(gsrc + (g * 27 + Dn) * 8);
+          const int4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+          const int32_t sid[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (sid[e] >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(&M[(int64_t)sid[e] * K + k]));
+        }
+#endif
 #if HFMM_M2L_DPF
         double2 mn[8];
         if (Dn < 27) load8(Dn, mn);
