@@ -626,7 +626,8 @@ def main():
         "stages_ms": {k: statistics.mean(v) for k, v in stage.items()},
         "plan": {"L_f": L_f, "source_level": info["source_level"],
                  "levels": [{k: lv[k] for k in ("level", "ell", "n_theta", "n_phi", "F", "active")}
-                            for lv in info["levels"]], "p2p_pairs": pairs, "s2m_evals": info["s2m_evals"]},
+                            for lv in info["levels"]], "p2p_pairs": pairs, "s2m_evals": info["s2m_evals"],
+                 "p2p_tile": info["p2p_tile"]},
         "setup_s": {"build_tree": t_tree, "precompute": t_pre},
         "clocks": clocks,
     }

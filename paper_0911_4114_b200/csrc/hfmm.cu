@@ -145,7 +145,7 @@ struct hfmm_plan {
   int64_t dir_nitems = 0;
   double *ux = nullptr, *uy = nullptr, *uz = nullptr;
   double uscale = 0;               // kappa TAB_STEPS / (2 pi)
-  int p2p_pt = 4;                  // targets per thread of the P2P kernels (tile = 128 x p2p_pt)
+  int p2p_pt = 4;                  // targets per thread of the P2P kernels (tile = 128 x p2p_pt: 3, 4 or 8)
   int64_t p2p_sym_pairs = 0;
   double dummy_t[3] = {0, 0, 0}, dummy_s[3] = {0, 0, 0};
   double2 *tmp = nullptr;
@@ -840,17 +840,25 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     // Per-plan tile (load balance): 4 targets per thread (512-point tiles, 3 CTAs / SM) unless
     // that leaves fewer than ~10 waves of items over the GPU, then 3 per thread (384-point tiles,
     // 4 CTAs / SM): the tail of a short grid costs more than the slightly lower per-item rate
-    // (C3: 11% faster; C4 / C5 keep 512, same-box A/B profiles/r01/p2p_occupancy_ab_r26.txt)
-    p->p2p_pt = 4;
-    build_items();
+    // (C3: 11% faster; C4 / C5 keep 512, same-box A/B profiles/r01/p2p_occupancy_ab_r26.txt).
+    // HFMM_P2P_PT = 3 / 4 / 8 forces a tile (A/B).  8 targets per thread (1,024-point tiles, 2
+    // CTAs / SM) needs fewer FP64 issue slots per evaluation (37.4 vs 38.7 by
+    // tools/sass_fp64_cost.py, +3.4% on the uniform-item rig profiles/r02/p2p_ablate2.txt) but is
+    // slower on the matvec configs (C4 71.8 vs 68.1 ms, C5 851 vs 758 ms,
+    // profiles/r02/pt_ab.txt): opt-in only.
     {
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-      const int64_t nit = (int64_t)(it[0].size() + it[1].size() + it[2].size()) / 4;
-      if (nit < 10 * 3 * (int64_t)nsm) {
-        p->p2p_pt = 3;
-        tile = (int64_t)P2P_TPB_HOST * 3;
+      int force = 0;
+      if (const char *e = getenv("HFMM_P2P_PT")) force = atoi(e);
+      const int cand[3] = {8, 4, 3}, ctas[3] = {2, 3, 4};
+      for (int c = force == 8 ? 0 : 1; c < 3; ++c) {
+        if ((force == 3 || force == 4 || force == 8) && cand[c] != force) continue;
+        p->p2p_pt = cand[c];
+        tile = (int64_t)P2P_TPB_HOST * cand[c];
         build_items();
+        const int64_t nit = (int64_t)(it[0].size() + it[1].size() + it[2].size()) / 4;
+        if (cand[c] == force || nit >= 10 * ctas[c] * (int64_t)nsm) break;
       }
     }
     // longest items first (LPT order against the tail of the grid)

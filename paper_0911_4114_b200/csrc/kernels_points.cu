@@ -78,6 +78,9 @@ __device__ __forceinline__ double2 cexpi_prod(double a, double b, const double2 
 #ifndef HFMM_P2P_RSQ32
 #define HFMM_P2P_RSQ32 0
 #endif
+#ifndef HFMM_RSQ_FORM
+#define HFMM_RSQ_FORM 1
+#endif
 __device__ __forceinline__ double rsqrt_fast(double r2) {
   double y;
 #if HFMM_P2P_RSQ32
@@ -86,7 +89,11 @@ __device__ __forceinline__ double rsqrt_fast(double r2) {
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
 #endif
   const double e = fma(-r2, y * y, 1.0);
+#if HFMM_RSQ_FORM == 0
   return fma(y * e, fma(e, 0.375, 0.5), y);
+#else
+  return y * fma(e, fma(e, 0.375, 0.5), 1.0);   // every DFMA reads <= 2 vector registers
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -103,7 +110,7 @@ __device__ __forceinline__ double rsqrt_fast(double r2) {
 // ---------------------------------------------------------------------------------------------
 constexpr int P2P_TPB = P2P_THREADS;
 // PT = targets per thread (tile = PT * P2P_TPB), MINB = resident CTAs per SM asked of ptxas;
-// instantiated as (4, HFMM_P2P_MINB) and (3, 4) -- the plan picks one per matvec (hfmm.cu)
+// instantiated as (8, 1), (4, HFMM_P2P_MINB) and (3, 4) -- the plan picks one per matvec (hfmm.cu)
 
 __device__ __forceinline__ double2 green_u(double tx, double ty, double tz, double xs, double ys, double zs,
                                            const double2 *tab) {
@@ -320,6 +327,8 @@ void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kin
   if (nitems <= 0) return;
   if (pt == 3)
     launch_p2p_items_t<3, 4>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
+  else if (pt == 8)
+    launch_p2p_items_t<8, 1>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
   else
     launch_p2p_items_t<4, HFMM_P2P_MINB>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
 }

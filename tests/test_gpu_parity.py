@@ -403,3 +403,33 @@ def test_deterministic_near_field(hf, case):
     plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=gd.info()["source_level"])
     yo = OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q)
     assert rel(y1.cpu().numpy(), yo) <= PARITY and rel(y0.cpu().numpy(), yo) <= PARITY
+
+
+# ---- P2P tile per plan: 384 / 512 / 1,024-point target tiles -------------------
+@pytest.mark.parametrize("pt", [3, 4, 8])
+@pytest.mark.parametrize("case", ["fmm", "nofar"])
+def test_p2p_tiles_agree(hf, pt, case, monkeypatch):
+    """Every P2P instantiation the plan can pick (3, 4 or 8 targets per thread; forced with
+    HFMM_P2P_PT) gives the oracle's matvec.  "nofar": no admissible level, so the matvec is
+    the near field over the whole point set -- several 1,024-point tiles, a ragged last tile,
+    symmetric tile pairs and diagonal tiles; "fmm": leaves smaller than a tile (partial tiles).
+    The all-pairs entry point (hfmm_direct) with the same tile == the oracle's direct sum."""
+    if case == "nofar":
+        cfg = small_config("p2p_pt_nofar", n=3001, kappa=2 * math.pi, depth=3, eps=1e-4, seed=31)
+    else:
+        cfg = small_config("p2p_pt_fmm", n=6000, kappa=8 * math.pi, depth=3, eps=1e-6, seed=31)
+    x, q = points_and_charges(cfg)
+    monkeypatch.setenv("HFMM_P2P_PT", str(pt))
+    g = gpu_plan(hf, cfg, x)
+    monkeypatch.delenv("HFMM_P2P_PT")
+    assert g.info()["p2p_tile"] == 128 * pt
+    y, yd = g.matvec(q), g.direct(q)
+    yref = direct_sum(x, q, cfg.kappa)
+    assert rel(yd, yref) <= PARITY
+    if case == "nofar":
+        assert (g.info()["L_f"] or 0) < 2
+        assert rel(y, yref) <= PARITY
+    else:
+        plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha,
+                         source_level=g.info()["source_level"])
+        assert rel(y, OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q)) <= PARITY
