@@ -108,6 +108,11 @@ typedef struct {
   int ragged;       /* 1: ragged rows N_phi(theta_n) (R-15, HFMM_RAGGED); K = stored points   */
   int m2l_block;    /* 1: M2L runs the parent-block kernel, 0: the merged-list kernel (both
                        compute exactly the interaction-list sum; M2L)             */
+  int halo;         /* multi-rank: 1 if M_l is exchanged as M2L halos (grouped ncclSend /
+                       ncclRecv of the peers' boxes in this rank's interaction lists; levels
+                       >= HFMM_HALO_LEVEL, default 4), 0 if all-gathered                      */
+  int64_t m_recv_boxes; /* multi-rank: boxes of M_l this rank receives per matvec (0: one rank) */
+  int64_t m_send_boxes; /* multi-rank: boxes of M_l this rank sends per matvec (sum over peers)  */
 } hfmm_level_info;
 
 typedef struct {

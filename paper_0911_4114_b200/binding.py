@@ -49,7 +49,8 @@ class LevelInfo(C.Structure):
                 ("n_phi", C.c_int), ("alpha", C.c_double), ("K", C.c_int64), ("F", C.c_double),
                 ("active", C.c_int),
                 ("boxes", C.c_int64), ("m2l_pairs", C.c_int64), ("rep", C.c_int), ("ragged", C.c_int),
-                ("m2l_block", C.c_int)]
+                ("m2l_block", C.c_int), ("halo", C.c_int), ("m_recv_boxes", C.c_int64),
+                ("m_send_boxes", C.c_int64)]
 
 
 class Info(C.Structure):
@@ -300,7 +301,9 @@ class HFMM:
             levels.append(dict(level=lv.level, a=lv.a, ell=lv.ell, n_theta=lv.n_theta, n_phi=lv.n_phi,
                                alpha=lv.alpha, K=lv.K,
                                F=lv.F, active=bool(lv.active), boxes=lv.boxes, m2l_pairs=lv.m2l_pairs,
-                               rep=bool(lv.rep), ragged=bool(lv.ragged), m2l_block=bool(lv.m2l_block)))
+                               rep=bool(lv.rep), ragged=bool(lv.ragged), m2l_block=bool(lv.m2l_block),
+                               halo=bool(lv.halo), m_recv_boxes=int(lv.m_recv_boxes),
+                               m_send_boxes=int(lv.m_send_boxes)))
         return dict(n=inf.n, depth=inf.depth, L_f=(None if inf.L_f < 0 else inf.L_f), kappa=inf.kappa,
                     eps=inf.eps, alpha=inf.alpha, tau=inf.tau, levels=levels, p2p_pairs=inf.p2p_pairs,
                     p2p_sym_pairs=inf.p2p_sym_pairs,

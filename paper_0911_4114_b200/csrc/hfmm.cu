@@ -51,6 +51,13 @@ struct LevelDev {
   int64_t nbox = 0;
   int64_t own0 = 0, own1 = 0;  // owned box range (Morton order)
   std::vector<int64_t> rlo, rhi; // every rank's owned range (for the all-gather)
+  // M2L halo (levels >= HFMM_HALO_LEVEL of a multi-rank plan): instead of the all-gather of M_l,
+  // rank r receives from each peer q exactly the q-owned boxes in the interaction lists of its
+  // owned boxes (sorted box ids; both sides derive the same lists from the replicated tree)
+  bool halo = false;
+  std::vector<int64_t> hs_off, hr_off;        // [R + 1] offsets of the send / receive lists by peer
+  int64_t *hs_idx = nullptr, *hr_idx = nullptr;  // box ids: sent (owned) / received (peers')
+  double2 *hs_buf = nullptr, *hr_buf = nullptr;  // packed [count][K]
   double *cx = nullptr, *cy = nullptr, *cz = nullptr;
   double *ks = nullptr;          // kappa s [3][K]
   double2 *T = nullptr;          // [34][K]: the canonical transfer vectors x >= y >= 0, z >= 0
@@ -193,7 +200,8 @@ static void free_levels(hfmm_plan *p) {
     L.m2lg = nullptr;
     for (void *ptr : {(void *)L.cx, (void *)L.cy, (void *)L.cz, (void *)L.ks, (void *)L.T, (void *)L.M,
                       (void *)L.I, (void *)L.L, (void *)L.perm, (void *)L.rows_d, (void *)L.off_d, (void *)L.wk,
-                      (void *)L.parent, (void *)L.oct, (void *)L.cbeg, (void *)L.shift})
+                      (void *)L.parent, (void *)L.oct, (void *)L.cbeg, (void *)L.shift, (void *)L.hs_idx,
+                      (void *)L.hr_idx, (void *)L.hs_buf, (void *)L.hr_buf})
       if (ptr) cudaFree(ptr);
   }
   p->lv.clear();
@@ -456,6 +464,14 @@ static void symmetry_perms_ragged(const LevelDev &L, std::vector<int32_t> &perm)
     }
 }
 
+// Levels l >= this exchange M2L halos instead of all-gathering M_l (multi-rank plans).  Default 4:
+// the coarse top levels (2, 3) are replicated by the all-gather; read at every
+// precompute so a test can move it (HFMM_HALO_LEVEL=2: every active level as halos).
+static int halo_min_level() {
+  const char *e = getenv("HFMM_HALO_LEVEL");
+  return e ? atoi(e) : 4;
+}
+
 static void partition(hfmm_plan *p) {
   // Ownership by contiguous Morton ranges of level-2 subtrees (or of points if no far field),
   // balanced by an estimate of FP64 work: P2P pairs + S2M/L2T evaluations.  Every rank
@@ -705,6 +721,45 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       row.push_back((int32_t)src.size());
     }
     L.il_nnz = (int64_t)src.size();
+    if (L.active && p->nranks > 1 && l >= halo_min_level()) {
+      // halo lists: recv[q] = q-owned sources of my owned targets, send[q] = my owned sources of
+      // q's owned targets (sorted, unique: the receiver and the sender build the same list)
+      const int R = p->nranks;
+      auto owner = [&](int64_t b) {
+        for (int q = 0; q < R; ++q)
+          if (b >= L.rlo[q] && b < L.rhi[q]) return q;
+        return -1;
+      };
+      std::vector<std::vector<int64_t>> snd(R), rcv(R);
+      for (int q = 0; q < R; ++q)
+        for (int64_t b = L.rlo[q]; b < L.rhi[q]; ++b)
+          for (int32_t e = row[b]; e < row[b + 1]; ++e) {
+            const int64_t sb = src[e];
+            const int o = owner(sb);
+            if (o < 0 || o == q) continue;
+            if (q == p->rank) rcv[o].push_back(sb);
+            else if (o == p->rank) snd[q].push_back(sb);
+          }
+      L.hs_off.assign(R + 1, 0), L.hr_off.assign(R + 1, 0);
+      std::vector<int64_t> hs, hr;
+      for (int q = 0; q < R; ++q) {
+        for (auto *v : {&snd[q], &rcv[q]}) {
+          std::sort(v->begin(), v->end());
+          v->erase(std::unique(v->begin(), v->end()), v->end());
+        }
+        hs.insert(hs.end(), snd[q].begin(), snd[q].end());
+        hr.insert(hr.end(), rcv[q].begin(), rcv[q].end());
+        L.hs_off[q + 1] = (int64_t)hs.size(), L.hr_off[q + 1] = (int64_t)hr.size();
+      }
+      L.halo = true;
+      L.hs_idx = dupload(hs), L.hr_idx = dupload(hr);
+      L.hs_buf = dalloc<double2>(hs.size() * (size_t)L.K);
+      L.hr_buf = dalloc<double2>(hr.size() * (size_t)L.K);
+      if ((!hs.empty() && (!L.hs_idx || !L.hs_buf)) || (!hr.empty() && (!L.hr_idx || !L.hr_buf))) {
+        p->err = "hfmm_precompute: allocation failed (M2L halo buffers)";
+        return HFMM_E_NOMEM;
+      }
+    }
     if (L.active) {
       std::vector<int32_t> pm;
       if (L.ragged) symmetry_perms_ragged(L, pm);
@@ -980,6 +1035,16 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     li.rep = L.rep ? 1 : 0;
     li.ragged = L.ragged ? 1 : 0;
     li.m2l_block = (L.m2lg && m2l_group_plan_kind(L.m2lg) == 1) ? 1 : 0;
+    li.halo = L.halo ? 1 : 0;
+    li.m_recv_boxes = li.m_send_boxes = 0;
+    if (L.active && p->nranks > 1) {
+      if (L.halo) {
+        li.m_recv_boxes = L.hr_off.back(), li.m_send_boxes = L.hs_off.back();
+      } else {
+        li.m_recv_boxes = L.nbox - (L.own1 - L.own0);
+        li.m_send_boxes = (L.own1 - L.own0) * (p->nranks - 1);
+      }
+    }
   }
   in.s2m_evals = p->L_f >= 2 ? (p->own_pt1 - p->own_pt0) * p->lv[p->D_s].K : 0;
   in.source_level = p->D_s;
@@ -1038,6 +1103,23 @@ static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
     CKN(ncclBroadcast(buf, buf, cnt, ncclDouble, r, p->comm, s));
   }
   CKN(ncclGroupEnd());
+  return HFMM_OK;
+}
+
+// M2L halo of one level: grouped point-to-point sends of the packed owned boxes each peer needs and
+// receives of the peers' boxes this rank needs, then one scatter into M_l
+static int halo_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
+  if (p->nranks <= 1) return HFMM_OK;
+  NvtxRange nv("hfmm:halo M_l");
+  CKN(ncclGroupStart());
+  for (int q = 0; q < p->nranks; ++q) {
+    if (q == p->rank) continue;
+    const size_t ns = (size_t)(L.hs_off[q + 1] - L.hs_off[q]) * L.K * 2, nr = (size_t)(L.hr_off[q + 1] - L.hr_off[q]) * L.K * 2;
+    if (ns) CKN(ncclSend((const double *)(L.hs_buf + L.hs_off[q] * L.K), ns, ncclDouble, q, p->comm, s));
+    if (nr) CKN(ncclRecv((double *)(L.hr_buf + L.hr_off[q] * L.K), nr, ncclDouble, q, p->comm, s));
+  }
+  CKN(ncclGroupEnd());
+  if (L.hr_off.back() > 0) launch_gather_boxes(L.hr_buf, nullptr, L.M, L.hr_idx, L.hr_off.back(), L.K, s);
   return HFMM_OK;
 }
 
@@ -1111,6 +1193,12 @@ static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool 
         }
       }
     }
+  }
+  // M2L halos: pack the owned boxes every peer needs (sorted lists) before the exchange
+  for (int l = 2; l <= p->L_f; ++l) {
+    const LevelDev &L = p->lv[l];
+    if (L.halo && L.hs_off.back() > 0)
+      launch_gather_boxes(L.M, L.hs_idx, L.hs_buf, nullptr, L.hs_off.back(), L.K, p->stream_hi);
   }
   CK(cudaEventRecord(p->ev_up, p->stream_hi));
   return HFMM_OK;
@@ -1192,7 +1280,7 @@ static int run_matvec(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, b
   int rc = run_up(p, q_dev, s_user, serial);
   if (rc) return rc;
   for (int l = 2; l <= p->L_f; ++l) {
-    rc = allgather_level(p, p->lv[l], p->stream_hi);
+    rc = p->lv[l].halo ? halo_level(p, p->lv[l], p->stream_hi) : allgather_level(p, p->lv[l], p->stream_hi);
     if (rc) return rc;
   }
   return run_down(p, s_user, sorted_out);
@@ -1342,6 +1430,16 @@ extern "C" int hfmm_vgroup_matvec(hfmm_vgroup *g, const double *q, double *y, vo
       if (cudaStreamWaitEvent(p->stream_hi, src->ev_up, 0) != cudaSuccess) return HFMM_E_CUDA;
       for (int l = 2; l <= p->L_f; ++l) {
         LevelDev &L = p->lv[l], &S = src->lv[l];
+        if (L.halo != S.halo) return HFMM_E_STATE;
+        if (L.halo) {  // the peer's packed send segment for rank r -> rank r's receive segment from rr
+          const int64_t cnt = L.hr_off[rr + 1] - L.hr_off[rr];
+          if (cnt != S.hs_off[r + 1] - S.hs_off[r]) return HFMM_E_STATE;
+          if (cnt > 0 &&
+              cudaMemcpyAsync(L.hr_buf + L.hr_off[rr] * L.K, S.hs_buf + S.hs_off[r] * S.K,
+                              (size_t)cnt * L.K * sizeof(double2), cudaMemcpyDeviceToDevice, p->stream_hi) != cudaSuccess)
+            return HFMM_E_CUDA;
+          continue;
+        }
         const int64_t b0 = L.rlo[rr], b1 = L.rhi[rr];
         if (b1 > b0 &&
             cudaMemcpyAsync(L.M + b0 * L.K, S.M + b0 * S.K, (size_t)(b1 - b0) * L.K * sizeof(double2),
@@ -1350,6 +1448,12 @@ extern "C" int hfmm_vgroup_matvec(hfmm_vgroup *g, const double *q, double *y, vo
       }
     }
   }
+  for (hfmm_plan *p : g->plans)  // scatter the received halos into M_l
+    for (int l = 2; l <= p->L_f; ++l) {
+      LevelDev &L = p->lv[l];
+      if (L.halo && L.hr_off.back() > 0)
+        launch_gather_boxes(L.hr_buf, nullptr, L.M, L.hr_idx, L.hr_off.back(), L.K, p->stream_hi);
+    }
   for (hfmm_plan *p : g->plans) {
     int rc = run_down(p, s, true);
     if (rc) return rc;

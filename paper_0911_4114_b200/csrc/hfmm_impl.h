@@ -95,6 +95,9 @@ struct TwiddleSet {
 
 void launch_permute_q(const double2 *q_in, const int64_t *perm, double2 *q_sorted, int64_t n,
                       cudaStream_t s);
+// out[(oidx ? oidx[i] : i)][k] = in[(iidx ? iidx[i] : i)][k] for i < count, k < K (M2L halo pack / scatter)
+void launch_gather_boxes(const double2 *in, const int64_t *iidx, double2 *out, const int64_t *oidx, int64_t count,
+                         int64_t K, cudaStream_t s);
 void launch_combine(const double2 *y_near, const double2 *y_far, const int64_t *perm,
                     double2 *y_out, int64_t n, int64_t begin, int64_t end, cudaStream_t s);
 

@@ -66,6 +66,13 @@ __device__ __forceinline__ double2 g_cfma(double2 a, double2 b, double2 c) {
 // or -1 for the 27 adjacent offsets |o|_inf <= 1 (parent-block kernel: their tables are zero)
 constexpr int M2LB_SLOTS = 343;
 __constant__ int16_t c_slot_id[M2LB_SLOTS];
+#ifndef HFMM_M2L_SKIP
+#define HFMM_M2L_SKIP 0  // parent-block kernel: skip the zero tables of adjacent slots (warp-uniform branch;
+                         // A/B: B64 50.0 vs 41.8 ms, the branches split the scheduled MAC stream -> off)
+#endif
+// c_zero_dl[D] bit dl: neighbour parent D = (Dx,Dy,Dz) + 1 in base 3 and child offset delta = e - d
+// (dl in base 3) give an adjacent offset 2D + delta (|.|_inf <= 1), whose table is zero
+__constant__ uint32_t c_zero_dl[27];
 
 __device__ __forceinline__ void fill_tables(double2 *Ts, const double2 *__restrict__ T, const int32_t *__restrict__ perm,
                                             int64_t K, int64_t k0) {
@@ -225,9 +232,15 @@ __global__ void __launch_bounds__(32 * M2LG_WARPS, 1) m2l_dense_kernel(
         // T[2D + delta] = Tb[delta slot offset]: base at cube position 2D + (-1,-1,-1)
         const int Dx = D / 9 - 1, Dy = (D / 3) % 3 - 1, Dz = D % 3 - 1;
         const double2 *Tb = Ts + ((2 * Dx + 2) * 49 + (2 * Dy + 2) * 7 + (2 * Dz + 2)) * M2LG_KC + lane;
+#if HFMM_M2L_SKIP
+        const uint32_t zm = c_zero_dl[D];  // warp-uniform: bit dl set when slot 2D + delta is adjacent
+#endif
 #pragma unroll
         for (int dl = 0; dl < 27; ++dl) {
           const int dx = dl / 9 - 1, dy = (dl / 3) % 3 - 1, dz = dl % 3 - 1;
+#if HFMM_M2L_SKIP
+          if ((zm >> dl) & 1u) continue;  // zero table: skip its load and its MACs
+#endif
           const double2 t = Tb[((dx + 1) * 49 + (dy + 1) * 7 + (dz + 1)) * M2LG_KC];
 #pragma unroll
           for (int d = 0; d < 8; ++d) {
@@ -492,6 +505,18 @@ static void upload_slot_table() {
     t[sl] = (int16_t)(adm ? offset_id(o[0], o[1], o[2]) : -1);
   }
   cudaMemcpyToSymbol(c_slot_id, t, sizeof(t));
+  uint32_t z[27];
+  for (int D = 0; D < 27; ++D) {
+    const int Dc[3] = {D / 9 - 1, (D / 3) % 3 - 1, D % 3 - 1};
+    z[D] = 0;
+    for (int dl = 0; dl < 27; ++dl) {
+      const int dc[3] = {dl / 9 - 1, (dl / 3) % 3 - 1, dl % 3 - 1};
+      bool adj = true;
+      for (int c = 0; c < 3; ++c) adj = adj && std::abs(2 * Dc[c] + dc[c]) <= 1;
+      if (adj) z[D] |= 1u << dl;
+    }
+  }
+  cudaMemcpyToSymbol(c_zero_dl, z, sizeof(z));
   done.insert(d);
 }
 

@@ -2,6 +2,8 @@
 //   Alg.1 bandlimited modified transfer function T^{s,L}, one CTA per (offset, phi column)
 //         (P:508-530); phi-truncation to T^{s,LL} when N_phi < 2 ell + 2
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <cstdint>
 
 #include "hfmm_impl.h"
@@ -161,6 +163,26 @@ __global__ void absmax_kernel(const double2 *__restrict__ v, int64_t n, unsigned
 void launch_absmax(const double2 *v, int64_t n, double *out, cudaStream_t s) {
   cudaMemsetAsync(out, 0, sizeof(double), s);
   absmax_kernel<<<148 * 4, 256, 0, s>>>(v, n, reinterpret_cast<unsigned long long *>(out));
+}
+
+// M2L halo pack / scatter: one CTA row per box (blockIdx.y strided), lanes over k (coalesced)
+__global__ void gather_boxes_kernel(const double2 *__restrict__ in, const int64_t *__restrict__ iidx,
+                                    double2 *__restrict__ out, const int64_t *__restrict__ oidx, int64_t count,
+                                    int64_t K) {
+  for (int64_t i = blockIdx.y; i < count; i += gridDim.y) {
+    const double2 *src = in + (iidx ? iidx[i] : i) * K;
+    double2 *dst = out + (oidx ? oidx[i] : i) * K;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x)
+      dst[k] = src[k];
+  }
+}
+
+void launch_gather_boxes(const double2 *in, const int64_t *iidx, double2 *out, const int64_t *oidx, int64_t count,
+                         int64_t K, cudaStream_t s) {
+  if (count <= 0 || K <= 0) return;
+  const unsigned gx = (unsigned)std::min<int64_t>((K + 255) / 256, 64);
+  const unsigned gy = (unsigned)std::min<int64_t>(count, 65535);
+  gather_boxes_kernel<<<dim3(gx, gy), 256, 0, s>>>(in, iidx, out, oidx, count, K);
 }
 
 }  // namespace hfmm

@@ -89,3 +89,76 @@ def test_virtual_ranks_equal_single_plan(hf, case, R):
     for p in plans:
         p.close()
     g1.close()
+
+
+def _check_group(hf, cfg, src, R, y1, qd):
+    vg = hf.VirtualGroup(R)
+    plans = [plan_for(hf, cfg, x_of(cfg), src, vg, r) for r in range(R)]
+    infos = [p.info() for p in plans]
+    Y = vg.matvec(qd).cpu().numpy()
+    Y2 = vg.matvec(qd).cpu().numpy()          # buffers (halo packs) re-used across matvecs
+    vg.close()
+    for p in plans:
+        p.close()
+    for r in range(R):
+        assert rel(Y[r], y1) <= 1e-13, (cfg.name, R, r, rel(Y[r], y1))
+    assert rel(Y2[0], y1) <= 1e-13
+    return infos
+
+
+def x_of(cfg):
+    return points_and_charges(cfg)[0]
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("R", [2, 8])
+def test_virtual_ranks_halo_every_level(hf, case, R, monkeypatch):
+    """M2L halos instead of the all-gather on every active level (HFMM_HALO_LEVEL=2): each rank
+    receives only the peers' boxes in its owned boxes' interaction lists (sorted lists built
+    independently by sender and receiver), packs / scatters them with the gather kernel, and
+    its y equals the single plan's to 1e-13."""
+    import torch
+    monkeypatch.setenv("HFMM_HALO_LEVEL", "2")
+    cfg, src = CASES[case]
+    x, q = points_and_charges(cfg)
+    g1 = plan_for(hf, cfg, x, src)
+    qd = torch.from_numpy(q).cuda()
+    y1 = g1.matvec(qd).cpu().numpy()
+    lv1 = {lv["level"]: lv for lv in g1.info()["levels"]}
+    g1.close()
+    infos = _check_group(hf, cfg, src, R, y1, qd)
+    for inf in infos:
+        for lv in inf["levels"]:
+            if not lv["active"]:
+                continue
+            assert lv["halo"], (case, R, lv["level"])
+            # a halo never exceeds what the all-gather would deliver (the peers' boxes)
+            assert 0 <= lv["m_recv_boxes"] < lv1[lv["level"]]["boxes"]
+    # every box sent is received by exactly one (rank, peer) list entry: totals agree
+    for l in {lv["level"] for inf in infos for lv in inf["levels"] if lv["active"]}:
+        sent = sum(lv["m_send_boxes"] for inf in infos for lv in inf["levels"] if lv["level"] == l)
+        recv = sum(lv["m_recv_boxes"] for inf in infos for lv in inf["levels"] if lv["level"] == l)
+        assert sent == recv > 0
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_virtual_ranks_halo_default_levels(hf, R, monkeypatch):
+    """Default policy: levels 2-3 all-gathered (replicated top levels), levels >= 4
+    exchanged as halos.  Cube, kappa = 48 pi, eps = 1e-4, depth 5: L_f = 4, so level 4 runs the
+    halo path next to all-gathered levels 2-3."""
+    import torch
+    monkeypatch.delenv("HFMM_HALO_LEVEL", raising=False)
+    cfg = small_config("vr_halo4", kind="cube", n=8000, kappa=48 * math.pi, depth=5, eps=1e-4, seed=9)
+    x, q = points_and_charges(cfg)
+    g1 = plan_for(hf, cfg, x, "lf")
+    assert g1.info()["L_f"] == 4
+    qd = torch.from_numpy(q).cuda()
+    y1 = g1.matvec(qd).cpu().numpy()
+    nbox4 = [lv for lv in g1.info()["levels"] if lv["level"] == 4][0]["boxes"]
+    g1.close()
+    infos = _check_group(hf, cfg, "lf", R, y1, qd)
+    for inf in infos:
+        by = {lv["level"]: lv for lv in inf["levels"]}
+        assert not by[2]["halo"] and not by[3]["halo"] and by[4]["halo"]
+        # the level-4 halo is a fraction of the all-gather volume
+        assert by[4]["m_recv_boxes"] < 0.75 * nbox4, by[4]
