@@ -606,7 +606,7 @@ def main():
         "e2e": {"value": 1e3 / te.item(), "unit": "matvec/s", "h2d_bytes_per_step": cfg.n * 16,
                 "d2h_bytes_per_step": cfg.n * 16,
                 "note": "hfmm_matvec with pinned host q / y: H2D, the matvec, the y gather across ranks "
-                        "(all-reduce) and the D2H inside the timed region"},
+                        "(all-gather of the owned sorted ranges) and the D2H inside the timed region"},
         "gpu_launches": launches,
         "roofline": {"kernel": "p2p", "bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved / peak_tflops, "traffic": traffic,

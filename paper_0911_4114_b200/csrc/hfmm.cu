@@ -893,9 +893,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     }
     };
     // Per-plan tile (load balance): 4 targets per thread (512-point tiles, 3 CTAs / SM) unless
-    // that leaves fewer than ~10 waves of items over the GPU, then 3 per thread (384-point tiles,
-    // 4 CTAs / SM): the tail of a short grid costs more than the slightly lower per-item rate
-    // (C3: 11% faster; C4 / C5 keep 512, same-box A/B profiles/r01/p2p_occupancy_ab_r26.txt).
+    // that leaves fewer than ~10 waves of items over the GPU, or the leaves fill 512-point tiles
+    // poorly (padded slots below), then 3 per thread (384-point tiles, 4 CTAs / SM): the tail of
+    // a short grid costs more than the slightly lower per-item rate (C3: 11% faster; C4 / C5 keep
+    // 512, same-box A/B profiles/r01/p2p_occupancy_ab_r26.txt).
     // HFMM_P2P_PT = 3 / 4 / 8 forces a tile (A/B).  8 targets per thread (1,024-point tiles, 2
     // CTAs / SM) needs fewer FP64 issue slots per evaluation (37.4 vs 38.7 by
     // tools/sass_fp64_cost.py, +3.4% on the uniform-item rig profiles/r02/p2p_ablate2.txt) but is
@@ -907,13 +908,40 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       int force = 0;
       if (const char *e = getenv("HFMM_P2P_PT")) force = atoi(e);
       const int cand[3] = {8, 4, 3}, ctas[3] = {2, 3, 4};
+      // thread-evaluation slots of the items: every thread of a tile evaluates PT targets
+      // (inactive ones at a dummy position) against the sources padded to 32
+      auto padded_slots = [&](int pt) {
+        double sl = 0.0;
+        for (auto &v : it)
+          for (size_t i = 0; i < v.size(); i += 4) sl += (double)P2P_TPB_HOST * pt * (double)((v[i + 3] - v[i + 2] + 31) / 32 * 32);
+        return sl;
+      };
+      double slots4 = 0.0;
       for (int c = force == 8 ? 0 : 1; c < 3; ++c) {
         if ((force == 3 || force == 4 || force == 8) && cand[c] != force) continue;
         p->p2p_pt = cand[c];
         tile = (int64_t)P2P_TPB_HOST * cand[c];
         build_items();
         const int64_t nit = (int64_t)(it[0].size() + it[1].size() + it[2].size()) / 4;
-        if (cand[c] == force || nit >= 10 * ctas[c] * (int64_t)nsm) break;
+        if (cand[c] == force) break;
+        if (cand[c] == 4) {
+          slots4 = padded_slots(4);
+          if (nit >= 10 * ctas[c] * (int64_t)nsm) {
+            // enough waves: keep 512-point tiles unless the leaves fill them poorly -- 384-point
+            // tiles must save > 8% of the padded slots to beat their lower per-slot rate (C4's
+            // 3,676-point leaves: 6.7% fewer slots, measured 1% slower at 384; C5 at eps/10
+            // (~305-point leaves): 512-point tiles are 60% full, 384-point tiles 79%)
+            tile = (int64_t)P2P_TPB_HOST * 3;
+            build_items();
+            if (padded_slots(3) * 1.08 < slots4) {
+              p->p2p_pt = 3;
+              break;
+            }
+            tile = (int64_t)P2P_TPB_HOST * 4;
+            build_items();
+            break;
+          }
+        }
       }
     }
     // longest items first (LPT order against the tail of the grid)

@@ -417,6 +417,20 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
   }
 }
 
+// Resident CTAs per SM asked of ptxas by the register-resident passes (A/B, C2 same box,
+// profiles/r02/rs2_minb_ab.txt): the downward passes and the upward rows pass fit 4 CTAs per SM
+// in shared memory and gain from the extra warps (B32 anterp 5.22 -> 4.67 ms, L2L 7.19 -> 6.04 ms,
+// interp 4.94 -> 4.87 ms); the upward column pass (cp.async staging, 64 KB) stays at 3 per SM,
+// where the 128-register cap only adds spills (B64 interp 16.9 -> 17.5 ms, M2M 20.2 -> 21.8 ms).
+#ifndef HFMM_RS2_MINB_UP
+#define HFMM_RS2_MINB_UP 3
+#endif
+#ifndef HFMM_RS2_MINB_UPROWS
+#define HFMM_RS2_MINB_UPROWS 4
+#endif
+#ifndef HFMM_RS2_MINB_DN
+#define HFMM_RS2_MINB_DN 4
+#endif
 // ---- register-resident two-level resample passes ----------------------------------------------
 // A 1-D resample N -> N' with N = N1 N2 and N' = M1 M2 (factors: register DFT sizes) by one group of
 // G lanes (G = the largest factor) inside a warp, data in registers between the passes:
@@ -427,7 +441,7 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
 //   forward N': the same two stages on Z; conj of the result = the resampled vector.
 // Three __syncwarp exchanges per vector instead of one shared round trip per radix pass.
 template <bool UP, int FN1, int FN2, int IN1, int IN2>
-__global__ void __launch_bounds__(128, 3) rows2_kernel(const double2 *__restrict__ in, int64_t nbox, int nth,
+__global__ void __launch_bounds__(128, UP ? HFMM_RS2_MINB_UPROWS : HFMM_RS2_MINB_DN) rows2_kernel(const double2 *__restrict__ in, int64_t nbox, int nth,
                                                       const double2 *__restrict__ twN,
                                                       const double2 *__restrict__ twN2,
                                                       const double2 *__restrict__ add, double2 *__restrict__ out) {
@@ -540,7 +554,7 @@ __global__ void __launch_bounds__(128, 3) rows2_kernel(const double2 *__restrict
 constexpr int RS2_CW = 8, RS2_CWP = 9;
 
 template <bool UP, int FN1, int FN2, int IN1, int IN2>
-__global__ void __launch_bounds__(128, 3) cols2_kernel(const double2 *__restrict__ in, int64_t nitem, int ncols,
+__global__ void __launch_bounds__(128, UP ? HFMM_RS2_MINB_UP : HFMM_RS2_MINB_DN) cols2_kernel(const double2 *__restrict__ in, int64_t nitem, int ncols,
                                                    int rowlen, const int32_t *__restrict__ cbeg, int64_t cbase,
                                                    const int32_t *__restrict__ par, const int8_t *__restrict__ oct,
                                                    const double2 *__restrict__ shift,
@@ -755,6 +769,9 @@ static bool launch_cols2(const double2 *in, int64_t nitem, int nth, int ncols, i
     RS2C(140, 60, 14, 10, 10, 6)
     RS2C(140, 240, 14, 10, 16, 15)
     RS2C(240, 140, 16, 15, 14, 10)
+    // accuracy-policy plans (tau = eps/10; C3_acc / C5_acc: 90x96 <-> 150x160)
+    RS2C(90, 150, 10, 9, 15, 10)
+    RS2C(150, 90, 15, 10, 10, 9)
 #undef RS2C
     default: return false;
   }
@@ -802,6 +819,8 @@ static bool launch_rows2(const double2 *in, int64_t nbox, int nth, int nph, int 
     RS2R(140, 60, 14, 10, 10, 6)
     RS2R(140, 240, 14, 10, 16, 15)
     RS2R(240, 140, 16, 15, 14, 10)
+    RS2R(96, 160, 12, 8, 16, 10)
+    RS2R(160, 96, 16, 10, 12, 8)
 #undef RS2R
     default: return false;
   }
@@ -1228,6 +1247,7 @@ bool box2_up_applies(int nth, int nph, int nth2, int nph2) {
   switch (gkey(nth, nph, nth2, nph2)) {
     case gkey(16, 16, 32, 32): case gkey(32, 32, 64, 64): case gkey(24, 24, 32, 32):
     case gkey(32, 32, 42, 48): case gkey(42, 48, 60, 60): case gkey(28, 28, 40, 40): case gkey(40, 40, 54, 56):
+    case gkey(40, 40, 90, 96):
       return true;
     case gkey(64, 64, 128, 128): return box2_big();
     default: return false;
@@ -1239,6 +1259,7 @@ bool box2_down_applies(int nth, int nph, int nth2, int nph2) {
   switch (gkey(nth, nph, nth2, nph2)) {
     case gkey(32, 32, 16, 16): case gkey(64, 64, 32, 32): case gkey(32, 32, 24, 24):
     case gkey(42, 48, 32, 32): case gkey(60, 60, 42, 48): case gkey(40, 40, 28, 28): case gkey(54, 56, 40, 40):
+    case gkey(90, 96, 40, 40):
       return true;
     case gkey(128, 128, 64, 64): return box2_big();
     default: return false;
@@ -1264,6 +1285,7 @@ bool launch_box2_down(const double2 *in, int64_t nitem, int nth, int nph, int nt
     B2D(60, 60, 42, 48, 10, 6, 8, 6, 10, 6, 7, 6)
     B2D(40, 40, 28, 28, 8, 5, 7, 4, 8, 5, 7, 4)
     B2D(54, 56, 40, 40, 8, 7, 8, 5, 9, 6, 8, 5)
+    B2D(90, 96, 40, 40, 12, 8, 8, 5, 10, 9, 8, 5)
 #undef B2D
     default: return false;
   }
@@ -1287,6 +1309,7 @@ bool launch_box2_up(const double2 *in, int64_t nitem, int nth, int nph, int nth2
     B2U(42, 48, 60, 60, 8, 6, 10, 6, 7, 6, 10, 6)
     B2U(28, 28, 40, 40, 7, 4, 8, 5, 7, 4, 8, 5)
     B2U(40, 40, 54, 56, 8, 5, 8, 7, 8, 5, 9, 6)
+    B2U(40, 40, 90, 96, 8, 5, 12, 8, 8, 5, 10, 9)
 #undef B2U
     default: return false;
   }

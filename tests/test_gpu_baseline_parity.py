@@ -119,6 +119,7 @@ CONFIG_PAIRS = sorted({
     ((140, 140), (240, 240)),                                                            # C4
     ((120, 120), (216, 216)), ((216, 216), (432, 432)),                                  # C5
     ((120, 120), (240, 240)), ((240, 240), (420, 420)),                                  # C1HF
+    ((40, 40), (90, 96)), ((90, 96), (150, 160)), ((150, 160), (216, 216)),              # C3_acc / C5_acc
 })
 
 
