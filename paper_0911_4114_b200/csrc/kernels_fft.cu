@@ -431,6 +431,14 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
 #ifndef HFMM_RS2_MINB_DN
 #define HFMM_RS2_MINB_DN 4
 #endif
+// ... for the power-of-two sizes (C2 grids) only: on the 7-smooth grids of the matvec configs the
+// extra CTAs per SM cost C3 0.45 ms per matvec next to the concurrent near field (3.74 -> 4.2 ms,
+// same box, profiles/r02/l2t_ab.txt "oldlb"), so those instantiations keep 3.
+constexpr bool rs2_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+template <bool UP, bool ROWS, int N, int N2>
+constexpr int rs2_minb() {
+  return !(rs2_pow2(N) && rs2_pow2(N2)) ? 3 : UP ? (ROWS ? HFMM_RS2_MINB_UPROWS : HFMM_RS2_MINB_UP) : HFMM_RS2_MINB_DN;
+}
 // ---- register-resident two-level resample passes ----------------------------------------------
 // A 1-D resample N -> N' with N = N1 N2 and N' = M1 M2 (factors: register DFT sizes) by one group of
 // G lanes (G = the largest factor) inside a warp, data in registers between the passes:
@@ -441,7 +449,7 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
 //   forward N': the same two stages on Z; conj of the result = the resampled vector.
 // Three __syncwarp exchanges per vector instead of one shared round trip per radix pass.
 template <bool UP, int FN1, int FN2, int IN1, int IN2>
-__global__ void __launch_bounds__(128, UP ? HFMM_RS2_MINB_UPROWS : HFMM_RS2_MINB_DN) rows2_kernel(const double2 *__restrict__ in, int64_t nbox, int nth,
+__global__ void __launch_bounds__(128, (rs2_minb<UP, true, FN1 * FN2, IN1 * IN2>())) rows2_kernel(const double2 *__restrict__ in, int64_t nbox, int nth,
                                                       const double2 *__restrict__ twN,
                                                       const double2 *__restrict__ twN2,
                                                       const double2 *__restrict__ add, double2 *__restrict__ out) {
@@ -554,7 +562,7 @@ __global__ void __launch_bounds__(128, UP ? HFMM_RS2_MINB_UPROWS : HFMM_RS2_MINB
 constexpr int RS2_CW = 8, RS2_CWP = 9;
 
 template <bool UP, int FN1, int FN2, int IN1, int IN2>
-__global__ void __launch_bounds__(128, UP ? HFMM_RS2_MINB_UP : HFMM_RS2_MINB_DN) cols2_kernel(const double2 *__restrict__ in, int64_t nitem, int ncols,
+__global__ void __launch_bounds__(128, (rs2_minb<UP, false, FN1 * FN2, IN1 * IN2>())) cols2_kernel(const double2 *__restrict__ in, int64_t nitem, int ncols,
                                                    int rowlen, const int32_t *__restrict__ cbeg, int64_t cbase,
                                                    const int32_t *__restrict__ par, const int8_t *__restrict__ oct,
                                                    const double2 *__restrict__ shift,

@@ -645,6 +645,87 @@ __global__ void __launch_bounds__(SMALL_TPB) l2t_warp2_kernel(PointsDev pts, con
   }
 }
 
+// L2T v3: directions on lanes like v2, but each lane accumulates its directions' terms for a
+// sub-batch of PB points over the whole direction loop and the warp reduces each point ONCE
+// (v2 reduced every point after every 64 directions: 20 SHFL + 10 DADD per point and chunk, about
+// as much shuffle-pipe time as the 48 FP64 instructions of the chunk).  Per (point, 32 directions):
+// phase 3 + e^{ix} 12 + MAC 4 FP64 instructions per lane; the 5-level butterfly per point is
+// amortised over K / 32 chunks.
+#ifndef HFMM_L2T_V3
+#define HFMM_L2T_V3 1
+#endif
+#ifndef HFMM_L2T_PB
+#define HFMM_L2T_PB 4   // points per lane sub-batch (4: 122 registers, 4 CTAs/SM; 8: 164, 3 CTAs/SM)
+#endif
+template <int PB>
+__global__ void __launch_bounds__(SMALL_TPB) l2t_warp3_kernel(PointsDev pts, const int64_t *__restrict__ first,
+                                                              const double *__restrict__ cx,
+                                                              const double *__restrict__ cy,
+                                                              const double *__restrict__ cz, int32_t box0,
+                                                              int32_t box1, const double *__restrict__ ks,
+                                                              int64_t K, const double2 *__restrict__ L, double w,
+                                                              const double *__restrict__ wk,
+                                                              double2 *__restrict__ y_far) {
+  static_assert(32 % PB == 0, "PB divides the 32-point batch");
+  __shared__ double2 tab[TAB];
+  __shared__ double wx[SMALL_WARPS][32], wy[SMALL_WARPS][32], wz[SMALL_WARPS][32];
+  fill_exp_table(tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * SMALL_WARPS;
+  const double ws = wk ? 1.0 : w;
+  for (int64_t b = box0 + (int64_t)blockIdx.x * SMALL_WARPS + warp; b < box1; b += nwarps) {
+    const int64_t s0 = first[b], s1 = first[b + 1];
+    const double c0x = cx[b], c0y = cy[b], c0z = cz[b];
+    const double2 *Lb = L + b * K;
+    for (int64_t j0 = s0; j0 < s1; j0 += 32) {  // batches of 32 points
+      const int cnt = (int)min((int64_t)32, s1 - j0);
+      __syncwarp();
+      {  // c_a - x_i (0 for the unused slots: their sums are discarded)
+        const bool v = lane < cnt;
+        wx[warp][lane] = v ? c0x - pts.x[j0 + lane] : 0.0;
+        wy[warp][lane] = v ? c0y - pts.y[j0 + lane] : 0.0;
+        wz[warp][lane] = v ? c0z - pts.z[j0 + lane] : 0.0;
+      }
+      __syncwarp();
+      double yr = 0.0, yi = 0.0;  // lane p: point j0 + p
+      for (int p0 = 0; p0 < cnt; p0 += PB) {
+        double ar[PB], ai[PB];
+#pragma unroll
+        for (int p = 0; p < PB; ++p) ar[p] = ai[p] = 0.0;
+        for (int64_t k0 = 0; k0 < K; k0 += 32) {
+          const int64_t k = k0 + lane;
+          const bool v = k < K;
+          const double kx = v ? ks[k] : 0.0, ky = v ? ks[K + k] : 0.0, kz = v ? ks[2 * K + k] : 0.0;
+          double2 l = v ? Lb[k] : make_double2(0.0, 0.0);
+          if (wk) {  // per-point weights (ragged rows, R-15)
+            const double wv = v ? wk[k] : 0.0;
+            l = make_double2(wv * l.x, wv * l.y);
+          }
+#pragma unroll
+          for (int p = 0; p < PB; ++p) {
+            const double dx = wx[warp][p0 + p], dy = wy[warp][p0 + p], dz = wz[warp][p0 + p];
+            const double2 e = cexpi_u(fma(kx, dx, fma(ky, dy, kz * dz)), tab);
+            ar[p] = fma(e.x, l.x, fma(-e.y, l.y, ar[p]));
+            ai[p] = fma(e.x, l.y, fma(e.y, l.x, ai[p]));
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < PB; ++p) {
+          double pr = ar[p], pi = ai[p];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            pr += __shfl_xor_sync(0xffffffffu, pr, off);
+            pi += __shfl_xor_sync(0xffffffffu, pi, off);
+          }
+          if (lane == p0 + p) yr = pr, yi = pi;
+        }
+      }
+      if (lane < cnt) y_far[j0 + lane] = make_double2(ws * yr, ws * yi);
+    }
+  }
+}
+
 static unsigned persistent_grid(int64_t nbox, const void *fn) {
   int per_sm = 0, dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -665,7 +746,10 @@ void launch_l2t_small(PointsDev pts, const int64_t *first, const double *cx, con
                       int32_t box0, int32_t box1, const double *ks, int64_t K, const double2 *L, double w,
                       const double *wk, double2 *y_far, cudaStream_t s) {
   if (box1 <= box0) return;
-#if HFMM_L2T_V2
+#if HFMM_L2T_V3
+  l2t_warp3_kernel<HFMM_L2T_PB><<<persistent_grid(box1 - box0, (const void *)l2t_warp3_kernel<HFMM_L2T_PB>), SMALL_TPB, 0, s>>>(
+      pts, first, cx, cy, cz, box0, box1, ks, K, L, w, wk, y_far);
+#elif HFMM_L2T_V2
   l2t_warp2_kernel<<<persistent_grid(box1 - box0, (const void *)l2t_warp2_kernel), SMALL_TPB, 0, s>>>(
       pts, first, cx, cy, cz, box0, box1, ks, K, L, w, wk, y_far);
 #else

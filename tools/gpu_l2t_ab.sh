@@ -1,18 +1,26 @@
+# L2T v3 (one warp reduction per point) vs v2 (reduction per 64 directions): parity + stage A/B
 mkdir -p gpurun_out
-: > gpurun_out/l2t_ab.log
-echo "[l2tv2 parity] $(HFMM_LIB=$PWD/paper_0911_4114_b200/libhfmm_l2tv2.so timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -1)" >> gpurun_out/l2t_ab.log
-for rep in 1 2; do
-  for v in "" l2tv2; do
-    lib=""; [ -n "$v" ] && lib="$PWD/paper_0911_4114_b200/libhfmm_$v.so"
-    HFMM_LIB=$lib HFMM_PROFILE_STAGES=1 timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --ops "" > gpurun_out/l2t_$v.log 2>&1
-    python - "$v" >> gpurun_out/l2t_ab.log <<'PY'
-import json, sys
-d = json.loads(open(f"gpurun_out/l2t_{sys.argv[1]}.log").read().strip().splitlines()[-1])
-oc = d.get("other_configs", {})
-print(sys.argv[1] or "default", "C4", round(d["ms_per_step"], 2), "C3", round(oc["C3"]["ms_per_matvec"], 3), "C5", round(oc["C5"]["ms_per_matvec"], 1))
-PY
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_virtual_ranks.py -x -q > gpurun_out/l2t_pytest.log 2>&1
+tail -2 gpurun_out/l2t_pytest.log
+timeout 900 python -m pytest tests/test_gpu_baseline_parity.py -x -q -k "acc or subset or c4_small" >> gpurun_out/l2t_pytest.log 2>&1
+tail -2 gpurun_out/l2t_pytest.log
+L=$PWD/paper_0911_4114_b200
+: > gpurun_out/l2t_ab.jsonl
+for r in 1 2; do
+for v in "" l2tv2 l2tpb8 oldlb; do
+  lib=""; [ -n "$v" ] && lib="$L/libhfmm_$v.so"
+  for a in "C5 acc serial" "C4 x serial" "C3 acc serial" "C3 x" "C3 x serial"; do
+    echo "{\"lib\": \"$v\", \"args\": \"$a\"}" >> gpurun_out/l2t_ab.jsonl
+    HFMM_LIB=$lib timeout 600 python tools/c5acc_stages.py $a >> gpurun_out/l2t_ab.jsonl 2>&1
   done
-done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:l2t -c 4 --csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --ops "" --extra "" 2>/dev/null | grep l2t | tail -2 >> gpurun_out/l2t_ab.log
-HFMM_LIB=$PWD/paper_0911_4114_b200/libhfmm_l2tv2.so timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:l2t -c 4 --csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --ops "" --extra "" 2>/dev/null | grep l2t | tail -2 >> gpurun_out/l2t_ab.log
-cat gpurun_out/l2t_ab.log
+done; done
+python - <<'PY'
+import json
+lib = None
+for l in open("gpurun_out/l2t_ab.jsonl"):
+    d = json.loads(l) if l.startswith("{") else None
+    if d is None: print(l[:200]); continue
+    if "lib" in d: lib = d["lib"] or "default(v3 pb4)"; continue
+    st = d["stages_ms"]
+    print(f"{lib:18s} {d['config']} acc={d['acc']} serial={d['serial']}  l2t {st['l2t']:.3f}  s2m {st['s2m']:.3f}  total {st['total']:.3f}")
+PY
