@@ -389,6 +389,7 @@ def bench_matvec_config(cfg, warmup: int, steps: int, tau: float = 0.0, golden: 
     out = {"n": cfg.n, "kappa": cfg.kappa, "depth": cfg.depth, "eps": cfg.eps, "geometry": cfg.kind, "tau": info["tau"],
            "L_f": info["L_f"], "source_level": info["source_level"], "ms_per_matvec": t, "matvec_per_s": 1e3 / t,
            "mpoints_per_s": cfg.n / t / 1e3, "p2p_pairs": info["p2p_pairs"], "steps": steps,
+           "p2p_tile": info["p2p_tile"], "p2p_rowskip": info["p2p_rowskip"], "p2p_dead_frac": info["p2p_dead_frac"],
            "parity": golden_parity(golden or cfg.name, yd.cpu().numpy(), info)}
     g.close()
     del qd, yd, flush
@@ -627,7 +628,8 @@ def main():
         "plan": {"L_f": L_f, "source_level": info["source_level"],
                  "levels": [{k: lv[k] for k in ("level", "ell", "n_theta", "n_phi", "F", "active")}
                             for lv in info["levels"]], "p2p_pairs": pairs, "s2m_evals": info["s2m_evals"],
-                 "p2p_tile": info["p2p_tile"]},
+                 "p2p_tile": info["p2p_tile"], "p2p_rowskip": info["p2p_rowskip"],
+                 "p2p_dead_frac": info["p2p_dead_frac"]},
         "setup_s": {"build_tree": t_tree, "precompute": t_pre},
         "clocks": clocks,
     }

@@ -133,6 +133,10 @@ typedef struct {
                               unless the items would fill fewer than ~10 waves of the GPU)     */
   int next4_passes;        /* M2M / L2L level passes run by the NEXT 4 coefficient-domain
                               symmetric kernels (HFMM_NEXT4=1 in the environment), else 0     */
+  int p2p_rowskip;         /* 1: the symmetric P2P kernel skips 32-target warp rows wholly past
+                              a tile's end (chosen when > 8% of the tile slots are dead)        */
+  double p2p_dead_frac;    /* fraction of the P2P tile slots (128 x targets-per-thread x padded
+                              sources) that hold no live target                                */
 } hfmm_info;
 
 /* Create a plan on CUDA device `device` (-1: the current device).  *out receives the plan. */
@@ -254,6 +258,19 @@ int hfmm_level_quadrature(double kappa, double a, double eps_level, double alpha
  * perm[0..n) (sorted position -> input index). */
 int hfmm_partition(int64_t n, const double *xyz, int depth, const double lo[3], double size, int L_f,
                    int64_t K, int nranks, int64_t *cuts, int64_t *pt_ranges, int64_t *perm);
+
+/* Host-only M2L halo lists (the exchange hfmm_precompute sets up for levels >= HFMM_HALO_LEVEL of
+ * a multi-rank plan; no GPU needed): with the ownership of hfmm_partition(..., L_f, K, nranks, ...)
+ * descended to `level` (2 <= level <= L_f), rank `rank` receives from each peer q the q-owned
+ * level-`level` boxes in the interaction lists of its own boxes, and sends each peer q its
+ * own boxes in the interaction lists of q's boxes.  Box ids index the occupied boxes of the level
+ * in Morton order.  recv_off / send_off [nranks + 1] (always written): list of peer q =
+ * [off[q], off[q+1]); recv_box / send_box: NULL (sizes only) or arrays of off[nranks] entries,
+ * each list sorted ascending (so q's send list to r equals r's receive list from q).  Caller owns
+ * all arrays.  Returns 0, or HFMM_E_ARG / a build_tree error. */
+int hfmm_halo_lists(int64_t n, const double *xyz, int depth, const double lo[3], double size, int L_f,
+                    int64_t K, int nranks, int rank, int level, int64_t *recv_off, int64_t *send_off,
+                    int64_t *recv_box, int64_t *send_box);
 
 /* ---- operator entry points (microbench, BASELINE config 2; device pointers) -----------------
  * Batched 5-step Fourier resampling of `nbatch` half-stored fields

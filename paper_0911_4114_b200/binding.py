@@ -37,7 +37,7 @@ EXPORTED = [
     "hfmm_create", "hfmm_set_dist", "hfmm_nccl_unique_id", "hfmm_build_tree", "hfmm_precompute", "hfmm_matvec",
     "hfmm_direct", "hfmm_get_info", "hfmm_stage_times", "hfmm_debug_copy", "hfmm_last_error",
     "hfmm_destroy", "hfmm_level_quadrature", "hfmm_resample_workspace", "hfmm_resample",
-    "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_rep_grid",
+    "hfmm_m2m_op", "hfmm_l2l_op", "hfmm_m2l_op", "hfmm_partition", "hfmm_halo_lists", "hfmm_rep_grid",
     "hfmm_m2l_op_plan", "hfmm_m2l_op_apply", "hfmm_m2l_op_free", "hfmm_m2l_op_kind", "hfmm_ragged_rows",
     "hfmm_vgroup_create", "hfmm_set_dist_virtual", "hfmm_vgroup_matvec", "hfmm_vgroup_destroy",
     "hfmm_set_next4", "hfmm_set_fused",
@@ -59,7 +59,8 @@ class Info(C.Structure):
                 ("level", LevelInfo * MAX_LEVELS), ("p2p_pairs", C.c_int64), ("p2p_sym_pairs", C.c_int64),
                 ("s2m_evals", C.c_int64),
                 ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64),
-                ("source_level", C.c_int), ("launches", C.c_int), ("p2p_tile", C.c_int), ("next4_passes", C.c_int)]
+                ("source_level", C.c_int), ("launches", C.c_int), ("p2p_tile", C.c_int), ("next4_passes", C.c_int),
+                ("p2p_rowskip", C.c_int), ("p2p_dead_frac", C.c_double)]
 
 
 class HFMMError(RuntimeError):
@@ -101,6 +102,7 @@ def load() -> C.CDLL:
         "hfmm_l2l_op": (ci, [ci, ci, ci, ci, ci, vp, vp, vp, vp, vp, vp]),
         "hfmm_m2l_op": (ci, [ci, i64, vp, vp, vp, vp, vp, vp, vp]),
         "hfmm_partition": (ci, [i64, vp, ci, vp, dbl, ci, i64, ci, vp, vp, vp]),
+        "hfmm_halo_lists": (ci, [i64, vp, ci, vp, dbl, ci, i64, ci, ci, ci, vp, vp, vp, vp]),
         "hfmm_rep_grid": (ci, [dbl, dbl, dbl, C.POINTER(ci), C.POINTER(ci)]),
         "hfmm_m2l_op_plan": (ci, [ci, i64, vp, vp, vp, C.POINTER(vp)]),
         "hfmm_m2l_op_apply": (ci, [vp, vp, vp, vp, vp]),
@@ -186,6 +188,27 @@ def partition(xyz, depth, lo, size, L_f, K, nranks):
     if rc < 0:
         raise HFMMError(rc, "hfmm_partition")
     return cuts, rng.reshape(nranks, 2), perm
+
+
+def halo_lists(xyz, depth, lo, size, L_f, K, nranks, rank, level):
+    """Host-only M2L halo lists of `rank` at `level` (the ones hfmm_precompute exchanges):
+    (recv, send), each a list over peers q of sorted level-`level` box indices (Morton order)."""
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    n = xyz.shape[0]
+    ro = np.zeros(nranks + 1, dtype=np.int64)
+    so = np.zeros(nranks + 1, dtype=np.int64)
+    lib = load()
+    args = (n, xyz.ctypes.data, depth, lo.ctypes.data, size, L_f, K, nranks, rank, level)
+    rc = lib.hfmm_halo_lists(*args, ro.ctypes.data, so.ctypes.data, None, None)
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_halo_lists")
+    rb = np.zeros(max(int(ro[-1]), 1), dtype=np.int64)
+    sb = np.zeros(max(int(so[-1]), 1), dtype=np.int64)
+    rc = lib.hfmm_halo_lists(*args, ro.ctypes.data, so.ctypes.data, rb.ctypes.data, sb.ctypes.data)
+    if rc < 0:
+        raise HFMMError(rc, "hfmm_halo_lists")
+    return ([rb[ro[q]:ro[q + 1]] for q in range(nranks)], [sb[so[q]:so[q + 1]] for q in range(nranks)])
 
 
 def _ptr(a) -> int:
@@ -309,7 +332,8 @@ class HFMM:
                     p2p_sym_pairs=inf.p2p_sym_pairs,
                     s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points,
                     source_level=(None if inf.source_level < 0 else inf.source_level), launches=inf.launches,
-                    p2p_tile=inf.p2p_tile, next4_passes=inf.next4_passes)
+                    p2p_tile=inf.p2p_tile, next4_passes=inf.next4_passes,
+                    p2p_rowskip=bool(inf.p2p_rowskip), p2p_dead_frac=inf.p2p_dead_frac)
 
     def stage_times(self):
         out = (C.c_double * 8)()

@@ -153,6 +153,8 @@ struct hfmm_plan {
   double *ux = nullptr, *uy = nullptr, *uz = nullptr;
   double uscale = 0;               // kappa TAB_STEPS / (2 pi)
   int p2p_pt = 4;                  // targets per thread of the P2P kernels (tile = 128 x p2p_pt: 3, 4 or 8)
+  bool p2p_rowskip = false;        // symmetric P2P skips dead warp rows (plan: > 8% dead tile slots)
+  double p2p_dead_frac = 0.0;      // tile slots of the P2P items holding no live target
   int64_t p2p_sym_pairs = 0;
   double dummy_t[3] = {0, 0, 0}, dummy_s[3] = {0, 0, 0};
   double2 *tmp = nullptr;
@@ -722,31 +724,13 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     }
     L.il_nnz = (int64_t)src.size();
     if (L.active && p->nranks > 1 && l >= halo_min_level()) {
-      // halo lists: recv[q] = q-owned sources of my owned targets, send[q] = my owned sources of
-      // q's owned targets (sorted, unique: the receiver and the sender build the same list)
+      // halo lists (host_tree.cpp m2l_halo_lists, also exported as hfmm_halo_lists)
       const int R = p->nranks;
-      auto owner = [&](int64_t b) {
-        for (int q = 0; q < R; ++q)
-          if (b >= L.rlo[q] && b < L.rhi[q]) return q;
-        return -1;
-      };
-      std::vector<std::vector<int64_t>> snd(R), rcv(R);
-      for (int q = 0; q < R; ++q)
-        for (int64_t b = L.rlo[q]; b < L.rhi[q]; ++b)
-          for (int32_t e = row[b]; e < row[b + 1]; ++e) {
-            const int64_t sb = src[e];
-            const int o = owner(sb);
-            if (o < 0 || o == q) continue;
-            if (q == p->rank) rcv[o].push_back(sb);
-            else if (o == p->rank) snd[q].push_back(sb);
-          }
+      std::vector<std::vector<int64_t>> snd, rcv;
+      m2l_halo_lists(t, l, L.rlo, L.rhi, p->rank, snd, rcv);
       L.hs_off.assign(R + 1, 0), L.hr_off.assign(R + 1, 0);
       std::vector<int64_t> hs, hr;
       for (int q = 0; q < R; ++q) {
-        for (auto *v : {&snd[q], &rcv[q]}) {
-          std::sort(v->begin(), v->end());
-          v->erase(std::unique(v->begin(), v->end()), v->end());
-        }
         hs.insert(hs.end(), snd[q].begin(), snd[q].end());
         hr.insert(hr.end(), rcv[q].begin(), rcv[q].end());
         L.hs_off[q + 1] = (int64_t)hs.size(), L.hr_off[q + 1] = (int64_t)hr.size();
@@ -908,12 +892,16 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       int force = 0;
       if (const char *e = getenv("HFMM_P2P_PT")) force = atoi(e);
       const int cand[3] = {8, 4, 3}, ctas[3] = {2, 3, 4};
-      // thread-evaluation slots of the items: every thread of a tile evaluates PT targets
-      // (inactive ones at a dummy position) against the sources padded to 32
-      auto padded_slots = [&](int pt) {
+      // thread-evaluation slots of the items against the sources padded to 32: every thread of a
+      // tile evaluates its PT targets (inactive ones at a dummy position), or -- live_only -- only
+      // the 32-target warp rows holding a live target (the row-skipping kernel)
+      auto padded_slots = [&](int pt, bool live_only = false) {
         double sl = 0.0;
         for (auto &v : it)
-          for (size_t i = 0; i < v.size(); i += 4) sl += (double)P2P_TPB_HOST * pt * (double)((v[i + 3] - v[i + 2] + 31) / 32 * 32);
+          for (size_t i = 0; i < v.size(); i += 4) {
+            const double rows = live_only ? (double)((v[i + 1] - v[i] + 31) / 32 * 32) : (double)P2P_TPB_HOST * pt;
+            sl += rows * (double)((v[i + 3] - v[i + 2] + 31) / 32 * 32);
+          }
         return sl;
       };
       double slots4 = 0.0;
@@ -943,6 +931,17 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
           }
         }
       }
+    // Row skipping (p2p_sym_kernel<..., RS = true>): warps skip their target rows wholly past the
+    // tile's end.  Its per-slot rate is a few % lower (same-box A/B, profiles/r02/rowskip_ab.txt:
+    // C4 / C5 0.5-2.4% slower with 6% / 4% dead slots; C3 4%, C3_acc 7%, C5_acc 2.5% faster), so the
+    // plan turns it on only when more than HFMM_P2P_ROWSKIP_MIN (default 8%) of the tile slots are dead.
+    {
+      double thr = 0.08;
+      if (const char *e = getenv("HFMM_P2P_ROWSKIP_MIN")) thr = atof(e);
+      const double full = padded_slots(p->p2p_pt), live = padded_slots(p->p2p_pt, true);
+      p->p2p_rowskip = p->p2p_pt != 8 && full > 0.0 && live < (1.0 - thr) * full;
+      p->p2p_dead_frac = full > 0.0 ? 1.0 - live / full : 0.0;
+    }
     }
     // longest items first (LPT order against the tail of the grid)
     std::vector<int64_t> sorted_items[3];
@@ -1096,6 +1095,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     }
     in.launches = nl;
     in.p2p_tile = P2P_TPB_HOST * p->p2p_pt;
+    in.p2p_rowskip = p->p2p_rowskip ? 1 : 0;
+    in.p2p_dead_frac = p->p2p_dead_frac;
     in.next4_passes = n4;
   }
   in.owned_points = p->own_pt1 - p->own_pt0;
@@ -1177,7 +1178,7 @@ static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool 
     for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD})
       launch_p2p_items(pu, p->p2p_items[k], p->p2p_nitems[k], (k == P2P_DIAG && HFMM_P2P_DSYM) ? P2P_DSYM : k,
                        p->uscale, p->dummy_t, p->dummy_s, p->y_near, p->stream2, p->p2p_pt,
-                       det ? p->p2p_part : nullptr, det ? p->p2p_slot[k] : nullptr);
+                       det ? p->p2p_part : nullptr, det ? p->p2p_slot[k] : nullptr, p->p2p_rowskip);
     if (det) launch_p2p_reduce(p->p2p_part, p->p2p_rp, p->p2p_idx, n, p->y_near, p->stream2);
   }
   if (prof) cudaEventRecord(p->sev[8], p->stream2);

@@ -68,6 +68,8 @@ int build_tree(const double *xyz, int64_t n, int depth, const double lo[3], doub
                std::string &err);
 uint32_t morton3(uint32_t x, uint32_t y, uint32_t z);
 void partition_level2(const Tree &t, int L_f, int64_t K, int R, std::vector<int64_t> &cut);
+void m2l_halo_lists(const Tree &t, int l, const std::vector<int64_t> &rlo, const std::vector<int64_t> &rhi, int r,
+                    std::vector<std::vector<int64_t>> &snd, std::vector<std::vector<int64_t>> &rcv);
 // offsets: id in [0,316) <-> (ox, oy, oz) in [-3,3]^3 \ [-1,1]^3, lexicographic x, y, z
 int offset_id(int ox, int oy, int oz);
 void offset_vec(int id, int o[3]);
@@ -124,6 +126,10 @@ constexpr int P2P_TPB_HOST = HFMM_P2P_TPB;  // work-item tile = P2P_TPB_HOST x t
 #endif
 constexpr int TAB_STEPS = HFMM_TAB_STEPS;  // e^{i h k} table size; h = 2 pi / TAB_STEPS
 enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2, P2P_DSYM = 3 };
+#ifndef HFMM_P2P_RS_MODE
+#define HFMM_P2P_RS_MODE 1  // row-skipping symmetric P2P (plan flag p2p_rowskip): 1 every tile through the
+                            // per-row-count variants, 2 full tiles through the inline loop
+#endif
 #ifndef HFMM_P2P_DSYM
 #define HFMM_P2P_DSYM 1  // matvec diagonal tiles with the symmetric kernel (each unordered pair once)
 #endif
@@ -135,7 +141,7 @@ enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2, P2P_DSYM = 3 };
 // dummy_t / dummy_s (scaled units): far positions used to pad partial symmetric tiles.
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
                       const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt,
-                      double2 *part = nullptr, const int64_t *slot = nullptr);
+                      double2 *part = nullptr, const int64_t *slot = nullptr, bool rowskip = false);
 // deterministic P2P accumulation: y_near[i] = sum of part[idx[e]], e in [row_ptr[i], row_ptr[i + 1])
 void launch_p2p_reduce(const double2 *part, const int64_t *row_ptr, const int64_t *idx, int64_t n, double2 *y_near,
                        cudaStream_t s);

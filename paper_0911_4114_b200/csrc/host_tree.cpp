@@ -209,6 +209,46 @@ void partition_level2(const Tree &t, int L_f, int64_t K, int R, std::vector<int6
   for (; k < R; ++k) cut[k] = B2.nbox();
 }
 
+// M2L halo lists of rank r at level l (multi-rank plans; used by hfmm_precompute and exported as
+// hfmm_halo_lists): recv[q] = the boxes owned by q != r in the interaction list (children of
+// the parent's neighbours that are not adjacent) of a box owned by r; send[q] = the boxes owned by r
+// in the interaction list of a box owned by q.  Sorted and unique, so the sender's send[r'] and the
+// receiver's recv[r] are the same list.  rlo / rhi: every rank's owned box range at level l.
+void m2l_halo_lists(const Tree &t, int l, const std::vector<int64_t> &rlo, const std::vector<int64_t> &rhi, int r,
+                    std::vector<std::vector<int64_t>> &snd, std::vector<std::vector<int64_t>> &rcv) {
+  const LevelBoxes &B = t.levels[l];
+  const int R = (int)rlo.size();
+  snd.assign(R, {}), rcv.assign(R, {});
+  auto owner = [&](int64_t b) {
+    for (int q = 0; q < R; ++q)
+      if (b >= rlo[q] && b < rhi[q]) return q;
+    return -1;
+  };
+  for (int64_t b = 0; b < B.nbox(); ++b) {
+    const int ob = owner(b);
+    if (ob < 0) continue;
+    const int px = B.ix[b] >> 1, py = B.iy[b] >> 1, pz = B.iz[b] >> 1;
+    for (int dx = -3; dx <= 3; ++dx)
+      for (int dy = -3; dy <= 3; ++dy)
+        for (int dz = -3; dz <= 3; ++dz) {
+          if (std::max(std::abs(dx), std::max(std::abs(dy), std::abs(dz))) < 2) continue;
+          const int x = B.ix[b] + dx, y = B.iy[b] + dy, z = B.iz[b] + dz;
+          if (std::abs((x >> 1) - px) > 1 || std::abs((y >> 1) - py) > 1 || std::abs((z >> 1) - pz) > 1) continue;
+          const int32_t k = B.find(x, y, z);
+          if (k < 0) continue;
+          const int os = owner(k);
+          if (os < 0 || os == ob) continue;
+          if (ob == r) rcv[os].push_back(k);
+          else if (os == r) snd[ob].push_back(k);
+        }
+  }
+  for (int q = 0; q < R; ++q)
+    for (auto *v : {&snd[q], &rcv[q]}) {
+      std::sort(v->begin(), v->end());
+      v->erase(std::unique(v->begin(), v->end()), v->end());
+    }
+}
+
 // 34 canonical transfer vectors (Fig. SemiOctant): x >= y >= 0, z >= 0, in the
 // lexicographic order of the 316.  Offset o = F P c with c canonical, P the x<->y swap (when
 // |o_y| > |o_x|) and F the sign flips of o's negative components, so
@@ -285,5 +325,34 @@ extern "C" int hfmm_partition(int64_t n, const double *xyz, int depth, const dou
   }
   if (perm)
     for (int64_t i = 0; i < n; ++i) perm[i] = t.perm[i];
+  return 0;
+}
+
+extern "C" int hfmm_halo_lists(int64_t n, const double *xyz, int depth, const double lo[3], double size, int L_f,
+                               int64_t K, int nranks, int rank, int level, int64_t *recv_off, int64_t *send_off,
+                               int64_t *recv_box, int64_t *send_box) {
+  using namespace hfmm;
+  if (!xyz || !lo || !recv_off || !send_off || nranks < 1 || rank < 0 || rank >= nranks || L_f < 2 || L_f > depth ||
+      level < 2 || level > L_f || K <= 0)
+    return HFMM_E_ARG;
+  Tree t;
+  std::string err;
+  int rc = build_tree(xyz, n, depth, lo, size, t, err);
+  if (rc) return rc;
+  std::vector<int64_t> cut;
+  partition_level2(t, L_f, K, nranks, cut);
+  std::vector<int64_t> rlo(cut.begin(), cut.end() - 1), rhi(cut.begin() + 1, cut.end());
+  for (int l = 2; l < level; ++l)   // descend to `level` (children ranges are contiguous)
+    for (int q = 0; q < nranks; ++q)
+      rlo[q] = t.levels[l].child_begin[rlo[q]], rhi[q] = t.levels[l].child_begin[rhi[q]];
+  std::vector<std::vector<int64_t>> snd, rcv;
+  m2l_halo_lists(t, level, rlo, rhi, rank, snd, rcv);
+  recv_off[0] = send_off[0] = 0;
+  for (int q = 0; q < nranks; ++q) {
+    recv_off[q + 1] = recv_off[q] + (int64_t)rcv[q].size();
+    send_off[q + 1] = send_off[q] + (int64_t)snd[q].size();
+    if (recv_box) std::copy(rcv[q].begin(), rcv[q].end(), recv_box + recv_off[q]);
+    if (send_box) std::copy(snd[q].begin(), snd[q].end(), send_box + send_off[q]);
+  }
   return 0;
 }

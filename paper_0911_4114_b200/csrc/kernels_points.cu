@@ -191,7 +191,61 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_ord_kernel(PointsU pts,
 // block pairs (target block tb = warp + (P2P_TPB / 32) p, source block sb) with tb < sb in full, tb == sb for half
 // of the systolic rotation (steps 1..15 and lanes < 16 of step 16; step 0 is the excluded self pair,
 // P:90), tb > sb skipped (warp-uniform branches).
-template <bool DS, int PT, int MINB>
+// One 32-source block of the symmetric item for a warp whose first NP target rows p (targets
+// t0 + 32 warp + 128 p + lane) hold live targets: rows p >= NP lie wholly past the tile's end
+// and are not evaluated at all (warp-row granularity instead of the tile's; the dispatch below is
+// warp-uniform and outside the source loop, so each variant keeps the straight-line schedule).
+template <bool DS, int PT, int NP>
+__device__ __forceinline__ void p2p_sym_block(const double (&tx)[PT], const double (&ty)[PT], const double (&tz)[PT],
+                                              const double2 (&tq)[PT], double (&ar)[PT], double (&ai)[PT],
+                                              const double *sx, const double *sy, const double *sz,
+                                              const double2 *sq, const double2 *tab, int lane, int warp,
+                                              int base, int sb, double &cr_out, double &ci_out) {
+  double cr = 0.0, ci = 0.0;
+#pragma unroll 2
+  for (int u = 0; u < 32; ++u) {
+    const int s = base + ((lane + u) & 31);
+    const double xs = sx[s], ys = sy[s], zs = sz[s];
+    const double2 qs = sq[s];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      double w = 1.0;
+      if (DS) {
+        const int tb = warp + (P2P_TPB / 32) * p;
+        if (tb > sb) continue;
+        if (tb == sb) {
+          if (u == 0 || u > 16) continue;
+          if (u == 16 && lane >= 16) w = 0.0;   // the other half of the antipodal step
+        }
+      }
+      double2 g = green_u(tx[p], ty[p], tz[p], xs, ys, zs, tab);
+      if (DS) g = make_double2(g.x * w, g.y * w);
+      ar[p] = fma(g.x, qs.x, fma(-g.y, qs.y, ar[p]));
+      ai[p] = fma(g.x, qs.y, fma(g.y, qs.x, ai[p]));
+      cr = fma(g.x, tq[p].x, fma(-g.y, tq[p].y, cr));
+      ci = fma(g.x, tq[p].y, fma(g.y, tq[p].x, ci));
+    }
+    cr = __shfl_sync(0xffffffffu, cr, (lane + 1) & 31);   // accumulator follows its source
+    ci = __shfl_sync(0xffffffffu, ci, (lane + 1) & 31);
+  }
+  cr_out = cr, ci_out = ci;
+}
+
+template <bool DS, int PT, int NP>
+__device__ __forceinline__ void p2p_sym_dispatch(int np, const double (&tx)[PT], const double (&ty)[PT],
+                                                 const double (&tz)[PT], const double2 (&tq)[PT], double (&ar)[PT],
+                                                 double (&ai)[PT], const double *sx, const double *sy,
+                                                 const double *sz, const double2 *sq, const double2 *tab, int lane,
+                                                 int warp, int base, int sb, double &cr, double &ci) {
+  if constexpr (NP == 0) {
+    cr = ci = 0.0;   // no live target in this warp: its column partial sums are zero
+  } else {
+    if (np >= NP) p2p_sym_block<DS, PT, NP>(tx, ty, tz, tq, ar, ai, sx, sy, sz, sq, tab, lane, warp, base, sb, cr, ci);
+    else p2p_sym_dispatch<DS, PT, NP - 1>(np, tx, ty, tz, tq, ar, ai, sx, sy, sz, sq, tab, lane, warp, base, sb, cr, ci);
+  }
+}
+
+template <bool DS, int PT, int MINB, bool RS>
 __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
                                                                         const int64_t *__restrict__ items,
                                                                         double scale, double3 dummy_t,
@@ -218,6 +272,12 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
     tq[p] = v ? pts.q[i] : make_double2(0.0, 0.0);
     ar[p] = ai[p] = 0.0;
   }
+  // live target rows of this warp: row p holds targets t0 + 32 warp + 128 p + lane
+  int np_w = PT;
+  if (RS) {
+    const int64_t left = t1 - (it[0] + 32 * warp);
+    np_w = left <= 0 ? 0 : (int)min((int64_t)PT, (left + P2P_TPB - 1) / P2P_TPB);
+  }
   for (int64_t c0 = s0; c0 < s1; c0 += P2P_TPB) {
     const int cnt = (int)min((int64_t)P2P_TPB, s1 - c0);
     __syncthreads();
@@ -236,31 +296,37 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
       const int base = blk << 5;
       const int sb = (int)((c0 - s0) >> 5) + blk;  // source block (DS)
       double cr = 0.0, ci = 0.0;
+      if (RS && HFMM_P2P_RS_MODE == 2 && np_w < PT) {
+        p2p_sym_dispatch<DS, PT, PT - 1>(np_w, tx, ty, tz, tq, ar, ai, sx, sy, sz, sq, tab, lane, warp, base, sb, cr, ci);
+      } else if (RS && HFMM_P2P_RS_MODE == 1) {
+        p2p_sym_dispatch<DS, PT, PT>(np_w, tx, ty, tz, tq, ar, ai, sx, sy, sz, sq, tab, lane, warp, base, sb, cr, ci);
+      } else {  // all PT rows (the full-tile loop, inline)
 #pragma unroll 2
-      for (int u = 0; u < 32; ++u) {
-        const int s = base + ((lane + u) & 31);
-        const double xs = sx[s], ys = sy[s], zs = sz[s];
-        const double2 qs = sq[s];
+        for (int u = 0; u < 32; ++u) {
+          const int s = base + ((lane + u) & 31);
+          const double xs = sx[s], ys = sy[s], zs = sz[s];
+          const double2 qs = sq[s];
 #pragma unroll
-        for (int p = 0; p < PT; ++p) {
-          double w = 1.0;
-          if (DS) {
-            const int tb = warp + (P2P_TPB / 32) * p;
-            if (tb > sb) continue;
-            if (tb == sb) {
-              if (u == 0 || u > 16) continue;
-              if (u == 16 && lane >= 16) w = 0.0;   // the other half of the antipodal step
+          for (int p = 0; p < PT; ++p) {
+            double w = 1.0;
+            if (DS) {
+              const int tb = warp + (P2P_TPB / 32) * p;
+              if (tb > sb) continue;
+              if (tb == sb) {
+                if (u == 0 || u > 16) continue;
+                if (u == 16 && lane >= 16) w = 0.0;   // the other half of the antipodal step
+              }
             }
+            double2 g = green_u(tx[p], ty[p], tz[p], xs, ys, zs, tab);
+            if (DS) g = make_double2(g.x * w, g.y * w);
+            ar[p] = fma(g.x, qs.x, fma(-g.y, qs.y, ar[p]));
+            ai[p] = fma(g.x, qs.y, fma(g.y, qs.x, ai[p]));
+            cr = fma(g.x, tq[p].x, fma(-g.y, tq[p].y, cr));
+            ci = fma(g.x, tq[p].y, fma(g.y, tq[p].x, ci));
           }
-          double2 g = green_u(tx[p], ty[p], tz[p], xs, ys, zs, tab);
-          if (DS) g = make_double2(g.x * w, g.y * w);
-          ar[p] = fma(g.x, qs.x, fma(-g.y, qs.y, ar[p]));
-          ai[p] = fma(g.x, qs.y, fma(g.y, qs.x, ai[p]));
-          cr = fma(g.x, tq[p].x, fma(-g.y, tq[p].y, cr));
-          ci = fma(g.x, tq[p].y, fma(g.y, tq[p].x, ci));
+          cr = __shfl_sync(0xffffffffu, cr, (lane + 1) & 31);   // accumulator follows its source
+          ci = __shfl_sync(0xffffffffu, ci, (lane + 1) & 31);
         }
-        cr = __shfl_sync(0xffffffffu, cr, (lane + 1) & 31);   // accumulator follows its source
-        ci = __shfl_sync(0xffffffffu, ci, (lane + 1) & 31);
       }
       col[warp][base + lane] = make_double2(cr, ci);
     }
@@ -306,12 +372,12 @@ void launch_p2p_reduce(const double2 *part, const int64_t *row_ptr, const int64_
   p2p_reduce_kernel<<<blocks, 256, 0, s>>>(part, row_ptr, idx, n, y_near);
 }
 
-template <int PT, int MINB>
+template <int PT, int MINB, bool RS>
 static void launch_p2p_items_t(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
                                const double dummy_t[3], const double dummy_s[3], double2 *y_near, double2 *part,
                                const int64_t *slot, cudaStream_t s) {
   if (kind == P2P_SYM || kind == P2P_DSYM) {
-    auto kern = kind == P2P_SYM ? p2p_sym_kernel<false, PT, MINB> : p2p_sym_kernel<true, PT, MINB>;
+    auto kern = kind == P2P_SYM ? p2p_sym_kernel<false, PT, MINB, RS> : p2p_sym_kernel<true, PT, MINB, RS>;
     kern<<<(unsigned)nitems, P2P_TPB, 0, s>>>(pts, items, scale, make_double3(dummy_t[0], dummy_t[1], dummy_t[2]),
                                              make_double3(dummy_s[0], dummy_s[1], dummy_s[2]), y_near, part, slot);
   }
@@ -323,14 +389,18 @@ static void launch_p2p_items_t(PointsU pts, const int64_t *items, int64_t nitems
 
 void launch_p2p_items(PointsU pts, const int64_t *items, int64_t nitems, int kind, double scale,
                       const double dummy_t[3], const double dummy_s[3], double2 *y_near, cudaStream_t s, int pt,
-                      double2 *part, const int64_t *slot) {
+                      double2 *part, const int64_t *slot, bool rowskip) {
   if (nitems <= 0) return;
-  if (pt == 3)
-    launch_p2p_items_t<3, 4>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
+  if (pt == 3 && rowskip)
+    launch_p2p_items_t<3, 4, true>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
+  else if (pt == 3)
+    launch_p2p_items_t<3, 4, false>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
   else if (pt == 8)
-    launch_p2p_items_t<8, 1>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
+    launch_p2p_items_t<8, 1, false>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
+  else if (rowskip)
+    launch_p2p_items_t<4, HFMM_P2P_MINB, true>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
   else
-    launch_p2p_items_t<4, HFMM_P2P_MINB>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
+    launch_p2p_items_t<4, HFMM_P2P_MINB, false>(pts, items, nitems, kind, scale, dummy_t, dummy_s, y_near, part, slot, s);
 }
 
 // ---------------------------------------------------------------------------------------------
