@@ -905,6 +905,7 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
         return sl;
       };
       double slots4 = 0.0;
+      bool short_grid = false;   // fewer than ~10 waves of 512-point items: the tail dominates
       for (int c = force == 8 ? 0 : 1; c < 3; ++c) {
         if ((force == 3 || force == 4 || force == 8) && cand[c] != force) continue;
         p->p2p_pt = cand[c];
@@ -914,7 +915,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
         if (cand[c] == force) break;
         if (cand[c] == 4) {
           slots4 = padded_slots(4);
-          if (nit >= 10 * ctas[c] * (int64_t)nsm) {
+          short_grid = nit < 10 * ctas[c] * (int64_t)nsm;
+          if (!short_grid) {
             // enough waves: keep 512-point tiles unless the leaves fill them poorly -- 384-point
             // tiles must save > 8% of the padded slots to beat their lower per-slot rate (C4's
             // 3,676-point leaves: 6.7% fewer slots, measured 1% slower at 384; C5 at eps/10
@@ -932,14 +934,15 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
         }
       }
     // Row skipping (p2p_sym_kernel<..., RS = true>): warps skip their target rows wholly past the
-    // tile's end.  Its per-slot rate is a few % lower (same-box A/B, profiles/r02/rowskip_ab.txt:
-    // C4 / C5 0.5-2.4% slower with 6% / 4% dead slots; C3 4%, C3_acc 7%, C5_acc 2.5% faster), so the
-    // plan turns it on only when more than HFMM_P2P_ROWSKIP_MIN (default 8%) of the tile slots are dead.
+    // tile's end.  Its per-slot rate is lower (same-box A/Bs, profiles/r02/rowskip_ab*.txt: C4 / C5
+    // 0.7% / 2.4% slower with 5% / 4% dead slots; C3_acc 7% and C5_acc 4% faster with 29% / 17%
+    // dead; C3, a short grid, 4% faster with 3.5%), so the plan turns it on when more than
+    // HFMM_P2P_ROWSKIP_MIN (default 8%) of the tile slots are dead, or for short grids.
     {
       double thr = 0.08;
       if (const char *e = getenv("HFMM_P2P_ROWSKIP_MIN")) thr = atof(e);
       const double full = padded_slots(p->p2p_pt), live = padded_slots(p->p2p_pt, true);
-      p->p2p_rowskip = p->p2p_pt != 8 && full > 0.0 && live < (1.0 - thr) * full;
+      p->p2p_rowskip = p->p2p_pt != 8 && full > 0.0 && (live < (1.0 - thr) * full || (short_grid && thr < 1.0));
       p->p2p_dead_frac = full > 0.0 ? 1.0 - live / full : 0.0;
     }
     }

@@ -126,10 +126,6 @@ constexpr int P2P_TPB_HOST = HFMM_P2P_TPB;  // work-item tile = P2P_TPB_HOST x t
 #endif
 constexpr int TAB_STEPS = HFMM_TAB_STEPS;  // e^{i h k} table size; h = 2 pi / TAB_STEPS
 enum { P2P_SYM = 0, P2P_DIAG = 1, P2P_ORD = 2, P2P_DSYM = 3 };
-#ifndef HFMM_P2P_RS_MODE
-#define HFMM_P2P_RS_MODE 1  // row-skipping symmetric P2P (plan flag p2p_rowskip): 1 every tile through the
-                            // per-row-count variants, 2 full tiles through the inline loop
-#endif
 #ifndef HFMM_P2P_DSYM
 #define HFMM_P2P_DSYM 1  // matvec diagonal tiles with the symmetric kernel (each unordered pair once)
 #endif

@@ -296,9 +296,8 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
       const int base = blk << 5;
       const int sb = (int)((c0 - s0) >> 5) + blk;  // source block (DS)
       double cr = 0.0, ci = 0.0;
-      if (RS && HFMM_P2P_RS_MODE == 2 && np_w < PT) {
-        p2p_sym_dispatch<DS, PT, PT - 1>(np_w, tx, ty, tz, tq, ar, ai, sx, sy, sz, sq, tab, lane, warp, base, sb, cr, ci);
-      } else if (RS && HFMM_P2P_RS_MODE == 1) {
+      if (RS) {   // every tile through the per-row-count variants (full tiles through the inline
+                  // loop below instead: C4 68.1 vs 67.1 ms with skipping on, profiles/r02/rowskip_ab2.txt)
         p2p_sym_dispatch<DS, PT, PT>(np_w, tx, ty, tz, tq, ar, ai, sx, sy, sz, sq, tab, lane, warp, base, sb, cr, ci);
       } else {  // all PT rows (the full-tile loop, inline)
 #pragma unroll 2
