@@ -488,6 +488,169 @@ struct M2LGroupPlan {
   uint32_t *dmask = nullptr;
 };
 
+// ---- parent-block M2L on the FP64 tensor core (DMMA m8n8k4) -----------------------------------
+// For one direction k and one neighbour-parent slot D the parent-block sum is a matrix product
+// shared by every sibling group:  I[d][g] += sum_e A_{D,k}[d][e] B_{D,k}[e][g],  A[d][e] =
+// T[2D + e - d][k] (8 x 8, zero at adjacent offsets), B[e][g] = M[child e of (P_g + D)][k].
+// A warp runs it for a direction pair (k, k + 1) and a batch of 8 groups as real 8 x 8 x 4
+// DMMAs (mma.sync.m8n8k4.f64: thread t holds A[t/4][t%4], B[t%4][t/4], C[t/4][2(t%4) + j]):
+//   C_re += A_re B_re - A_im B_im,   C_im += A_re B_im + A_im B_re   (two k-steps over e)
+// 16 DMMAs (4,096 FMAs) per (D, pair, batch) replace 512 DFMA warp-instructions: the MACs issue as
+// a few dozen instructions and never read three vector registers per FMA (the DFMA kernel's
+// issue / register-port ceiling, DESIGN 6.1).  B200's DMMA and DFMA share one FP64 pipe
+// (profiles/r02/dmma_probe.txt: 37.1 TFLOP/s DMMA alone), so the gain would be the issue side.
+// Measured (same box, C2 B64): 78 ms with B fragments loaded from global memory (L1TEX 94% busy:
+// 32 rows per warp load), 69 ms with the batch's source ids staged, 62.7 ms with the sources
+// staged by cp.async (tensor pipe 39% active; stalls: DMMA dependency waits, shared-memory
+// scoreboards, 12 warps/SM) vs 41.7 ms for the DFMA parent-block kernel: kept off (parity-green).
+// Tables: the chunk's [M2LD_KC directions][343 cube slots] k-major in shared memory (a warp reads
+// 32 different slots of one direction: no bank conflicts), M from global / L2 as 32-byte (k, k+1)
+// pairs.  Same plan data (dtarget / dsrc / dmask) and the same terms as m2l_dense_kernel.
+#ifndef HFMM_M2L_DMMA
+#define HFMM_M2L_DMMA 0   // A/B (profiles/r02/m2l_dmma_ab.txt): B64 62.7 vs 41.7 ms for the DFMA kernel -> off
+#endif
+constexpr int M2LD_KC = 8;       // directions per table chunk (4 direction pairs = 4 warps)
+constexpr int M2LD_WARPS = M2LD_KC / 2;
+constexpr int M2LD_MP = M2LD_KC + 1;   // staged-source row pitch (complex values): conflict-free B reads
+
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void m2ld_cp16(double2 *smem, const double2 *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+__device__ __forceinline__ void fill_tables_kmajor(double2 *Ts, const double2 *__restrict__ T,
+                                                   const int32_t *__restrict__ perm, int64_t K, int64_t k0) {
+  // Ts[kk][sl] = T_{o(sl)}[k0 + kk]; consecutive threads take consecutive directions of one slot
+  for (int i = threadIdx.x; i < M2LB_SLOTS * M2LD_KC; i += blockDim.x) {
+    const int sl = i / M2LD_KC, kk = i % M2LD_KC;
+    const int o = c_slot_id[sl];
+    const int64_t kg = k0 + kk;
+    double2 v = make_double2(0.0, 0.0);
+    if (o >= 0 && kg < K) {
+      if (perm) {
+        const int32_t code = c_sym_of[o];
+        v = T[(int64_t)(code >> 4) * K + perm[(int64_t)(code & 15) * K + kg]];
+      } else {
+        v = T[(int64_t)o * K + kg];
+      }
+    }
+    Ts[kk * M2LB_SLOTS + sl] = v;
+  }
+}
+
+// Sources of one neighbour-parent slot D for the batch's 8 groups: the CTA stages
+// Ms[g * 8 + e][kk] = M[child e of (P_g + D)][k0 + kk] (kk < M2LD_KC; 128-byte rows, cp.async,
+// zeros for missing children) so the DMMA B fragments come from shared memory -- loading them
+// straight from global memory put 32 different rows under every warp load (8x the L1
+// wavefronts of the DFMA kernel; ncu: L1TEX at 94% and the tensor pipe at 35%).
+__device__ __forceinline__ void m2ld_stage(double2 *Ms, const int32_t *sid_s, int D, const double2 *__restrict__ M,
+                                           int64_t K, int64_t k0) {
+  for (int i = threadIdx.x; i < 64 * M2LD_KC; i += blockDim.x) {
+    const int row = i / M2LD_KC, kk = i % M2LD_KC;
+    const int g = row >> 3, e = row & 7;
+    const int32_t sid = sid_s[(g * 27 + D) * 8 + e];
+    double2 *dst = Ms + row * M2LD_MP + kk;
+    if (sid >= 0 && k0 + kk < K) m2ld_cp16(dst, M + (int64_t)sid * K + k0 + kk);
+    else *dst = make_double2(0.0, 0.0);
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
+__global__ void __launch_bounds__(32 * M2LD_WARPS, 3) m2l_dmma_kernel(
+    int64_t K, int64_t ngroups, int64_t batches_per_unit, int64_t nunits, const int32_t *__restrict__ gtarget,
+    const int32_t *__restrict__ gsrc, const uint32_t *__restrict__ gmask, const double2 *__restrict__ T,
+    const int32_t *__restrict__ perm, const double2 *__restrict__ M, double2 *__restrict__ I) {
+  extern __shared__ double2 Ts[];  // [M2LD_KC][343] tables, [2][64][M2LD_MP] staged sources, source ids
+  double2 *Ms = Ts + M2LB_SLOTS * M2LD_KC;
+  int32_t *sid_s = reinterpret_cast<int32_t *>(Ms + 2 * 64 * M2LD_MP);  // [8 groups][27][8]
+  __shared__ uint32_t mask_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane >> 2, c = lane & 3;   // fragment row / column of this thread
+  const int64_t nchunks = (K + M2LD_KC - 1) / M2LD_KC;
+  const int64_t nbatch = (ngroups + 7) / 8;
+  const int64_t ranges = (nunits + nchunks - 1) / nchunks;
+  // A[d = r][e = c + 4 s]: offset delta = e - d in child units
+  const int dx0 = -(r >> 2), dy0 = -((r >> 1) & 1), dz0 = -(r & 1);
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t chunk = u / ranges, range = u % ranges;
+    const int64_t kbase = chunk * M2LD_KC;
+    __syncthreads();  // previous unit done with Ts
+    fill_tables_kmajor(Ts, T, perm, K, kbase);
+    const int kk = 2 * warp;                      // this warp's direction pair (kbase + kk, + 1)
+    const int64_t k = kbase + kk;
+    const bool kv0 = k < K, kv1 = k + 1 < K;
+    const int64_t b0 = range * batches_per_unit, b1 = min(nbatch, b0 + batches_per_unit);
+    for (int64_t bt = b0; bt < b1; ++bt) {
+      __syncthreads();  // tables filled / previous batch done with sid_s and Ms
+      for (int i = threadIdx.x; i < 8 * 27 * 8; i += blockDim.x) {
+        const int64_t g = bt * 8 + i / (27 * 8);
+        sid_s[i] = g < ngroups ? __ldg(&gsrc[bt * 8 * 27 * 8 + i]) : -1;
+      }
+      if (warp == 0) {
+        const uint32_t m = (lane < 8 && bt * 8 + lane < ngroups) ? __ldg(&gmask[bt * 8 + lane]) : 0u;
+        const uint32_t all = __reduce_or_sync(0xffffffffu, m);
+        if (lane == 0) mask_s = all;
+      }
+      __syncthreads();
+      uint32_t mask = mask_s;
+      double cre[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, cim[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [k][j]
+      int D = mask ? __ffs(mask) - 1 : 27;
+      int buf = 0;
+      if (D < 27) m2ld_stage(Ms, sid_s, D, M, K, kbase);
+      while (D < 27) {
+        const uint32_t rest = mask & ~((2u << D) - 1u);
+        const int Dn = rest ? __ffs(rest) - 1 : 27;
+        if (Dn < 27) {   // next parent's sources into the other buffer while this one is used
+          m2ld_stage(Ms + (buf ^ 1) * 64 * M2LD_MP, sid_s, Dn, M, K, kbase);
+          asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncthreads();
+        const double2 *Mb = Ms + buf * 64 * M2LD_MP;
+        const int Dx = D / 9 - 1, Dy = (D / 3) % 3 - 1, Dz = D % 3 - 1;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int e = c + 4 * s;
+          // A: T[2D + e - d][k, k + 1] from the k-major chunk tables
+          const int ox = 2 * Dx + (e >> 2) + dx0, oy = 2 * Dy + ((e >> 1) & 1) + dy0, oz = 2 * Dz + (e & 1) + dz0;
+          const int sl = (ox + 3) * 49 + (oy + 3) * 7 + (oz + 3);
+          const double2 a0 = Ts[kk * M2LB_SLOTS + sl], a1 = Ts[(kk + 1) * M2LB_SLOTS + sl];
+          // B: M[child e of (P_g + D)][k, k + 1], g = r
+          const double2 m0 = Mb[(r * 8 + e) * M2LD_MP + kk], m1 = Mb[(r * 8 + e) * M2LD_MP + kk + 1];
+          // C_re += A_re B_re - A_im B_im;  C_im += A_re B_im + A_im B_re  (k, then k + 1)
+          dmma_8x8x4(cre[0][0], cre[0][1], a0.x, m0.x);
+          dmma_8x8x4(cim[0][0], cim[0][1], a0.x, m0.y);
+          dmma_8x8x4(cre[1][0], cre[1][1], a1.x, m1.x);
+          dmma_8x8x4(cim[1][0], cim[1][1], a1.x, m1.y);
+          dmma_8x8x4(cre[0][0], cre[0][1], -a0.y, m0.y);
+          dmma_8x8x4(cim[0][0], cim[0][1], a0.y, m0.x);
+          dmma_8x8x4(cre[1][0], cre[1][1], -a1.y, m1.y);
+          dmma_8x8x4(cim[1][0], cim[1][1], a1.y, m1.x);
+        }
+        __syncthreads();  // every warp done with this buffer before it is refilled
+        buf ^= 1;
+        D = Dn;
+      }
+      // C[d = r][g = 2c + j] -> I[target d of group bt*8 + 2c + j][k, k + 1]
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t g = bt * 8 + 2 * c + j;
+        if (g >= ngroups) continue;
+        const int32_t b = __ldg(&gtarget[g * 8 + r]);
+        if (b < 0) continue;
+        if (kv0) I[(int64_t)b * K + k] = make_double2(cre[0][j], cim[0][j]);
+        if (kv1) I[(int64_t)b * K + k + 1] = make_double2(cre[1][j], cim[1][j]);
+      }
+    }
+  }
+}
+
 #ifndef HFMM_M2L_DENSE_MIN
 #define HFMM_M2L_DENSE_MIN 0.5  // use the parent-block kernel when useful / issued MACs >= this
 #endif
@@ -758,6 +921,19 @@ void m2l_group_apply(const M2LGroupPlan *pl, const double2 *T, const int32_t *pe
       // same units (groups_per_unit = per_warp x 16): 8 warps x 2 groups each cover them
       m2l_dense2_kernel<<<grid, 32 * M2LB2_WARPS, smem_b, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget,
                                                                pl->dsrc, pl->dmask, T, perm, M, I);
+    } else if (HFMM_M2L_DMMA) {
+      const size_t smem_d = ((size_t)M2LB_SLOTS * M2LD_KC + 2 * 64 * M2LD_MP) * sizeof(double2) + 8 * 27 * 8 * sizeof(int32_t);
+      cudaFuncSetAttribute(m2l_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+      // units = (8-direction chunk, range of 8-group batches), chunk-major over persistent CTAs
+      // (3 per SM); a unit holds up to 4 batches per CTA (the table fill amortised over 32 groups)
+      const int64_t nch = (pl->K + M2LD_KC - 1) / M2LD_KC;
+      const int64_t nbatch = (pl->ngroups + 7) / 8;
+      const int64_t bpu = std::max<int64_t>(1, std::min<int64_t>(4, nbatch / (3 * (int64_t)nsm)));
+      const int64_t rng = (nbatch + bpu - 1) / bpu;
+      const int64_t nu = nch * rng;
+      const unsigned gridd = (unsigned)std::min<int64_t>(nu, 3 * (int64_t)nsm);
+      m2l_dmma_kernel<<<gridd, 32 * M2LD_WARPS, smem_d, s>>>(pl->K, pl->ngroups, bpu, nu, pl->dtarget, pl->dsrc,
+                                                            pl->dmask, T, perm, M, I);
     } else {
       m2l_dense_kernel<<<grid, 32 * M2LG_WARPS, smem_b, s>>>(pl->K, pl->ngroups, gpu, nunits, pl->dtarget, pl->dsrc,
                                                            pl->dmask, T, perm, M, I);
