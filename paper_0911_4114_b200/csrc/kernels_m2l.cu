@@ -502,7 +502,8 @@ struct M2LGroupPlan {
 // Measured (same box, C2 B64): 78 ms with B fragments loaded from global memory (L1TEX 94% busy:
 // 32 rows per warp load), 69 ms with the batch's source ids staged, 62.7 ms with the sources
 // staged by cp.async (tensor pipe 39% active; stalls: DMMA dependency waits, shared-memory
-// scoreboards, 12 warps/SM) vs 41.7 ms for the DFMA parent-block kernel: kept off (parity-green).
+// scoreboards, 12 warps/SM; split accumulators, 8 chains per warp: 65.2 ms) vs 41.7 ms for the
+// DFMA parent-block kernel: kept off (parity-green).
 // Tables: the chunk's [M2LD_KC directions][343 cube slots] k-major in shared memory (a warp reads
 // 32 different slots of one direction: no bank conflicts), M from global / L2 as 32-byte (k, k+1)
 // pairs.  Same plan data (dtarget / dsrc / dmask) and the same terms as m2l_dense_kernel.
