@@ -431,6 +431,11 @@ __global__ void __launch_bounds__(RS_COLS_TPB) cols_kernel(const double2 *__rest
 #ifndef HFMM_RS2_MINB_DN
 #define HFMM_RS2_MINB_DN 4
 #endif
+#ifndef HFMM_RS2_REGACC
+#define HFMM_RS2_REGACC 1   // M2M column pass on power-of-two grids: sum the 8 children in registers (ACC
+                            // flavour; 2 CTAs/SM at 256 points) instead of through the output (A/B
+                            // profiles/r02/regacc_ab.txt: C2 B32 M2M 5.29 -> 5.11 ms, B64 20.1 -> 18.6-19.0 ms)
+#endif
 // ... for the power-of-two sizes (C2 grids) only: on the 7-smooth grids of the matvec configs the
 // extra CTAs per SM cost C3 0.45 ms per matvec next to the concurrent near field (3.74 -> 4.2 ms,
 // same box, profiles/r02/l2t_ab.txt "oldlb"), so those instantiations keep 3.
@@ -561,8 +566,9 @@ __global__ void __launch_bounds__(128, (rs2_minb<UP, true, FN1 * FN2, IN1 * IN2>
 // DOWN (L2L / anterpolation): unit = (child c, strip) of conj(shift[oct[c]]) * in[par[c]].
 constexpr int RS2_CW = 8, RS2_CWP = 9;
 
-template <bool UP, int FN1, int FN2, int IN1, int IN2>
-__global__ void __launch_bounds__(128, (rs2_minb<UP, false, FN1 * FN2, IN1 * IN2>())) cols2_kernel(const double2 *__restrict__ in, int64_t nitem, int ncols,
+template <bool UP, int FN1, int FN2, int IN1, int IN2, bool ACC = false>
+__global__ void __launch_bounds__(128, (ACC ? (IN1 * IN2 >= 256 ? 2 : 3) : rs2_minb<UP, false, FN1 * FN2, IN1 * IN2>()))
+cols2_kernel(const double2 *__restrict__ in, int64_t nitem, int ncols,
                                                    int rowlen, const int32_t *__restrict__ cbeg, int64_t cbase,
                                                    const int32_t *__restrict__ par, const int8_t *__restrict__ oct,
                                                    const double2 *__restrict__ shift,
@@ -607,6 +613,7 @@ __global__ void __launch_bounds__(128, (rs2_minb<UP, false, FN1 * FN2, IN1 * IN2
   if (u >= nunit) return;
   int64_t c0, c1;
   crange(u, c0, c1);
+  double2 acc[ACC ? IN2 : 1];   // ACC (M2M): the unit's child sum (this thread's outputs)
   int64_t c = c0;
   if (PF) issue(u, c);
   for (;;) {
@@ -703,6 +710,15 @@ __global__ void __launch_bounds__(128, (rs2_minb<UP, false, FN1 * FN2, IN1 * IN2
 #pragma unroll
               for (int k2 = 0; k2 < IN2; ++k2) x[k2] = c_mul(x[k2], t[k2]);
             }
+            if constexpr (ACC) {
+            // children summed in registers; one store after the unit's last child
+#pragma unroll
+            for (int k2 = 0; k2 < IN2; ++k2) acc[k2] = (c != c0) ? c_add(acc[k2], x[k2]) : x[k2];
+            if (c + 1 == c1) {
+#pragma unroll
+              for (int k2 = 0; k2 < IN2; ++k2) ob[(int64_t)(g + IN1 * k2) * ncols] = acc[k2];
+            }
+            } else {
             if (c != c0) {
               double2 t[IN2];
 #pragma unroll
@@ -712,6 +728,7 @@ __global__ void __launch_bounds__(128, (rs2_minb<UP, false, FN1 * FN2, IN1 * IN2
             }
 #pragma unroll
             for (int k2 = 0; k2 < IN2; ++k2) ob[(int64_t)(g + IN1 * k2) * ncols] = x[k2];
+            }
           }
         } else if (mok) {
           double2 *ob = out + c * (int64_t)N2 * ncols + m;
@@ -732,7 +749,9 @@ static void launch_cols2_t(const double2 *in, int64_t nitem, int ncols, int rowl
   constexpr int N = FN1 * FN2, N2 = IN1 * IN2;
   constexpr int BUFR = Max2<Max2<FN1 * (FN2 + 1), IN1 * (IN2 + 1)>::v, Max2<N, N2>::v>::v;
   const size_t smem = ((size_t)N + N2 + (size_t)(BUFR + (UP ? N : 0)) * RS2_CWP) * sizeof(double2);
-  auto kern = cols2_kernel<UP, FN1, FN2, IN1, IN2>;
+  auto kern = cols2_kernel<UP, FN1, FN2, IN1, IN2, false>;
+  if constexpr (UP && rs2_pow2(FN1 * FN2) && rs2_pow2(IN1 * IN2))
+    if (HFMM_RS2_REGACC && cbeg) kern = cols2_kernel<UP, FN1, FN2, IN1, IN2, true>;
   cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 148, per = 0;
   cudaGetDevice(&dev);
