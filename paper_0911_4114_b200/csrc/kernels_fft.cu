@@ -776,7 +776,7 @@ template <bool UP>
 static bool launch_cols2(const double2 *in, int64_t nitem, int nth, int ncols, int rowlen, int nth2,
                          const int32_t *cbeg, int64_t cbase, const int32_t *par, const int8_t *oct,
                          const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
-  if (!rs2_enabled() || std::max(nth, nth2) < (UP ? 128 : 64)) return false;
+  if (!rs2_enabled() || (std::max(nth, nth2) < (UP ? 128 : 64) && !(nth == 40 || nth2 == 40))) return false;
   switch (nth * 1000 + nth2) {
 #define RS2C(a, b, F1, F2, I1, I2) \
   case a * 1000 + b: launch_cols2_t<UP, F1, F2, I1, I2>(in, nitem, ncols, rowlen, cbeg, cbase, par, oct, shift, out, tw, s); return true;
@@ -799,6 +799,8 @@ static bool launch_cols2(const double2 *in, int64_t nitem, int nth, int ncols, i
     // accuracy-policy plans (tau = eps/10; C3_acc / C5_acc: 90x96 <-> 150x160)
     RS2C(90, 150, 10, 9, 15, 10)
     RS2C(150, 90, 15, 10, 10, 9)
+    RS2C(40, 90, 8, 5, 10, 9)     // two-pass alternative to box2 40 <-> 90x96 (HFMM_BOX2_4090=0)
+    RS2C(90, 40, 10, 9, 8, 5)
 #undef RS2C
     default: return false;
   }
@@ -848,6 +850,8 @@ static bool launch_rows2(const double2 *in, int64_t nbox, int nth, int nph, int 
     RS2R(240, 140, 16, 15, 14, 10)
     RS2R(96, 160, 12, 8, 16, 10)
     RS2R(160, 96, 16, 10, 12, 8)
+    RS2R(40, 96, 8, 5, 12, 8)
+    RS2R(96, 40, 12, 8, 8, 5)
 #undef RS2R
     default: return false;
   }
@@ -1256,6 +1260,14 @@ static void launch_box2_t(const double2 *in, int64_t nitem, const int32_t *cbeg,
 
 // (nth, nph) -> (nth2, nph2) upward resamples done in one pass (square grids of the C2 microbench
 // B8 / B16 and the C4 translation-only levels); false: use the two-pass kernels
+static bool box2_4090() {  // single pass for 40 <-> 90x96 (else the two-pass rs2 kernels; A/B)
+  static const int v = [] {
+    const char *e = getenv("HFMM_BOX2_4090");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 static bool box2_big() {  // single pass for 64 <-> 128 grids (A/B switch HFMM_BOX2_BIG)
   static const int v = [] {
     const char *e = getenv("HFMM_BOX2_BIG");
@@ -1275,7 +1287,7 @@ bool box2_up_applies(int nth, int nph, int nth2, int nph2) {
     case gkey(16, 16, 32, 32): case gkey(32, 32, 64, 64): case gkey(24, 24, 32, 32):
     case gkey(32, 32, 42, 48): case gkey(42, 48, 60, 60): case gkey(28, 28, 40, 40): case gkey(40, 40, 54, 56):
     case gkey(40, 40, 90, 96):
-      return true;
+      return box2_4090();
     case gkey(64, 64, 128, 128): return box2_big();
     default: return false;
   }
@@ -1287,7 +1299,7 @@ bool box2_down_applies(int nth, int nph, int nth2, int nph2) {
     case gkey(32, 32, 16, 16): case gkey(64, 64, 32, 32): case gkey(32, 32, 24, 24):
     case gkey(42, 48, 32, 32): case gkey(60, 60, 42, 48): case gkey(40, 40, 28, 28): case gkey(54, 56, 40, 40):
     case gkey(90, 96, 40, 40):
-      return true;
+      return box2_4090();
     case gkey(128, 128, 64, 64): return box2_big();
     default: return false;
   }
