@@ -195,6 +195,15 @@ std::recursive_mutex &hfmm::cache_mutex() {
       return HFMM_E_NCCL;                                                            \
     }                                                                                \
   } while (0)
+// inside an ncclGroupStart / ncclGroupEnd pair: remember the first failure, keep going so the
+// group is always closed (an error return from inside an open group would leave it open)
+#define CKG(call)                                                                    \
+  do {                                                                               \
+    if (gr_ == ncclSuccess) {                                                        \
+      gr_ = (call);                                                                  \
+      if (gr_ != ncclSuccess) p->err = std::string(#call) + ": " + ncclGetErrorString(gr_); \
+    }                                                                                \
+  } while (0)
 
 static void free_levels(hfmm_plan *p) {
   for (auto &L : p->lv) {
@@ -1128,14 +1137,15 @@ static int allgather_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
   NvtxRange nv("hfmm:allgather M_l");
   // all-gather of M_l over variable-size Morton ranges: one broadcast per root, grouped
   CKN(ncclGroupStart());
+  ncclResult_t gr_ = ncclSuccess;
   for (int r = 0; r < p->nranks; ++r) {
     size_t cnt = (size_t)(L.rhi[r] - L.rlo[r]) * L.K * 2;
     if (!cnt) continue;
     double *buf = (double *)(L.M + L.rlo[r] * L.K);
-    CKN(ncclBroadcast(buf, buf, cnt, ncclDouble, r, p->comm, s));
+    CKG(ncclBroadcast(buf, buf, cnt, ncclDouble, r, p->comm, s));
   }
   CKN(ncclGroupEnd());
-  return HFMM_OK;
+  return gr_ == ncclSuccess ? HFMM_OK : HFMM_E_NCCL;
 }
 
 // M2L halo of one level: grouped point-to-point sends of the packed owned boxes each peer needs and
@@ -1144,13 +1154,15 @@ static int halo_level(hfmm_plan *p, LevelDev &L, cudaStream_t s) {
   if (p->nranks <= 1) return HFMM_OK;
   NvtxRange nv("hfmm:halo M_l");
   CKN(ncclGroupStart());
+  ncclResult_t gr_ = ncclSuccess;
   for (int q = 0; q < p->nranks; ++q) {
     if (q == p->rank) continue;
     const size_t ns = (size_t)(L.hs_off[q + 1] - L.hs_off[q]) * L.K * 2, nr = (size_t)(L.hr_off[q + 1] - L.hr_off[q]) * L.K * 2;
-    if (ns) CKN(ncclSend((const double *)(L.hs_buf + L.hs_off[q] * L.K), ns, ncclDouble, q, p->comm, s));
-    if (nr) CKN(ncclRecv((double *)(L.hr_buf + L.hr_off[q] * L.K), nr, ncclDouble, q, p->comm, s));
+    if (ns) CKG(ncclSend((const double *)(L.hs_buf + L.hs_off[q] * L.K), ns, ncclDouble, q, p->comm, s));
+    if (nr) CKG(ncclRecv((double *)(L.hr_buf + L.hr_off[q] * L.K), nr, ncclDouble, q, p->comm, s));
   }
   CKN(ncclGroupEnd());
+  if (gr_ != ncclSuccess) return HFMM_E_NCCL;
   if (L.hr_off.back() > 0) launch_gather_boxes(L.hr_buf, nullptr, L.M, L.hr_idx, L.hr_off.back(), L.K, s);
   return HFMM_OK;
 }
@@ -1325,13 +1337,15 @@ static int gather_y(hfmm_plan *p, cudaStream_t s) {
   // of the (variable-size) ranges -- one broadcast per root, grouped -- then every rank
   // unpermutes the whole vector (N x 16 B per rank on the wire instead of an all-reduce's 2x)
   CKN(ncclGroupStart());
+  ncclResult_t gr_ = ncclSuccess;
   for (int r = 0; r < p->nranks; ++r) {
     const size_t cnt = (size_t)(p->pt_hi[r] - p->pt_lo[r]) * 2;
     if (!cnt) continue;
     double *buf = (double *)(p->y_sorted + p->pt_lo[r]);
-    CKN(ncclBroadcast(buf, buf, cnt, ncclDouble, r, p->comm, s));
+    CKG(ncclBroadcast(buf, buf, cnt, ncclDouble, r, p->comm, s));
   }
   CKN(ncclGroupEnd());
+  if (gr_ != ncclSuccess) return HFMM_E_NCCL;
   launch_combine(p->y_sorted, nullptr, p->perm, p->y_out, p->tree.n, 0, p->tree.n, s);
   return HFMM_OK;
 }
