@@ -776,7 +776,10 @@ template <bool UP>
 static bool launch_cols2(const double2 *in, int64_t nitem, int nth, int ncols, int rowlen, int nth2,
                          const int32_t *cbeg, int64_t cbase, const int32_t *par, const int8_t *oct,
                          const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
-  if (!rs2_enabled() || (std::max(nth, nth2) < (UP ? 128 : 64) && !(nth == 40 || nth2 == 40))) return false;
+  // size floor (same-box A/Bs on the power-of-two C2 grids); the 7-smooth matvec pairs always take the
+  // register-resident pass when instantiated (C3 / C5 54 -> 120 upward: the tiled column pass took 3x
+  // the time of the downward cols2 pass, profiles/r02/launches_c3_r02f.csv)
+  if (!rs2_enabled() || (std::max(nth, nth2) < (UP ? 128 : 64) && rs2_pow2(nth) && rs2_pow2(nth2))) return false;
   switch (nth * 1000 + nth2) {
 #define RS2C(a, b, F1, F2, I1, I2) \
   case a * 1000 + b: launch_cols2_t<UP, F1, F2, I1, I2>(in, nitem, ncols, rowlen, cbeg, cbase, par, oct, shift, out, tw, s); return true;
