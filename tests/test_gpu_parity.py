@@ -406,13 +406,15 @@ def test_deterministic_near_field(hf, case):
 
 
 # ---- P2P tile per plan: 384 / 512 / 1,024-point target tiles -------------------
+@pytest.mark.parametrize("rowskip", ["on", "off"])
 @pytest.mark.parametrize("pt", [3, 4, 8])
 @pytest.mark.parametrize("case", ["fmm", "nofar"])
-def test_p2p_tiles_agree(hf, pt, case, monkeypatch):
-    """Every P2P instantiation the plan can pick (3, 4 or 8 targets per thread; forced with
-    HFMM_P2P_PT) gives the oracle's matvec.  "nofar": no admissible level, so the matvec is
-    the near field over the whole point set -- several 1,024-point tiles, a ragged last tile,
-    symmetric tile pairs and diagonal tiles; "fmm": leaves smaller than a tile (partial tiles).
+def test_p2p_tiles_agree(hf, pt, case, rowskip, monkeypatch):
+    """Every P2P instantiation the plan can pick (3, 4 or 8 targets per thread, forced with
+    HFMM_P2P_PT; the row-skipping flavour forced on / off with HFMM_P2P_ROWSKIP_MIN = 0 / 1, DESIGN
+    6.1) gives the oracle's matvec.  "nofar": no admissible level, so the matvec is the near
+    field over the whole point set -- several 1,024-point tiles, a ragged last tile, symmetric tile
+    pairs and diagonal tiles; "fmm": leaves smaller than a tile (partial tiles, dead warp rows).
     The all-pairs entry point (hfmm_direct) with the same tile == the oracle's direct sum."""
     if case == "nofar":
         cfg = small_config("p2p_pt_nofar", n=3001, kappa=2 * math.pi, depth=3, eps=1e-4, seed=31)
@@ -420,9 +422,12 @@ def test_p2p_tiles_agree(hf, pt, case, monkeypatch):
         cfg = small_config("p2p_pt_fmm", n=6000, kappa=8 * math.pi, depth=3, eps=1e-6, seed=31)
     x, q = points_and_charges(cfg)
     monkeypatch.setenv("HFMM_P2P_PT", str(pt))
+    monkeypatch.setenv("HFMM_P2P_ROWSKIP_MIN", "0" if rowskip == "on" else "1")
     g = gpu_plan(hf, cfg, x)
     monkeypatch.delenv("HFMM_P2P_PT")
+    monkeypatch.delenv("HFMM_P2P_ROWSKIP_MIN")
     assert g.info()["p2p_tile"] == 128 * pt
+    assert g.info()["p2p_rowskip"] == (rowskip == "on" and pt != 8)
     y, yd = g.matvec(q), g.direct(q)
     yref = direct_sum(x, q, cfg.kappa)
     assert rel(yd, yref) <= PARITY
