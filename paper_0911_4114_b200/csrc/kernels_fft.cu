@@ -866,6 +866,20 @@ static bool launch_rows2(const double2 *in, int64_t nbox, int nth, int nph, int 
 // intermediate, then the column pass (8 columns x 16 group lanes per 4 warps) reads the theta-
 // periodic columns from it and stores the shifted (and child-summed) parent field.  The
 // intermediate never leaves the SM: HBM traffic is the algorithmic read-child + write-parent.
+// Column strips of the single-pass kernels: CW columns x GC group lanes per 128 threads, GC the
+// power of two covering the column DFT factors -- 8 lanes (16 columns) when every factor is <= 8,
+// so the stages with 4-6 active lanes no longer idle half of a 16-lane group (HFMM_BOX2_WIDE=0: the
+// previous 8 x 16 strips).
+#ifndef HFMM_BOX2_WIDE
+#define HFMM_BOX2_WIDE 1
+#endif
+template <int CF1, int CF2, int CI1, int CI2>
+struct Box2Cols {
+  static constexpr int GM = Max2<Max2<CF1, CF2>::v, Max2<CI1, CI2>::v>::v;
+  static constexpr int GC = (HFMM_BOX2_WIDE && GM <= 8) ? 8 : 16;
+  static constexpr int CW = 128 / GC, CWP = CW + 1;
+};
+
 template <int RF1, int RF2, int RI1, int RI2, int CF1, int CF2, int CI1, int CI2>
 __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict__ in, int64_t nitem,
                                                      const int32_t *__restrict__ cbeg, int64_t cbase,
@@ -876,6 +890,7 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
                                                      double2 *__restrict__ out) {
   constexpr int NR = RF1 * RF2, NR2 = RI1 * RI2;   // nph -> nph2 (rows)
   constexpr int NC = CF1 * CF2, NC2 = CI1 * CI2;   // nth -> nth2 (columns)
+  using BC = Box2Cols<CF1, CF2, CI1, CI2>;
   constexpr int h = NR / 2, h2 = NR2 / 2, nrow = NC / 2 + 1;
   constexpr int GM = Max2<Max2<RF1, RF2>::v, Max2<RI1, RI2>::v>::v;
   constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;
@@ -888,7 +903,7 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
   double2 *tr1 = sm, *tr2 = tr1 + NR, *tc1 = tr2 + NR2, *tc2 = tc1 + NC;
   double2 *inter = tc2 + NC2;                      // [nrow][IP]
   double2 *rbuf = inter + nrow * IP;               // [4 warps][VW][RBUF]
-  double2 *cbuf = rbuf + 4 * VW * RBUF;            // [CBUF][RS2_CWP]
+  double2 *cbuf = rbuf + 4 * VW * RBUF;            // [CBUF][BC::CWP]
   for (int j = threadIdx.x; j < NR; j += blockDim.x) tr1[j] = twR[j];
   for (int j = threadIdx.x; j < NR2; j += blockDim.x) tr2[j] = twR2[j];
   for (int j = threadIdx.x; j < NC; j += blockDim.x) tc1[j] = twC[j];
@@ -896,7 +911,7 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / G, gr = lane - grp * G;   // row pass: lane group, lane in group
   double2 *rb = rbuf + (warp * VW + grp) * RBUF;
-  const int v = threadIdx.x & (RS2_CW - 1), g = threadIdx.x >> 3;  // column pass
+  const int v = threadIdx.x % BC::CW, g = threadIdx.x / BC::CW;  // column pass
   for (int64_t item = blockIdx.x; item < nitem; item += gridDim.x) {
     int64_t c0 = item, c1 = item + 1;
     if (cbeg) c0 = cbeg[item], c1 = cbeg[item + 1];
@@ -964,7 +979,7 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
         __syncwarp();
       }
       // ---- columns m < h2 of the intermediate: nth -> nth2, shift, sum into the parent ----
-      for (int m0 = 0; m0 < h2; m0 += RS2_CW) {
+      for (int m0 = 0; m0 < h2; m0 += BC::CW) {
         const int m = m0 + v;
         const bool mok = m < h2;
         __syncthreads();  // intermediate complete / previous strip's cbuf consumed
@@ -979,18 +994,18 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
 #pragma unroll
           for (int k1 = 1; k1 < CF1; ++k1) x[k1] = c_mul(x[k1], tc1[g * k1]);
 #pragma unroll
-          for (int k1 = 0; k1 < CF1; ++k1) cbuf[(k1 * (CF2 + 1) + g) * RS2_CWP + v] = x[k1];
+          for (int k1 = 0; k1 < CF1; ++k1) cbuf[(k1 * (CF2 + 1) + g) * BC::CWP + v] = x[k1];
         }
         __syncthreads();
         if (g < CF1) {
 #pragma unroll
-          for (int n2 = 0; n2 < CF2; ++n2) x[n2] = cbuf[(g * (CF2 + 1) + n2) * RS2_CWP + v];
+          for (int n2 = 0; n2 < CF2; ++n2) x[n2] = cbuf[(g * (CF2 + 1) + n2) * BC::CWP + v];
         }
         __syncthreads();
         if (g < CF1) {
           dft<CF2>(x);
 #pragma unroll
-          for (int k2 = 0; k2 < CF2; ++k2) cbuf[(g + CF1 * k2) * RS2_CWP + v] = x[k2];
+          for (int k2 = 0; k2 < CF2; ++k2) cbuf[(g + CF1 * k2) * BC::CWP + v] = x[k2];
         }
         __syncthreads();
         if (g < CI2) {
@@ -1000,7 +1015,7 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
             const int f = (i <= NC2 / 2) ? i : i - NC2;
             double2 z = make_double2(0.0, 0.0);
             if (f <= KC && f >= -KC) {
-              const double2 y = cbuf[(f >= 0 ? f : f + NC) * RS2_CWP + v];
+              const double2 y = cbuf[(f >= 0 ? f : f + NC) * BC::CWP + v];
               z = make_double2(y.x * (1.0 / NC), -y.y * (1.0 / NC));
             }
             x[m1] = z;
@@ -1012,12 +1027,12 @@ __global__ void __launch_bounds__(128) box2_up_kernel(const double2 *__restrict_
 #pragma unroll
           for (int k1 = 1; k1 < CI1; ++k1) x[k1] = c_mul(x[k1], tc2[g * k1]);
 #pragma unroll
-          for (int k1 = 0; k1 < CI1; ++k1) cbuf[(k1 * (CI2 + 1) + g) * RS2_CWP + v] = x[k1];
+          for (int k1 = 0; k1 < CI1; ++k1) cbuf[(k1 * (CI2 + 1) + g) * BC::CWP + v] = x[k1];
         }
         __syncthreads();
         if (g < CI1 && mok) {
 #pragma unroll
-          for (int n2 = 0; n2 < CI2; ++n2) x[n2] = cbuf[(g * (CI2 + 1) + n2) * RS2_CWP + v];
+          for (int n2 = 0; n2 < CI2; ++n2) x[n2] = cbuf[(g * (CI2 + 1) + n2) * BC::CWP + v];
           dft<CI2>(x);
           double2 *ob = out + item * (int64_t)NC2 * h2 + m;
 #pragma unroll
@@ -1058,6 +1073,7 @@ __global__ void __launch_bounds__(128) box2_down_kernel(const double2 *__restric
                                                        const double2 *__restrict__ add, double2 *__restrict__ out) {
   constexpr int NR = RF1 * RF2, NR2 = RI1 * RI2;   // nph -> nph2 (rows)
   constexpr int NC = CF1 * CF2, NC2 = CI1 * CI2;   // nth -> nth2 (columns)
+  using BC = Box2Cols<CF1, CF2, CI1, CI2>;
   constexpr int h = NR / 2, h2 = NR2 / 2, nrow = NC2 / 2 + 1;
   constexpr int GM = Max2<Max2<RF1, RF2>::v, Max2<RI1, RI2>::v>::v;
   constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;
@@ -1078,13 +1094,13 @@ __global__ void __launch_bounds__(128) box2_down_kernel(const double2 *__restric
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / G, gr = lane - grp * G;
   double2 *rb = rbuf + (warp * VW + grp) * RBUF;
-  const int v = threadIdx.x & (RS2_CW - 1), g = threadIdx.x >> 3;
+  const int v = threadIdx.x % BC::CW, g = threadIdx.x / BC::CW;
   for (int64_t c = blockIdx.x; c < nitem; c += gridDim.x) {
     double2 x[16];
     const double2 *pb = in + (int64_t)(par ? par[c] : c) * NC * h;
     const double2 *sbase = shift ? shift + (int64_t)(oct ? oct[c] : 0) * NC * h : nullptr;
     // ---- columns m < h of the shifted parent: nth -> nth2 into inter[t][m] ----
-    for (int m0 = 0; m0 < h; m0 += RS2_CW) {
+    for (int m0 = 0; m0 < h; m0 += BC::CW) {
       const int m = m0 + v;
       const bool mok = m < h;
       __syncthreads();
@@ -1102,18 +1118,18 @@ __global__ void __launch_bounds__(128) box2_down_kernel(const double2 *__restric
 #pragma unroll
         for (int k1 = 1; k1 < CF1; ++k1) x[k1] = c_mul(x[k1], tc1[g * k1]);
 #pragma unroll
-        for (int k1 = 0; k1 < CF1; ++k1) cbuf[(k1 * (CF2 + 1) + g) * RS2_CWP + v] = x[k1];
+        for (int k1 = 0; k1 < CF1; ++k1) cbuf[(k1 * (CF2 + 1) + g) * BC::CWP + v] = x[k1];
       }
       __syncthreads();
       if (g < CF1) {
 #pragma unroll
-        for (int n2 = 0; n2 < CF2; ++n2) x[n2] = cbuf[(g * (CF2 + 1) + n2) * RS2_CWP + v];
+        for (int n2 = 0; n2 < CF2; ++n2) x[n2] = cbuf[(g * (CF2 + 1) + n2) * BC::CWP + v];
       }
       __syncthreads();
       if (g < CF1) {
         dft<CF2>(x);
 #pragma unroll
-        for (int k2 = 0; k2 < CF2; ++k2) cbuf[(g + CF1 * k2) * RS2_CWP + v] = x[k2];
+        for (int k2 = 0; k2 < CF2; ++k2) cbuf[(g + CF1 * k2) * BC::CWP + v] = x[k2];
       }
       __syncthreads();
       if (g < CI2) {
@@ -1123,7 +1139,7 @@ __global__ void __launch_bounds__(128) box2_down_kernel(const double2 *__restric
           const int f = (i <= NC2 / 2) ? i : i - NC2;
           double2 z = make_double2(0.0, 0.0);
           if (f <= KC && f >= -KC) {
-            const double2 y = cbuf[(f >= 0 ? f : f + NC) * RS2_CWP + v];
+            const double2 y = cbuf[(f >= 0 ? f : f + NC) * BC::CWP + v];
             z = make_double2(y.x * (1.0 / NC), -y.y * (1.0 / NC));
           }
           x[m1] = z;
@@ -1135,12 +1151,12 @@ __global__ void __launch_bounds__(128) box2_down_kernel(const double2 *__restric
 #pragma unroll
         for (int k1 = 1; k1 < CI1; ++k1) x[k1] = c_mul(x[k1], tc2[g * k1]);
 #pragma unroll
-        for (int k1 = 0; k1 < CI1; ++k1) cbuf[(k1 * (CI2 + 1) + g) * RS2_CWP + v] = x[k1];
+        for (int k1 = 0; k1 < CI1; ++k1) cbuf[(k1 * (CI2 + 1) + g) * BC::CWP + v] = x[k1];
       }
       __syncthreads();
       if (g < CI1 && mok) {
 #pragma unroll
-        for (int n2 = 0; n2 < CI2; ++n2) x[n2] = cbuf[(g * (CI2 + 1) + n2) * RS2_CWP + v];
+        for (int n2 = 0; n2 < CI2; ++n2) x[n2] = cbuf[(g * (CI2 + 1) + n2) * BC::CWP + v];
         dft<CI2>(x);
 #pragma unroll
         for (int k2 = 0; k2 < CI2; ++k2) inter[(g + CI1 * k2) * IP + m] = c_conj(x[k2]);
@@ -1223,12 +1239,13 @@ static void launch_box2d_t(const double2 *in, int64_t nitem, const int32_t *par,
                            const double2 *shift, const double2 *add, double2 *out, const TwiddleSet &tw,
                            cudaStream_t s) {
   constexpr int NR = RF1 * RF2, NR2 = RI1 * RI2, NC = CF1 * CF2, NC2 = CI1 * CI2;
+  using BC = Box2Cols<CF1, CF2, CI1, CI2>;
   constexpr int GM = Max2<Max2<RF1, RF2>::v, Max2<RI1, RI2>::v>::v;
   constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;
   constexpr int RBUF = Max2<Max2<RF1 * (RF2 + 1), RI1 * (RI2 + 1)>::v, Max2<NR, NR2>::v>::v;
   constexpr int CBUF = Max2<Max2<CF1 * (CF2 + 1), CI1 * (CI2 + 1)>::v, Max2<NC, NC2>::v>::v;
   const size_t smem = ((size_t)NR + NR2 + NC + NC2 + (size_t)NC2 * (NR / 2 + 1) + 4 * (32 / G) * RBUF +
-                       (size_t)CBUF * RS2_CWP) * sizeof(double2);
+                       (size_t)CBUF * BC::CWP) * sizeof(double2);
   auto kern = box2_down_kernel<RF1, RF2, RI1, RI2, CF1, CF2, CI1, CI2>;
   cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 148, per = 0;
@@ -1244,12 +1261,13 @@ template <int RF1, int RF2, int RI1, int RI2, int CF1, int CF2, int CI1, int CI2
 static void launch_box2_t(const double2 *in, int64_t nitem, const int32_t *cbeg, int64_t cbase, const int8_t *oct,
                           const double2 *shift, double2 *out, const TwiddleSet &tw, cudaStream_t s) {
   constexpr int NR = RF1 * RF2, NR2 = RI1 * RI2, NC = CF1 * CF2, NC2 = CI1 * CI2;
+  using BC = Box2Cols<CF1, CF2, CI1, CI2>;
   constexpr int GM = Max2<Max2<RF1, RF2>::v, Max2<RI1, RI2>::v>::v;
   constexpr int G = GM <= 1 ? 1 : GM <= 2 ? 2 : GM <= 4 ? 4 : GM <= 8 ? 8 : 16;
   constexpr int RBUF = Max2<Max2<RF1 * (RF2 + 1), RI1 * (RI2 + 1)>::v, Max2<NR, NR2>::v>::v;
   constexpr int CBUF = Max2<Max2<CF1 * (CF2 + 1), CI1 * (CI2 + 1)>::v, Max2<NC, NC2>::v>::v;
   const size_t smem = ((size_t)NR + NR2 + NC + NC2 + (size_t)(NC / 2 + 1) * (NR2 + 1) + 4 * (32 / G) * RBUF +
-                       (size_t)CBUF * RS2_CWP) * sizeof(double2);
+                       (size_t)CBUF * BC::CWP) * sizeof(double2);
   auto kern = box2_up_kernel<RF1, RF2, RI1, RI2, CF1, CF2, CI1, CI2>;
   cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 148, per = 0;
