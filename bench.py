@@ -390,6 +390,7 @@ def bench_matvec_config(cfg, warmup: int, steps: int, tau: float = 0.0, golden: 
            "L_f": info["L_f"], "source_level": info["source_level"], "ms_per_matvec": t, "matvec_per_s": 1e3 / t,
            "mpoints_per_s": cfg.n / t / 1e3, "p2p_pairs": info["p2p_pairs"], "steps": steps,
            "p2p_tile": info["p2p_tile"], "p2p_rowskip": info["p2p_rowskip"], "p2p_dead_frac": info["p2p_dead_frac"],
+           "p2p_mixed_items": info["p2p_mixed_items"],
            "parity": golden_parity(golden or cfg.name, yd.cpu().numpy(), info)}
     g.close()
     del qd, yd, flush
@@ -629,7 +630,7 @@ def main():
                  "levels": [{k: lv[k] for k in ("level", "ell", "n_theta", "n_phi", "F", "active")}
                             for lv in info["levels"]], "p2p_pairs": pairs, "s2m_evals": info["s2m_evals"],
                  "p2p_tile": info["p2p_tile"], "p2p_rowskip": info["p2p_rowskip"],
-                 "p2p_dead_frac": info["p2p_dead_frac"]},
+                 "p2p_dead_frac": info["p2p_dead_frac"], "p2p_mixed_items": info["p2p_mixed_items"]},
         "setup_s": {"build_tree": t_tree, "precompute": t_pre},
         "clocks": clocks,
     }

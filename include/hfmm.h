@@ -137,6 +137,9 @@ typedef struct {
                               a tile's end (chosen when > 8% of the tile slots are dead)        */
   double p2p_dead_frac;    /* fraction of the P2P tile slots (128 x targets-per-thread x padded
                               sources) that hold no live target                                */
+  int64_t p2p_mixed_items; /* mixed tiles: work items of the <= 384-point target-tile class (each
+                              leaf cut into full 512-point tiles plus <= 384-point ones, one
+                              launch per class); 0 when the plan uses one tile size             */
 } hfmm_info;
 
 /* Create a plan on CUDA device `device` (-1: the current device).  *out receives the plan. */

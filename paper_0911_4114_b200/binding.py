@@ -60,7 +60,7 @@ class Info(C.Structure):
                 ("s2m_evals", C.c_int64),
                 ("rank", C.c_int), ("nranks", C.c_int), ("owned_points", C.c_int64),
                 ("source_level", C.c_int), ("launches", C.c_int), ("p2p_tile", C.c_int), ("next4_passes", C.c_int),
-                ("p2p_rowskip", C.c_int), ("p2p_dead_frac", C.c_double)]
+                ("p2p_rowskip", C.c_int), ("p2p_dead_frac", C.c_double), ("p2p_mixed_items", C.c_int64)]
 
 
 class HFMMError(RuntimeError):
@@ -333,7 +333,8 @@ class HFMM:
                     s2m_evals=inf.s2m_evals, rank=inf.rank, nranks=inf.nranks, owned_points=inf.owned_points,
                     source_level=(None if inf.source_level < 0 else inf.source_level), launches=inf.launches,
                     p2p_tile=inf.p2p_tile, next4_passes=inf.next4_passes,
-                    p2p_rowskip=bool(inf.p2p_rowskip), p2p_dead_frac=inf.p2p_dead_frac)
+                    p2p_rowskip=bool(inf.p2p_rowskip), p2p_dead_frac=inf.p2p_dead_frac,
+                    p2p_mixed_items=int(inf.p2p_mixed_items))
 
     def stage_times(self):
         out = (C.c_double * 8)()

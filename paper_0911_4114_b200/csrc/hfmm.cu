@@ -116,6 +116,8 @@ struct hfmm_plan {
   int device = 0;
   cudaStream_t stream = nullptr, stream2 = nullptr, stream_hi = nullptr;  // near field low, far chain high priority
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join_hi = nullptr;
+  cudaStream_t stream3 = nullptr;   // second near-field stream (low priority): the <= 384-point tile class
+  cudaEvent_t ev_mix = nullptr;     // ... joined into stream2 before the near-field reduction
   cudaEvent_t ev_up = nullptr;   // far chain: M_l of every level up to date (virtual-rank exchange)
   std::string err;
   bool have_tree = false, have_plan = false;
@@ -148,6 +150,8 @@ struct hfmm_plan {
   // all-pairs items of hfmm_direct; positions pre-scaled to table steps (kappa-dependent)
   int64_t *p2p_items[3] = {nullptr, nullptr, nullptr};
   int64_t p2p_nitems[3] = {0, 0, 0};
+  int64_t p2p_n4[3] = {0, 0, 0};   // mixed tiles: the first p2p_n4[k] items hold 512-point tiles, the rest <= 384
+  bool p2p_mix = false;            // 512- and 384-point target tiles mixed per leaf (fewest padded slots)
   int64_t *dir_items = nullptr;
   int64_t dir_nitems = 0;
   double *ux = nullptr, *uy = nullptr, *uz = nullptr;
@@ -283,15 +287,18 @@ extern "C" int hfmm_create(hfmm_plan **out, int device) {
     CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
 #if HFMM_STREAM_PRIORITY
     CKC(cudaStreamCreateWithPriority(&p->stream2, cudaStreamNonBlocking, lo));
+    CKC(cudaStreamCreateWithPriority(&p->stream3, cudaStreamNonBlocking, lo));
     CKC(cudaStreamCreateWithPriority(&p->stream_hi, cudaStreamNonBlocking, hi));
 #else
     CKC(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&p->stream3, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithFlags(&p->stream_hi, cudaStreamNonBlocking));
 #endif
   }
   CKC(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_join_hi, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&p->ev_mix, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&p->ev_up, cudaEventDisableTiming));
   for (auto &e : p->sev) CKC(cudaEventCreate(&e));
   const char *prof = std::getenv("HFMM_PROFILE_STAGES");
@@ -837,6 +844,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     std::vector<int64_t> it[3];
     int64_t pairs = 0, sym_pairs = 0;
     int64_t tile = (int64_t)P2P_TPB_HOST * 4;   // targets per item: 128 threads x PT targets
+    bool mix_tiles = false;
+    const double kMix3Cost = 1.08;   // per-slot cost of the 384-point kernel relative to the 512-point one
     auto add = [&](int kind, int64_t t0, int64_t t1, int64_t s0, int64_t s1) {
       if (t1 <= t0 || s1 <= s0) return;
       it[kind].insert(it[kind].end(), {t0, t1, s0, s1});
@@ -844,10 +853,28 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     auto own_box = [&](int64_t A0, int64_t A1, const std::vector<std::pair<int64_t, int64_t>> &others_owned,
                        const std::vector<std::pair<int64_t, int64_t>> &others_foreign) {
       // targets [A0, A1) of one owned box; others_* = neighbour ranges (sym: only beta > alpha)
-      for (int64_t t0 = A0; t0 < A1; t0 += tile) {
-        const int64_t t1 = std::min(t0 + tile, A1);
+      // tile boundaries of the box: fixed tiles, or (mix_tiles) a full 512-point tiles followed by
+      // b tiles of <= 384 points, (a, b) minimising the padded slots 512 a + kMix3Cost 384 b
+      std::vector<int64_t> cut{A0};
+      if (!mix_tiles) {
+        for (int64_t t0 = A0; t0 < A1; t0 += tile) cut.push_back(std::min(t0 + tile, A1));
+      } else {
+        const int64_t nA = A1 - A0, T4 = (int64_t)P2P_TPB_HOST * 4, T3 = (int64_t)P2P_TPB_HOST * 3;
+        int64_t ba = 0, bb = 0;
+        double best = 1e300;
+        for (int64_t a = 0; a <= (nA + T4 - 1) / T4; ++a) {
+          const int64_t rest = std::max<int64_t>(0, nA - a * T4), b = (rest + T3 - 1) / T3;
+          const double c = (double)(a * T4) + kMix3Cost * (double)(b * T3);
+          if (c < best) best = c, ba = a, bb = b;
+        }
+        int64_t t0 = A0;
+        for (int64_t a = 0; a < ba && t0 < A1; ++a) t0 = std::min(t0 + T4, A1), cut.push_back(t0);
+        for (int64_t b = 0; b < bb && t0 < A1; ++b) t0 = std::min(t0 + T3, A1), cut.push_back(t0);
+      }
+      for (size_t c = 0; c + 1 < cut.size(); ++c) {
+        const int64_t t0 = cut[c], t1 = cut[c + 1];
         add(P2P_DIAG, t0, t1, t0, t1);
-        for (int64_t u0 = t1; u0 < A1; u0 += tile) add(P2P_SYM, t0, t1, u0, std::min(u0 + tile, A1));
+        for (size_t d = c + 1; d + 1 < cut.size(); ++d) add(P2P_SYM, t0, t1, cut[d], cut[d + 1]);
         for (auto &r : others_owned) add(P2P_SYM, t0, t1, r.first, r.second);
         for (auto &r : others_foreign) add(P2P_ORD, t0, t1, r.first, r.second);
       }
@@ -908,7 +935,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
         double sl = 0.0;
         for (auto &v : it)
           for (size_t i = 0; i < v.size(); i += 4) {
-            const double rows = live_only ? (double)((v[i + 1] - v[i] + 31) / 32 * 32) : (double)P2P_TPB_HOST * pt;
+            const int ptm = mix_tiles ? (v[i + 1] - v[i] > 3 * (int64_t)P2P_TPB_HOST ? 4 : 3) : pt;
+            const double rows = live_only ? (double)((v[i + 1] - v[i] + 31) / 32 * 32) : (double)P2P_TPB_HOST * ptm;
             sl += rows * (double)((v[i + 3] - v[i + 2] + 31) / 32 * 32);
           }
         return sl;
@@ -942,6 +970,20 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
           }
         }
       }
+      // Mixed tiles (default when the plan kept 512-point tiles; HFMM_P2P_MIX=0 opts out): each leaf is
+      // cut into full 512-point tiles plus <= 384-point tiles, launched as two item classes (4 and 3
+      // targets per thread), instead of a last 512-slot tile that is mostly padding.
+      {
+        const char *e = getenv("HFMM_P2P_MIX");
+        const int mode = e ? atoi(e) : 1;   // 2: also on short grids (tests)
+        if (!force && ((mode == 1 && p->p2p_pt == 4 && !short_grid) || mode == 2)) {
+          p->p2p_pt = 4;
+          mix_tiles = true;
+          tile = (int64_t)P2P_TPB_HOST * 4;
+          build_items();
+          p->p2p_mix = true;
+        }
+      }
     // Row skipping (p2p_sym_kernel<..., RS = true>): warps skip their target rows wholly past the
     // tile's end.  Its per-slot rate is lower (same-box A/Bs, profiles/r02/rowskip_ab*.txt: C4 / C5
     // 0.7% / 2.4% slower with 5% / 4% dead slots; C3_acc 7% and C5_acc 4% faster with 29% / 17%
@@ -951,7 +993,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       double thr = 0.08;
       if (const char *e = getenv("HFMM_P2P_ROWSKIP_MIN")) thr = atof(e);
       const double full = padded_slots(p->p2p_pt), live = padded_slots(p->p2p_pt, true);
-      p->p2p_rowskip = p->p2p_pt != 8 && full > 0.0 && (live < (1.0 - thr) * full || (short_grid && thr < 1.0));
+      p->p2p_rowskip = !p->p2p_mix && p->p2p_pt != 8 && full > 0.0 &&
+                       (live < (1.0 - thr) * full || (short_grid && thr < 1.0));
       p->p2p_dead_frac = full > 0.0 ? 1.0 - live / full : 0.0;
     }
     }
@@ -962,7 +1005,17 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       std::vector<int64_t> ord(m);
       std::iota(ord.begin(), ord.end(), 0);
       auto cost = [&](int64_t i) { return (it[k][4 * i + 1] - it[k][4 * i]) * (it[k][4 * i + 3] - it[k][4 * i + 2]); };
-      std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return cost(x) > cost(y); });
+      // mixed tiles: the 512-point class first (one launch per class), longest first inside a class
+      auto small = [&](int64_t i) { return p->p2p_mix && it[k][4 * i + 1] - it[k][4 * i] <= 3 * (int64_t)P2P_TPB_HOST; };
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
+        if (small(x) != small(y)) return small(y);
+        return cost(x) > cost(y);
+      });
+      p->p2p_n4[k] = m;
+      if (p->p2p_mix) {
+        p->p2p_n4[k] = 0;
+        for (int64_t i = 0; i < m; ++i) p->p2p_n4[k] += small(i) ? 0 : 1;
+      }
       std::vector<int64_t> sorted(4 * m);
       for (int64_t i = 0; i < m; ++i)
         for (int c = 0; c < 4; ++c) sorted[4 * i + c] = it[k][4 * ord[i] + c];
@@ -1089,7 +1142,10 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
   in.source_level = p->D_s;
   {  // kernel launches of one matvec (run_matvec): permute, P2P kinds, far chain, combine
     int nl = 2 + ((flags & HFMM_ATOMIC_NEAR) ? 0 : 1), n4 = 0;   // + the partial-sum reduction
-    for (int k = 0; k < 3; ++k) nl += p->p2p_nitems[k] > 0 ? 1 : 0;
+    for (int k = 0; k < 3; ++k) {   // one launch per kind and (mixed tiles) tile class
+      const int64_t c4 = p->p2p_mix ? p->p2p_n4[k] : p->p2p_nitems[k];
+      nl += (c4 > 0 ? 1 : 0) + (p->p2p_nitems[k] > c4 ? 1 : 0);
+    }
     if (p->L_f >= 2) {
       for (int l = p->D_s; l > 2; --l) {          // M2M: rows + cols pass per level (or one pass)
         const LevelDev &C = p->lv[l], &P = p->lv[l - 1];
@@ -1109,6 +1165,9 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     in.p2p_tile = P2P_TPB_HOST * p->p2p_pt;
     in.p2p_rowskip = p->p2p_rowskip ? 1 : 0;
     in.p2p_dead_frac = p->p2p_dead_frac;
+    in.p2p_mixed_items = 0;
+    if (p->p2p_mix)
+      for (int k = 0; k < 3; ++k) in.p2p_mixed_items += p->p2p_nitems[k] - p->p2p_n4[k];
     in.next4_passes = n4;
   }
   in.owned_points = p->own_pt1 - p->own_pt0;
@@ -1190,10 +1249,26 @@ static int run_up(hfmm_plan *p, const double2 *q_dev, cudaStream_t s_user, bool 
   {
     NvtxRange nv("hfmm:P2P");
     PointsU pu{p->ux, p->uy, p->uz, p->q_sorted};
-    for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD})
-      launch_p2p_items(pu, p->p2p_items[k], p->p2p_nitems[k], (k == P2P_DIAG && HFMM_P2P_DSYM) ? P2P_DSYM : k,
-                       p->uscale, p->dummy_t, p->dummy_s, p->y_near, p->stream2, p->p2p_pt,
-                       det ? p->p2p_part : nullptr, det ? p->p2p_slot[k] : nullptr, p->p2p_rowskip);
+    // mixed tiles: the <= 384-point class (3 targets per thread) on its own stream next to the
+    // 512-point class when the partial sums go to per-item slots (det); behind it with atomics
+    // (y_near is zeroed on stream2)
+    const bool mix3 = p->p2p_mix && det && !serial;
+    cudaStream_t s3 = mix3 ? p->stream3 : p->stream2;
+    if (mix3) CK(cudaStreamWaitEvent(s3, p->ev_fork, 0));
+    for (int k : {P2P_SYM, P2P_DIAG, P2P_ORD}) {
+      const int kind = (k == P2P_DIAG && HFMM_P2P_DSYM) ? P2P_DSYM : k;
+      const int64_t n4 = p->p2p_mix ? p->p2p_n4[k] : p->p2p_nitems[k];
+      launch_p2p_items(pu, p->p2p_items[k], n4, kind, p->uscale, p->dummy_t, p->dummy_s, p->y_near, p->stream2,
+                       p->p2p_pt, det ? p->p2p_part : nullptr, det ? p->p2p_slot[k] : nullptr, p->p2p_rowskip);
+      if (p->p2p_nitems[k] > n4)
+        launch_p2p_items(pu, p->p2p_items[k] + 4 * n4, p->p2p_nitems[k] - n4, kind, p->uscale, p->dummy_t,
+                         p->dummy_s, p->y_near, s3, 3, det ? p->p2p_part : nullptr,
+                         det ? p->p2p_slot[k] + 2 * n4 : nullptr, false);
+    }
+    if (mix3) {
+      CK(cudaEventRecord(p->ev_mix, s3));
+      CK(cudaStreamWaitEvent(p->stream2, p->ev_mix, 0));
+    }
     if (det) launch_p2p_reduce(p->p2p_part, p->p2p_rp, p->p2p_idx, n, p->y_near, p->stream2);
   }
   if (prof) cudaEventRecord(p->sev[8], p->stream2);
@@ -1624,6 +1699,8 @@ extern "C" void hfmm_destroy(hfmm_plan *p) {
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->ev_join_hi) cudaEventDestroy(p->ev_join_hi);
+  if (p->ev_mix) cudaEventDestroy(p->ev_mix);
+  if (p->stream3) cudaStreamDestroy(p->stream3);
   if (p->ev_up) cudaEventDestroy(p->ev_up);
   if (p->vg && p->rank < (int)p->vg->plans.size() && p->vg->plans[p->rank] == p) p->vg->plans[p->rank] = nullptr;
   if (p->stream_hi) cudaStreamDestroy(p->stream_hi);

@@ -60,10 +60,17 @@ __device__ __forceinline__ double2 cexpi_u(double u, const double2 *__restrict__
 // e^{i h a b} for a phase given as a product a b (P2P: r^2 * (1/r)): the rounding to the nearest
 // step comes straight from the exact product, k = round(a b) = fma(a, b, 1.5 * 2^52) - 1.5 * 2^52,
 // and the remainder r = fma(a, b, -k) is rounded once -- one DMUL fewer than forming a b first.
+#ifndef HFMM_P2P_I2F
+#define HFMM_P2P_I2F 0   // A/B negative: C4 63.28 vs 62.99 ms (profiles/r02/mix_ab.txt)
+#endif
 __device__ __forceinline__ double2 cexpi_prod(double a, double b, const double2 *__restrict__ tab) {
   const double t = fma(a, b, kMagic);
   const int k = __double2loint(t);
+#if HFMM_P2P_I2F   // A/B: k back to double on the conversion unit instead of a DADD on the FP64 pipe
+  const double r = fma(a, b, -__int2double_rn(k));
+#else
   const double r = fma(a, b, -(t - kMagic));
+#endif
   const double r2 = r * r;
   const double s = sin_poly(r, r2);
   const double c = fma(r2, fma(r2, kC4, kC2), 1.0);
@@ -80,6 +87,9 @@ __device__ __forceinline__ double2 cexpi_prod(double a, double b, const double2 
 #endif
 #ifndef HFMM_RSQ_FORM
 #define HFMM_RSQ_FORM 1
+#endif
+#ifndef HFMM_P2P_UNROLL
+#define HFMM_P2P_UNROLL 4   // 4 vs 2: C4 62.86 vs 62.99 ms, C5 719.7 vs 722.8 (profiles/r02/mix_ab.txt)
 #endif
 __device__ __forceinline__ double rsqrt_fast(double r2) {
   double y;
@@ -109,6 +119,7 @@ __device__ __forceinline__ double rsqrt_fast(double r2) {
 //             registers) and G q_i to y_j (columns: systolic warp reduction, below)
 // ---------------------------------------------------------------------------------------------
 constexpr int P2P_TPB = P2P_THREADS;
+constexpr int kP2PUnroll = HFMM_P2P_UNROLL;   // source steps unrolled in the symmetric loops (A/B)
 // PT = targets per thread (tile = PT * P2P_TPB), MINB = resident CTAs per SM asked of ptxas;
 // instantiated as (8, 1), (4, HFMM_P2P_MINB) and (3, 4) -- the plan picks one per matvec (hfmm.cu)
 
@@ -202,7 +213,7 @@ __device__ __forceinline__ void p2p_sym_block(const double (&tx)[PT], const doub
                                               const double2 *sq, const double2 *tab, int lane, int warp,
                                               int base, int sb, double &cr_out, double &ci_out) {
   double cr = 0.0, ci = 0.0;
-#pragma unroll 2
+#pragma unroll kP2PUnroll
   for (int u = 0; u < 32; ++u) {
     const int s = base + ((lane + u) & 31);
     const double xs = sx[s], ys = sy[s], zs = sz[s];
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(P2P_TPB, MINB) p2p_sym_kernel(PointsU pts,
                   // loop below instead: C4 68.1 vs 67.1 ms with skipping on, profiles/r02/rowskip_ab2.txt)
         p2p_sym_dispatch<DS, PT, PT>(np_w, tx, ty, tz, tq, ar, ai, sx, sy, sz, sq, tab, lane, warp, base, sb, cr, ci);
       } else {  // all PT rows (the full-tile loop, inline)
-#pragma unroll 2
+#pragma unroll kP2PUnroll
         for (int u = 0; u < 32; ++u) {
           const int s = base + ((lane + u) & 31);
           const double xs = sx[s], ys = sy[s], zs = sz[s];

@@ -405,6 +405,49 @@ def test_deterministic_near_field(hf, case):
     assert rel(y1.cpu().numpy(), yo) <= PARITY and rel(y0.cpu().numpy(), yo) <= PARITY
 
 
+# ---- Mixed P2P tiles: 512- and <= 384-point target tiles of one leaf ----------------
+_MIX_ORACLE = {}
+
+
+@pytest.mark.parametrize("case", ["leaves", "nofar"])
+@pytest.mark.parametrize("near", ["det", "atomic"])
+def test_p2p_mixed_tiles(hf, case, near, monkeypatch):
+    """The mixed-tile plan (each leaf cut into full 512-point tiles plus <= 384-point tiles, one
+    launch per class on two streams; forced on these short grids with HFMM_P2P_MIX=2) gives the
+    oracle's matvec and the one-tile-size plan's.  "leaves": level-2 leaves of ~400-570 points
+    (one 512-slot tile up to 512 points, two <= 384-point tiles above: both classes, symmetric items
+    across them); "nofar": all pairs at the root (2,400 points: four 512-point tiles and one of 352)."""
+    if case == "nofar":
+        cfg = small_config("p2p_mix_nofar", n=2400, kappa=2 * math.pi, depth=3, eps=1e-4, seed=37)
+    else:
+        cfg = small_config("p2p_mix_leaves", n=24000, kappa=16 * math.pi, depth=2, eps=1e-6, seed=37)
+    x, q = points_and_charges(cfg)
+    flags = hf.HFMM_ATOMIC_NEAR if near == "atomic" else 0
+    monkeypatch.setenv("HFMM_P2P_MIX", "2")
+    g = gpu_plan(hf, cfg, x, flags=flags)
+    monkeypatch.setenv("HFMM_P2P_MIX", "0")
+    g0 = gpu_plan(hf, cfg, x, flags=flags)
+    monkeypatch.delenv("HFMM_P2P_MIX")
+    info, info0 = g.info(), g0.info()
+    assert info["p2p_mixed_items"] > 0 and info0["p2p_mixed_items"] == 0
+    assert info["p2p_tile"] == 512 and not info["p2p_rowskip"]
+    assert info["p2p_pairs"] == info0["p2p_pairs"] and info["p2p_sym_pairs"] == info0["p2p_sym_pairs"]
+    assert info["p2p_dead_frac"] < info0["p2p_dead_frac"] or info0["p2p_rowskip"]
+    y, y0 = g.matvec(q), g0.matvec(q)
+    assert rel(y, y0) <= 1e-13
+    if near == "det":
+        assert np.array_equal(y, g.matvec(q))   # per-item slots, fixed-order sum: bitwise repeatable
+    if case == "nofar":
+        assert (info["L_f"] or 0) < 2
+        assert rel(y, direct_sum(x, q, cfg.kappa)) <= PARITY
+    else:
+        assert info["L_f"] == 2
+        if "yo" not in _MIX_ORACLE:   # one oracle matvec for both accumulation flavours
+            plan = make_plan(cfg.kappa, cfg.eps, cfg.size, cfg.depth, cfg.alpha, source_level=info["source_level"])
+            _MIX_ORACLE["yo"] = OracleFMM(x, cfg.lo, cfg.size, plan).matvec(q)
+        assert rel(y, _MIX_ORACLE["yo"]) <= PARITY
+
+
 # ---- P2P tile per plan (DESIGN.md 6.1): 384 / 512 / 1,024-point target tiles -------------------
 @pytest.mark.parametrize("rowskip", ["on", "off"])
 @pytest.mark.parametrize("pt", [3, 4, 8])
