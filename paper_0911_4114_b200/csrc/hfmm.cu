@@ -845,7 +845,8 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
     int64_t pairs = 0, sym_pairs = 0;
     int64_t tile = (int64_t)P2P_TPB_HOST * 4;   // targets per item: 128 threads x PT targets
     bool mix_tiles = false;
-    const double kMix3Cost = 1.08;   // per-slot cost of the 384-point kernel relative to the 512-point one
+    // per-slot cost of the 384-point kernel relative to the 512-point one (HFMM_P2P_MIX3COST: A/B)
+    const double kMix3Cost = getenv("HFMM_P2P_MIX3COST") ? atof(getenv("HFMM_P2P_MIX3COST")) : 1.08;
     auto add = [&](int kind, int64_t t0, int64_t t1, int64_t s0, int64_t s1) {
       if (t1 <= t0 || s1 <= s0) return;
       it[kind].insert(it[kind].end(), {t0, t1, s0, s1});
@@ -1007,9 +1008,17 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       auto cost = [&](int64_t i) { return (it[k][4 * i + 1] - it[k][4 * i]) * (it[k][4 * i + 3] - it[k][4 * i + 2]); };
       // mixed tiles: the 512-point class first (one launch per class), longest first inside a class
       auto small = [&](int64_t i) { return p->p2p_mix && it[k][4 * i + 1] - it[k][4 * i] <= 3 * (int64_t)P2P_TPB_HOST; };
+      // run time of an item: every thread of the tile evaluates its PT targets, live or not, so
+      // (without row skipping) a launch's items are ordered by their source count alone -- a
+      // partly filled last tile runs as long as a full one (HFMM_P2P_SORT=0: by live pairs)
+      static const bool by_slots = !(getenv("HFMM_P2P_SORT") && atoi(getenv("HFMM_P2P_SORT")) == 0);
+      auto key = [&](int64_t i) {
+        if (!by_slots || p->p2p_rowskip || k == P2P_DIAG) return cost(i);
+        return it[k][4 * i + 3] - it[k][4 * i + 2];
+      };
       std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
         if (small(x) != small(y)) return small(y);
-        return cost(x) > cost(y);
+        return key(x) > key(y);
       });
       p->p2p_n4[k] = m;
       if (p->p2p_mix) {
