@@ -590,13 +590,14 @@ def main():
     p2p_flops = P2P_FLOPS_PER_EVAL * evals + P2P_FLOPS_PER_MAC * pairs
     peak_tflops = 2 * 64 * 148 * (clocks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
     achieved = p2p_flops / (p2p_ms * 1e-3) / 1e12
-    traffic = None
+    traffic = traffic_scope = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(cfg.name, {}).get("p2p")
+            tj = json.load(open(tpath)).get(cfg.name, {})
+            traffic, traffic_scope = tj.get("p2p"), tj.get("p2p_scope")
         except Exception:
-            traffic = None
+            traffic = traffic_scope = None
     L_f = info["L_f"]
     launches = info["launches"]                  # counted by libhfmm for one matvec (hfmm_info.launches)
     line = {
@@ -611,7 +612,7 @@ def main():
                         "(all-gather of the owned sorted ranges) and the D2H inside the timed region"},
         "gpu_launches": launches,
         "roofline": {"kernel": "p2p", "bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tflops, "traffic": traffic,
+                     "frac": achieved / peak_tflops, "traffic": traffic, "traffic_scope": traffic_scope,
                      "peak_source": "derived: 64 FP64 FMA/clk/SM x 148 SMs x 2 x sm_max_mhz (DESIGN.md)",
                      "per_unit": f"{P2P_FLOPS_PER_EVAL} FP64 flops per kernel evaluation + "
                                  f"{P2P_FLOPS_PER_MAC} per ordered pair (MAC)",
