@@ -1008,13 +1008,17 @@ extern "C" int hfmm_precompute(hfmm_plan *p, double kappa, double eps, double al
       auto cost = [&](int64_t i) { return (it[k][4 * i + 1] - it[k][4 * i]) * (it[k][4 * i + 3] - it[k][4 * i + 2]); };
       // mixed tiles: the 512-point class first (one launch per class), longest first inside a class
       auto small = [&](int64_t i) { return p->p2p_mix && it[k][4 * i + 1] - it[k][4 * i] <= 3 * (int64_t)P2P_TPB_HOST; };
-      // run time of an item: every thread of the tile evaluates its PT targets, live or not, so
-      // (without row skipping) a launch's items are ordered by their source count alone -- a
-      // partly filled last tile runs as long as a full one (HFMM_P2P_SORT=0: by live pairs)
-      static const bool by_slots = !(getenv("HFMM_P2P_SORT") && atoi(getenv("HFMM_P2P_SORT")) == 0);
+      // run time of an item: every thread of the tile evaluates its PT targets, live or not (with
+      // row skipping: its live 128-target rows), so a launch's items are ordered by their source
+      // count (x live rows) -- a partly filled last tile runs as long as a full one
+      // (HFMM_P2P_SORT=0: by live pairs)
+      const bool by_slots = !(getenv("HFMM_P2P_SORT") && atoi(getenv("HFMM_P2P_SORT")) == 0);
       auto key = [&](int64_t i) {
-        if (!by_slots || p->p2p_rowskip || k == P2P_DIAG) return cost(i);
-        return it[k][4 * i + 3] - it[k][4 * i + 2];
+        if (!by_slots || k == P2P_DIAG) return cost(i);
+        const int64_t ns = it[k][4 * i + 3] - it[k][4 * i + 2];
+        // row skipping: the item runs for the live 128-target rows of its first warp
+        if (p->p2p_rowskip) return (it[k][4 * i + 1] - it[k][4 * i] + P2P_TPB_HOST - 1) / P2P_TPB_HOST * ns;
+        return ns;
       };
       std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
         if (small(x) != small(y)) return small(y);

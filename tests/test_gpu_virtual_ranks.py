@@ -162,3 +162,25 @@ def test_virtual_ranks_halo_default_levels(hf, R, monkeypatch):
         assert not by[2]["halo"] and not by[3]["halo"] and by[4]["halo"]
         # the level-4 halo is a fraction of the all-gather volume
         assert by[4]["m_recv_boxes"] < 0.75 * nbox4, by[4]
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_virtual_ranks_mixed_p2p_tiles(hf, R, monkeypatch):
+    """Mixed P2P tiles (512- and <= 384-point target tiles of one leaf, one launch per class on two
+    streams; forced on this short grid with HFMM_P2P_MIX=2) under the rank split: the ordered items
+    against neighbour leaves owned by a peer are cut into the same two classes, the ranks' P2P
+    pairs partition the single plan's, and every rank's y equals the single (mixed) plan's to 1e-13
+    (that plan == the oracle: test_gpu_parity.py::test_p2p_mixed_tiles)."""
+    import torch
+    monkeypatch.setenv("HFMM_P2P_MIX", "2")
+    cfg = small_config("vr_mix", n=24000, kappa=16 * math.pi, depth=2, eps=1e-6, seed=37)
+    x, q = points_and_charges(cfg)
+    g1 = plan_for(hf, cfg, x, "lf")
+    assert g1.info()["p2p_mixed_items"] > 0 and g1.info()["L_f"] == 2
+    qd = torch.from_numpy(q).cuda()
+    y1 = g1.matvec(qd).cpu().numpy()
+    pairs1 = g1.info()["p2p_pairs"]
+    g1.close()
+    infos = _check_group(hf, cfg, "lf", R, y1, qd)
+    assert sum(i["p2p_pairs"] for i in infos) == pairs1
+    assert all(i["p2p_mixed_items"] > 0 for i in infos)
